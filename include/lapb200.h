@@ -1,0 +1,227 @@
+/*
+ * lapb200.h -- C ABI of the B200-native Laplacian-eigensolver hot path.
+ *
+ * The reference package (lapeig 0.1.0, /root/reference/pkg/src/lapeig) is
+ * pure Python; its "plugin" seams are duck-typed Python functions.  Every
+ * entry point below replaces one of those seams and is what a ctypes / cffi
+ * binding in the reference would call:
+ *
+ *   lg_csr_create / lg_spmv*      <- sparse.py:26-139   (CsrMatrix, spmv)
+ *   lg_build_laplacian            <- graphs.py:250-263  (build_laplacian)
+ *   lg_ic0_factorize              <- ic0.py:48-116      (_attempt, ic0_factorize)
+ *   lg_ic0_create / lg_ic0_apply  <- ic0.py:24-45,139-150 (Ic0Factor.apply)
+ *   lg_fused                      <- pcg.py:55-60 (DeflationBasis.project_out),
+ *                                    kernels.py:22-55 (Gram-Schmidt sweeps),
+ *                                    dacg.py:36-96 / pcg.py:131-155 (dots, axpys)
+ *   lg_gemm_small                 <- jd.py:67-73,89-90; irlm.py:166,192 (V @ y)
+ *   lg_scalar                     <- the scalar recurrences of dacg.py:188-233,
+ *                                    pcg.py:133-155 executed on the device
+ *
+ * Conventions
+ *   - every function returns 0 on success and a negative LG_E* code on error;
+ *     lg_last_error() returns a thread-local message for the last failure.
+ *   - pointers named *_h are host pointers; every other double* / int* is a
+ *     device pointer owned by the caller (torch tensors in the Python layer).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *   - handles (lg_csr, lg_ic0) are immutable after creation and may be used
+ *     concurrently from several streams; lg_ws (reduction workspace) must be
+ *     used by one stream at a time.
+ *   - all reductions are deterministic (fixed partition + fixed tree order,
+ *     no floating-point atomics): identical inputs give bitwise identical
+ *     outputs run to run.
+ */
+#ifndef LAPB200_H
+#define LAPB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LG_OK 0
+#define LG_EINVAL -1      /* bad argument (maps to ValueError)              */
+#define LG_ECUDA -2       /* CUDA runtime failure (maps to RuntimeError)    */
+#define LG_ENOMEM -3      /* allocation failure                             */
+#define LG_EBREAKDOWN -4  /* IC(0) pivot breakdown at every shift (Ic0Error) */
+
+/* ---- library / device -------------------------------------------------- */
+const char* lg_last_error(void);
+int lg_version(void);                        /* 100 * major + minor        */
+int lg_device_info(int* sm_count, int* l2_bytes, int* cc_major, int* cc_minor);
+/* async D2H copy of `bytes` into pinned host memory followed by a stream
+ * synchronisation: the single host<->device round trip a solver iteration
+ * pays for its convergence test. */
+int lg_readback(const void* dev, void* host_pinned, int64_t bytes, void* stream);
+int lg_upload(void* dev, const void* host, int64_t bytes, void* stream);
+
+/* ---- reduction workspace ---------------------------------------------- */
+typedef struct lg_ws lg_ws;
+int lg_ws_create(lg_ws** out);
+int lg_ws_destroy(lg_ws* ws);
+
+/* ---- CSR matrix + SpMV (sparse.py:26-139) ------------------------------ */
+typedef struct lg_csr lg_csr;
+/* Upload an n x n CSR (int64 row_ptr, int64 col, f64 val as held by the
+ * reference CsrMatrix, sparse.py:39-41).  Columns are stored as int32 when
+ * n < 2^31.  Builds the nnz-balanced row-block schedule and, when the
+ * off-diagonal values take few distinct values, the packed value table.
+ * flags: bit0 = disable packed-value format. */
+int lg_csr_create(int64_t n, int64_t nnz, const int64_t* row_ptr_h,
+                  const int64_t* col_h, const double* val_h, int flags,
+                  lg_csr** out);
+int lg_csr_destroy(lg_csr* a);
+/* n, nnz, number of row blocks, long rows, packed format flag, and the
+ * bytes one SpMV streams from HBM under the stored format. */
+int lg_csr_info(const lg_csr* a, int64_t* n, int64_t* nnz, int64_t* nblocks,
+                int64_t* nlong, int* packed, int64_t* stream_bytes);
+/* Read the device arrays back (row_ptr, col, val in the canonical layout):
+ * the byte-identity check of an upload. */
+int lg_csr_download(const lg_csr* a, int64_t* row_ptr_h, int64_t* col_h,
+                    double* val_h);
+
+/* y = A x - theta x, with theta = theta_h (+ *theta_d when theta_d != NULL,
+ * sign flipped when theta_neg).  Optional fused epilogue dot products of the
+ * freshly computed y:
+ *   out[0:ndots]          = y . dvec[d]           (dvec[d] == NULL -> y . y)
+ *   out[ndots:ndots+nq]   = Q^T y                 (Q column-major, ld ldq)
+ * out may be NULL when ndots == nq == 0.  skip (device int*) != NULL and
+ * *skip != 0 turns the launch into a no-op (device-side predication used by
+ * speculative solver iterations). */
+int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
+            const double* theta_d, int theta_neg, int ndots,
+            const double* const* dvec, const double* q, int64_t ldq, int nq,
+            double* out, lg_ws* ws, const int* skip, void* stream);
+/* End-to-end call through host buffers: H2D of x, SpMV, D2H of y. */
+int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h,
+                 double* x_dev_scratch, double* y_dev_scratch, void* stream);
+/* Batched SpMM: Y[:, j] = A X[:, j] for j < k (column-major, ld = n). */
+int lg_spmm(const lg_csr* a, const double* x, double* y, int k, void* stream);
+
+/* ---- Laplacian assembly (graphs.py:250-263), bit-exact ----------------- */
+/* Canonical edge list (i < j, lexicographically sorted, w > 0) -> CSR of
+ * L = D - A with explicit diagonal.  Degrees are summed in the reference's
+ * order (graphs.py:257-258: upper-row weights ascending, then lower-row
+ * weights ascending, from 0.0).  Runs on the device; results copied to the
+ * host arrays (row_ptr_h[n+1], col_h[n+2m], val_h[n+2m]). */
+int lg_build_laplacian(int64_t n, int64_t m, const int64_t* i_h,
+                       const int64_t* j_h, const double* w_h,
+                       int64_t* row_ptr_h, int64_t* col_h, double* val_h);
+
+/* ---- IC(0) factorization (ic0.py:48-116), host, bit-exact -------------- */
+/* Factor A + alpha diag(A) on the lower pattern of A, trying shift0 and then
+ * every schedule entry > shift0, then 0.1 * max diag (ic0.py:98-111).
+ * Subtractions run in ascending column order as in ic0.py:56-71 and the
+ * file is compiled with -ffp-contract=off, so the factor equals the
+ * reference's bit for bit.  On success fills the lower-triangular factor
+ * (row_ptr_h[n+1], col_h, val_h with capacity = nnz of the lower part of A,
+ * diagonal last in each row), *shift and *attempts.  LG_EBREAKDOWN when all
+ * shifts fail. */
+int lg_ic0_factorize(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
+                     const double* val_h, double shift0, const double* sched_h,
+                     int nsched, int64_t* l_row_ptr_h, int64_t* l_col_h,
+                     double* l_val_h, double* shift, int* attempts);
+
+/* ---- IC(0) apply (ic0.py:40-45) ---------------------------------------- */
+typedef struct lg_ic0 lg_ic0;
+/* Upload the lower factor L (CSR, diagonal last in each row) and build L^T
+ * for the backward sweep. */
+int lg_ic0_create(int64_t n, const int64_t* l_row_ptr_h, const int64_t* l_col_h,
+                  const double* l_val_h, lg_ic0** out);
+int lg_ic0_destroy(lg_ic0* f);
+int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels);
+/* z = (L L^T)^{-1} r: sync-free forward sweep on L then backward sweep on
+ * L^T, one cooperative persistent kernel each.  The forward result lives in
+ * scratch owned by the handle, so applies of one handle must be ordered on
+ * one stream.  z may alias r. */
+int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
+                 void* stream);
+/* Jacobi (diagonal) apply z = r / diag, a flagged non-reference variant. */
+int lg_diag_apply(int64_t n, const double* dinv, const double* r, double* z,
+                  const int* skip, void* stream);
+
+/* ---- fused vector pass -------------------------------------------------- */
+#define LG_MAXT 4   /* linear-combination terms per output          */
+#define LG_MAXD 8   /* explicit dot pairs                           */
+#define LG_MAXB 2   /* column blocks for Q^T v dots                 */
+#define LG_MAXO 3   /* outputs per pass                             */
+#define LG_MAXQ 64  /* total block columns per launch               */
+/* sentinel vector pointers naming the outputs of the same pass */
+#define LG_OUT0 ((const double*)(uintptr_t)1)
+#define LG_OUT1 ((const double*)(uintptr_t)2)
+#define LG_OUT2 ((const double*)(uintptr_t)3)
+
+typedef struct {
+  const double* v;     /* input vector (may be LG_OUT0 for out1 terms)   */
+  double h;            /* host scale                                      */
+  const double* d;     /* device scalar multiplier or NULL                */
+} lg_term;
+
+typedef struct {
+  double* out;         /* NULL: output disabled                            */
+  int nterms;
+  lg_term t[LG_MAXT];
+  /* optional block update: out -= sum_j (cscale * c[j]) Q[:, j]          */
+  const double* uq;
+  int64_t uld;
+  int uk;
+  const double* uc;    /* device coefficients (k of them)                  */
+  double cscale;
+  /* optional final scaling by a device scalar p = *d_post:
+   * post_mode 1: out *= p, 2: out /= p, 3: out /= sqrt(p)               */
+  const double* d_post;
+  int post_mode;
+} lg_output;
+
+typedef struct {
+  const double* q;     /* column-major block, ld                          */
+  int64_t ld;
+  int k;
+  const double* v;     /* vector dotted against every column (or LG_OUTx) */
+} lg_block;
+
+typedef struct {
+  int64_t n;
+  lg_output o[LG_MAXO];
+  int ndots;
+  /* dot d = (da[d] - dc[d]) . db[d]; dc NULL = 0; db NULL = same as the
+   * first operand.  Any operand may name an output (LG_OUTx). */
+  const double* da[LG_MAXD];
+  const double* db[LG_MAXD];
+  const double* dc[LG_MAXD];
+  int nblocks;
+  lg_block b[LG_MAXB];
+  double* result;              /* device: [ndots + sum(b.k)]              */
+  const int* skip;
+} lg_fused_args;
+
+/* One streaming pass over n rows: up to three outputs, each a linear
+ * combination of up to four vectors (inputs or earlier outputs) minus a
+ * block combination Q c, optionally rescaled by a device scalar, plus
+ * deterministic dot products / Q^T v block dots of inputs and outputs. */
+int lg_fused(const lg_fused_args* args, lg_ws* ws, void* stream);
+
+/* Out[:, 0:p] = In[:, 0:m] * Y  (Y is m x p column-major, host, copied by
+ * value into the launch; m <= 64, p <= 32; In/Out column-major ld = n). */
+int lg_gemm_small(int64_t n, const double* in, int64_t ldi, int m,
+                  const double* y_h, int p, double* out, int64_t ldo,
+                  void* stream);
+
+/* ---- device scalar programs -------------------------------------------- */
+/* The scalar recurrences of the solvers (PR-beta, the 2x2 plane pencil, PCG
+ * gamma/beta, convergence and breakdown tests: dacg.py:188-233,
+ * pcg.py:133-155) run on the device so an iteration needs no host round trip
+ * until its status is read.  A program is a list of 4-byte instructions
+ * {op, dst, a, b} over a slot file s[0..255] (device doubles) and an int flag
+ * file (device ints, the `skip` predicates of the kernels).  Opcodes are
+ * enumerated in csrc/lg_scalar.cu (LG_OP_*); imm_h supplies constants. */
+#define LG_MAXOPS 192
+#define LG_MAXIMM 32
+int lg_scalar_prog(double* s, int* flags, const uint8_t* prog_h, int nops,
+                   const double* imm_h, int nimm, const int* skip,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAPB200_H */

@@ -1,0 +1,130 @@
+"""Device plumbing: CUDA availability, streams, workspaces, vector buffers.
+
+PyTorch provides device memory (the caching allocator), pinned host memory
+and the current stream; every computation is a liblapb200 kernel.  Vectors on
+the device are 1-D float64 torch tensors; column blocks (deflation bases,
+search spaces) are 2-D tensors of shape (k, n), i.e. column-major n x k with
+leading dimension n, so a column is a contiguous row of the tensor.
+"""
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _native as nat
+
+_state = threading.local()
+_checked = False
+
+
+def torch():
+    import torch as _t
+    return _t
+
+
+def require_cuda():
+    """Fail loudly when no CUDA device is present (no CPU fallback)."""
+    global _checked
+    if _checked:
+        return
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError(
+            "paper_1311_1695_b200 needs a CUDA device (B200 / sm_100a); "
+            "there is no CPU fallback")
+    nat.load()
+    _checked = True
+
+
+def device():
+    require_cuda()
+    return torch().device("cuda", torch().cuda.current_device())
+
+
+def stream_ptr():
+    """cudaStream_t of torch's current stream (as an int for ctypes)."""
+    return torch().cuda.current_stream().cuda_stream
+
+
+class Workspace:
+    """An lg_ws handle (deterministic-reduction scratch) bound to a stream."""
+
+    def __init__(self):
+        require_cuda()
+        h = ctypes.c_void_p()
+        nat.call("lg_ws_create", ctypes.byref(h))
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and h.value and nat._lib is not None:
+            nat._lib.lg_ws_destroy(h)
+
+
+def workspace():
+    """The workspace of the current stream (one per stream per thread)."""
+    cache = getattr(_state, "ws", None)
+    if cache is None:
+        cache = _state.ws = {}
+    s = stream_ptr()
+    ws = cache.get(s)
+    if ws is None:
+        ws = cache[s] = Workspace()
+    return ws
+
+
+def empty(n, dtype=None):
+    t = torch()
+    return t.empty(n, dtype=dtype or t.float64, device=device())
+
+
+def zeros(n, dtype=None):
+    t = torch()
+    return t.zeros(n, dtype=dtype or t.float64, device=device())
+
+
+def is_device_array(x):
+    t = torch()
+    return isinstance(x, t.Tensor) and x.is_cuda
+
+
+def to_device(x):
+    """float64 contiguous device tensor from numpy / torch input."""
+    t = torch()
+    if isinstance(x, t.Tensor):
+        x = x.to(device=device(), dtype=t.float64)
+        return x.contiguous()
+    arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    return t.from_numpy(arr).to(device())
+
+
+def to_host(x):
+    t = torch()
+    if isinstance(x, t.Tensor):
+        return x.detach().cpu().numpy()
+    return np.asarray(x, dtype=np.float64)
+
+
+def ptr(x):
+    return x.data_ptr() if x is not None else None
+
+
+class Pinned:
+    """Pinned host mirror of a small device array (status readbacks)."""
+
+    def __init__(self, dev_tensor):
+        t = torch()
+        self.dev = dev_tensor
+        self.host = t.empty(dev_tensor.shape, dtype=dev_tensor.dtype, pin_memory=True)
+        self.np = self.host.numpy()
+        self.nbytes = dev_tensor.numel() * dev_tensor.element_size()
+
+    def fetch(self, stream=None):
+        nat.call("lg_readback", self.dev.data_ptr(), self.host.data_ptr(),
+                 self.nbytes, stream if stream is not None else stream_ptr())
+        return self.np
+
+    def push(self, stream=None):
+        nat.call("lg_upload", self.dev.data_ptr(), self.host.data_ptr(),
+                 self.nbytes, stream if stream is not None else stream_ptr())

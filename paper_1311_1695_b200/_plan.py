@@ -1,0 +1,298 @@
+"""Prebuilt device launches: fused vector passes, scalar programs, SpMV,
+IC(0) apply.
+
+A solver iteration is a fixed sequence of launches whose operands are fixed
+device buffers and whose scalar coefficients live in a device slot file, so
+each launch's argument block is built once (ctypes structs) and replayed;
+the Python cost of an iteration is one ctypes call per launch.
+
+    Slots     named double slots + int flags in device memory
+    Prog      assembler for the device scalar interpreter (csrc/lg_scalar.cu)
+    Fused     one lg_fused pass
+    Spmv      one lg_spmv launch (optionally with epilogue dots)
+    Ic0Apply  one lg_ic0_apply (or Jacobi) launch
+"""
+
+import ctypes
+import struct
+
+import numpy as np
+
+from . import _device as dev
+from . import _native as nat
+
+OPS = {
+    "NOP": 0, "MOV": 1, "IMM": 2, "ADD": 3, "SUB": 4, "MUL": 5, "DIV": 6,
+    "SQRT": 7, "NEG": 8, "HYPOT": 9, "ABS": 10, "MAX": 11, "MIN": 12,
+    "LE": 13, "LT": 14, "EQ": 15, "SEL": 16, "AND": 17, "OR": 18, "NOT": 19,
+    "FLAG": 20, "FLAGOR": 21, "LDFLAG": 22, "HALTIF": 23, "DIVZ": 24,
+    "INC": 25, "RECIP": 26, "NE": 27, "GT": 28, "GE": 29,
+}
+
+
+def _addr(x):
+    """Integer device address of a tensor / sentinel / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+class Slots:
+    """Named scalar slots (device doubles) and flags (device int32)."""
+
+    NSLOT = 256
+    NFLAG = 32
+
+    def __init__(self, names=(), flags=()):
+        t = dev.torch()
+        self.s = dev.zeros(self.NSLOT)
+        self.f = dev.zeros(self.NFLAG, dtype=t.int32)
+        self.idx = {}
+        self.fidx = {}
+        for nm in names:
+            self.add(nm)
+        for nm in flags:
+            self.add_flag(nm)
+        self.pin_s = dev.Pinned(self.s)
+        self.pin_f = dev.Pinned(self.f)
+
+    def add(self, name, count=1):
+        """Allocate `count` consecutive slots under `name` (idempotent)."""
+        if name in self.idx:
+            return self.idx[name]
+        base = getattr(self, "_next", 0)
+        if base + count > self.NSLOT:
+            raise ValueError("scalar slot file exhausted")
+        self.idx[name] = base
+        self._next = base + count
+        return base
+
+    def add_flag(self, name):
+        if name not in self.fidx:
+            if len(self.fidx) >= self.NFLAG:
+                raise ValueError("flag file exhausted")
+            self.fidx[name] = len(self.fidx)
+        return self.fidx[name]
+
+    def p(self, name, off=0):
+        """Device address of slot `name` (+ offset)."""
+        return self.s.data_ptr() + 8 * (self.idx[name] + off)
+
+    def fp(self, name):
+        return self.f.data_ptr() + 4 * self.fidx[name]
+
+    # host access (synchronising)
+    def fetch(self):
+        st = dev.stream_ptr()
+        return self.pin_s.fetch(st), self.pin_f.fetch(st)
+
+    def read(self, *names):
+        s, _ = self.fetch()
+        return [float(s[self.idx[n]]) for n in names]
+
+    def set(self, **values):
+        """Write slots from the host (synchronous small upload)."""
+        for k, v in values.items():
+            self.s[self.idx[k]] = float(v)
+
+    def set_vec(self, name, values):
+        i = self.idx[name]
+        vals = np.asarray(values, dtype=np.float64)
+        self.s[i:i + vals.size] = dev.torch().from_numpy(vals).to(self.s.device)
+
+    def clear_flags(self):
+        self.f.zero_()
+
+    def setflag(self, name, value):
+        self.f[self.fidx[name]] = int(value)
+
+
+class Prog:
+    """Assembler for a device scalar program."""
+
+    def __init__(self, slots, skip=None):
+        self.S = slots
+        self.ops = []
+        self.imm = []
+        self.skip = skip
+        self._built = None
+
+    def _s(self, name):
+        if isinstance(name, int):
+            return name
+        if name not in self.S.idx:
+            self.S.add(name)
+        return self.S.idx[name]
+
+    def emit(self, op, dst=0, a=0, b=0):
+        self.ops.append(OPS[op] | (dst << 8) | (a << 16) | (b << 24))
+        self._built = None
+        return self
+
+    def const(self, dst, value):
+        if len(self.imm) >= nat.LG_MAXIMM:
+            raise ValueError("too many immediates")
+        self.imm.append(float(value))
+        return self.emit("IMM", self._s(dst), len(self.imm) - 1)
+
+    def __getattr__(self, opname):
+        up = opname.upper()
+        if up not in OPS:
+            raise AttributeError(opname)
+
+        def f(dst, a=0, b=0):
+            if up in ("FLAG", "FLAGOR"):
+                return self.emit(up, self.S.fidx[dst], self._s(a))
+            if up == "LDFLAG":
+                return self.emit(up, self._s(dst), self.S.fidx[a])
+            if up == "HALTIF":
+                return self.emit(up, 0, self._s(dst))
+            return self.emit(up, self._s(dst), self._s(a), self._s(b) if b != 0 else 0)
+
+        return f
+
+    def build(self):
+        if len(self.ops) > nat.LG_MAXOPS:
+            raise ValueError("scalar program too long")
+        ops = (ctypes.c_uint32 * max(1, len(self.ops)))(*self.ops)
+        imm = (ctypes.c_double * max(1, len(self.imm)))(*self.imm)
+        skip = self.S.fp(self.skip) if self.skip else None
+        self._built = (self.S.s.data_ptr(), self.S.f.data_ptr(), ctypes.cast(ops, ctypes.c_void_p),
+                       len(self.ops), ctypes.cast(imm, ctypes.c_void_p), len(self.imm), skip,
+                       ops, imm)
+        return self
+
+    def __call__(self, stream=None):
+        if self._built is None:
+            self.build()
+        b = self._built
+        nat.check(nat.load().lg_scalar_prog(b[0], b[1], b[2], b[3], b[4], b[5], b[6],
+                                            stream if stream is not None else dev.stream_ptr()),
+                  "lg_scalar_prog")
+
+
+class Fused:
+    """One fused streaming pass (lg_fused), built once and replayed.
+
+    outs:   list of dicts {out, terms: [(vec, h, dslot)], upd: (Q, k, cptr, cscale),
+                           post: (dptr, mode)}
+    dots:   list of (a, b, c) -> (a - c) . b   (b None: a . a)
+    blocks: list of (Q, k, vec) -> Q[:, :k]^T vec
+    Q is a (kcap, n) tensor (column-major n x kcap) or (address, ld) tuple.
+    """
+
+    def __init__(self, n, outs=(), dots=(), blocks=(), result=None, skip=None):
+        a = nat.FusedArgs()
+        a.n = n
+        self._keep = []
+        for k, o in enumerate(outs):
+            if o is None:
+                continue
+            oa = a.o[k]
+            oa.out = _addr(o["out"])
+            terms = o.get("terms", ())
+            if len(terms) > nat.LG_MAXT:
+                raise ValueError("too many terms")
+            oa.nterms = len(terms)
+            for t, term in enumerate(terms):
+                v, h = term[0], term[1]
+                d = term[2] if len(term) > 2 else None
+                oa.t[t].v = _addr(v)
+                oa.t[t].h = float(h)
+                oa.t[t].d = d
+            upd = o.get("upd")
+            if upd is not None:
+                q, kk, cptr = upd[0], upd[1], upd[2]
+                cs = upd[3] if len(upd) > 3 else 1.0
+                qa, ld = self._qaddr(q)
+                oa.uq, oa.uld, oa.uk, oa.uc, oa.cscale = qa, ld, int(kk), cptr, float(cs)
+            post = o.get("post")
+            if post is not None:
+                oa.d_post, oa.post_mode = post[0], int(post[1])
+        if len(dots) > nat.LG_MAXD:
+            raise ValueError("too many dots")
+        a.ndots = len(dots)
+        for d, dot in enumerate(dots):
+            x = dot[0]
+            y = dot[1] if len(dot) > 1 else None
+            c = dot[2] if len(dot) > 2 else None
+            a.da[d] = _addr(x)
+            a.db[d] = _addr(y)
+            a.dc[d] = _addr(c)
+        a.nblocks = len(blocks)
+        for b, blk in enumerate(blocks):
+            q, kk, v = blk
+            qa, ld = self._qaddr(q)
+            a.b[b].q, a.b[b].ld, a.b[b].k, a.b[b].v = qa, ld, int(kk), _addr(v)
+        a.result = _addr(result)
+        a.skip = skip
+        self.args = a
+        self.argp = ctypes.byref(a)
+        self.nres = len(dots) + sum(int(b[1]) for b in blocks)
+
+    @staticmethod
+    def _qaddr(q):
+        if isinstance(q, tuple):
+            return q[0], q[1]
+        return q.data_ptr(), q.shape[-1]
+
+    def set_k(self, block=None, upd=None):
+        """Change the live column count of a block dot / update (e.g. after a
+        deflation basis grew) without rebuilding."""
+        if block is not None:
+            bi, k = block
+            self.args.b[bi].k = int(k)
+        if upd is not None:
+            oi, k = upd
+            self.args.o[oi].uk = int(k)
+
+    def __call__(self, ws=None, stream=None):
+        ws = ws or dev.workspace()
+        nat.check(nat.load().lg_fused(self.argp, ws.handle,
+                                      stream if stream is not None else dev.stream_ptr()),
+                  "lg_fused")
+
+
+class Spmv:
+    """One lg_spmv launch: y = A x - theta x (+ epilogue dots into result)."""
+
+    def __init__(self, csr, x, y, theta=0.0, theta_d=None, theta_neg=False, dots=(),
+                 q=None, nq=0, result=None, skip=None):
+        self.csr = csr
+        self.h = csr.handle
+        self.x, self.y = _addr(x), _addr(y)
+        self.theta = float(theta)
+        self.theta_d = theta_d
+        self.neg = 1 if theta_neg else 0
+        self.nd = len(dots)
+        self.dv = (ctypes.c_void_p * max(1, len(dots)))(*[_addr(d) for d in dots])
+        if q is not None:
+            self.q, self.ldq = Fused._qaddr(q)
+        else:
+            self.q, self.ldq = None, 0
+        self.nq = int(nq)
+        self.result = _addr(result)
+        self.skip = skip
+
+    def __call__(self, ws=None, stream=None):
+        ws = ws or dev.workspace()
+        nat.check(nat.load().lg_spmv(self.h, self.x, self.y, self.theta, self.theta_d, self.neg,
+                                     self.nd, self.dv, self.q, self.ldq, self.nq, self.result,
+                                     ws.handle, self.skip,
+                                     stream if stream is not None else dev.stream_ptr()),
+                  "lg_spmv")
+
+
+class PrecApply:
+    """z = M^{-1} r for the device preconditioner of an Ic0Factor."""
+
+    def __init__(self, dfac, r, z, skip=None):
+        self.d = dfac
+        self.r, self.z = _addr(r), _addr(z)
+        self.skip = skip
+
+    def __call__(self, ws=None, stream=None):
+        self.d.apply_raw(self.r, self.z, self.skip,
+                         stream if stream is not None else dev.stream_ptr())

@@ -1,0 +1,691 @@
+// lg_ic0.cu -- IC(0) factorization (host, bit-exact) and the device apply.
+//
+// Factorization: ic0.py:48-116.  The reference builds each row i of L as a
+// dict, subtracting sum_p l_ip l_kp over the common pattern for every lower
+// entry k of the row (ic0.py:56-71).  Whichever dict it iterates, the
+// subtraction runs in ascending p, so a sorted-merge restatement with the
+// same operation order (s -= l_ip * l_kp; l_ik = s / l_kk; d = diag*(1+alpha);
+// d -= l_ip^2; l_ii = sqrt(d)) reproduces the factor bit for bit when built
+// without FMA contraction (-ffp-contract=off, see build.py).
+//
+// Apply: ic0.py:40-45 solves L y = r then L^T z = y (SuperLU, natural
+// ordering).  On the GPU each triangular sweep is a dependency DAG: 227
+// levels on C4, 476 on C3, 72 on C2.  A launch per level costs ~2 us x
+// levels and per-row ready flags with spinning lanes saturate L2 with polls
+// (measured: 8 ms per C4 apply), so each sweep is ONE cooperative persistent
+// kernel that walks the levels in order:
+//   * a level's rows are packed into warp tasks -- 32/L rows of one length
+//     class (L = 2, 4, 8 or 32 lanes per row), or a 512-nonzero chunk of a
+//     hub row (C4's largest lower row has 84,860 entries); a hub row's
+//     chunks publish partials and the last chunk to arrive (ticket) sums
+//     them in chunk order, so the result stays deterministic;
+//   * a "wide" level is spread over every warp of the grid and closed by a
+//     grid barrier (one atomic per CTA on a monotonic 64-bit counter);
+//   * a run of "narrow" levels (no more tasks than one CTA has warps) is
+//     executed by CTA 0 alone with __syncthreads between levels -- ~50 ns
+//     instead of a ~1 us grid barrier -- while the other CTAs wait at the
+//     next grid barrier.
+// Per-row summation order is fixed (lane-strided, butterfly), so z is
+// bitwise reproducible.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "lg_common.cuh"
+
+namespace lg {
+
+constexpr int kSweepThreads = 512;          // 16 warps per CTA
+constexpr int kSweepWarps = kSweepThreads / 32;
+constexpr int kHubChunk = 512;              // nonzeros per hub-row chunk task
+
+struct SweepTask {
+  int32_t p;  // pack: first permuted row          | chunk: permuted hub row
+  int32_t b;  // pack: lanes << 8 | count          | chunk: 0
+  int32_t c;  // chunk: chunk index
+  int32_t d;  // chunk: hub-row id
+};
+
+struct SweepSeg {
+  int32_t t0, t1;   // task range
+  int32_t narrow;   // 1: run by CTA 0 alone
+  int32_t barrier;  // 1: a grid barrier follows this segment
+};
+
+// Device data of one sweep direction.  Rows are stored PERMUTED into
+// processing order (level, length class), so a level's nonzeros are one
+// contiguous stream and a task needs one row-pointer load.
+struct SweepDev {
+  int64_t* prp = nullptr;    // permuted strictly-triangular row pointers
+  int32_t* pcol = nullptr;   // columns (original numbering)
+  double* pval = nullptr;
+  int32_t* perm = nullptr;   // permuted position -> original row
+  double* pdiag = nullptr;   // diagonal in permuted order
+  SweepTask* tasks = nullptr;
+  SweepSeg* segs = nullptr;
+  int32_t* hub_first = nullptr;   // first partial slot of each hub row
+  int32_t* hub_nchunk = nullptr;
+  unsigned* hub_ticket = nullptr;
+  double* hub_part = nullptr;
+  unsigned long long* bar = nullptr;
+  int32_t nsegs = 0;
+  int32_t nbar = 0;          // grid barriers per sweep
+  int levels = 0;
+};
+
+}  // namespace lg
+
+struct lg_ic0 {
+  int64_t n = 0, nnz_l = 0;  // nnz_l counts the diagonal
+  lg::SweepDev fwd, bwd;
+  double* diag = nullptr;
+  double* tmp = nullptr;     // forward result
+  int grid = 0;
+};
+
+namespace lg {
+
+// ------------------------------------------------------------ host side --
+// One no-fill factorization pass (ic0.py:48-78).  Returns true on success.
+// lrp/lcol describe the lower pattern of A plus the diagonal (last per row);
+// lval receives the factor.
+#pragma GCC push_options
+#pragma GCC optimize("fp-contract=off")
+static bool ic0_attempt(int64_t n, const std::vector<double>& diag,
+                        const std::vector<int64_t>& lrp,
+                        const std::vector<int64_t>& lcol,
+                        const std::vector<double>& aval, double alpha,
+                        std::vector<double>& lval, std::vector<int64_t>& stamp,
+                        std::vector<int64_t>& pos) {
+  std::fill(stamp.begin(), stamp.end(), (int64_t)-1);
+  const double floor_ = 1e-14;  // _PIVOT_FLOOR, ic0.py:17
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t lo = lrp[i], hi = lrp[i + 1] - 1;  // hi: diagonal slot
+    for (int64_t t = lo; t < hi; ++t) {
+      stamp[lcol[t]] = i;
+      pos[lcol[t]] = t;
+    }
+    for (int64_t t = lo; t < hi; ++t) {
+      const int64_t k = lcol[t];
+      double s = aval[t];
+      const int64_t klo = lrp[k], khi = lrp[k + 1] - 1;  // row k strictly lower
+      const int64_t nli = t - lo, nk = khi - klo;
+      if (nli <= nk) {
+        // iterate the computed prefix of row i (ascending p), look p up in row k
+        int64_t q = klo;
+        for (int64_t u = lo; u < t; ++u) {
+          const int64_t p = lcol[u];
+          // row k columns ascending: advance (galloping is unnecessary here)
+          if (nk > 32) {
+            const int64_t* b = lcol.data() + q;
+            const int64_t* e = lcol.data() + khi;
+            const int64_t* f = std::lower_bound(b, e, p);
+            q = f - lcol.data();
+          } else {
+            while (q < khi && lcol[q] < p) ++q;
+          }
+          if (q < khi && lcol[q] == p) s -= lval[u] * lval[q];
+        }
+      } else {
+        for (int64_t q = klo; q < khi; ++q) {
+          const int64_t p = lcol[q];
+          if (stamp[p] == i && pos[p] < t) s -= lval[pos[p]] * lval[q];
+        }
+      }
+      lval[t] = s / lval[khi];
+    }
+    const double scaled = diag[i] * (1.0 + alpha);
+    double d = scaled;
+    for (int64_t t = lo; t < hi; ++t) d -= lval[t] * lval[t];
+    if (d <= floor_ * std::fabs(scaled) || d <= 0.0) return false;
+    lval[hi] = std::sqrt(d);
+  }
+  return true;
+}
+#pragma GCC pop_options
+
+static int dag_levels(int64_t n, const std::vector<int64_t>& rp,
+                      const std::vector<int32_t>& col, bool forward,
+                      std::vector<int32_t>& level) {
+  level.assign((size_t)n, 0);
+  int maxl = 0;
+  if (forward) {
+    for (int64_t i = 0; i < n; ++i) {
+      int l = 0;
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) l = std::max(l, level[col[k]] + 1);
+      level[i] = l;
+      maxl = std::max(maxl, l);
+    }
+  } else {
+    for (int64_t i = n - 1; i >= 0; --i) {
+      int l = 0;
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) l = std::max(l, level[col[k]] + 1);
+      level[i] = l;
+      maxl = std::max(maxl, l);
+    }
+  }
+  return n ? maxl + 1 : 0;
+}
+
+static int lanes_for(int64_t len) {
+  if (len <= 4) return 2;
+  if (len <= 16) return 4;
+  if (len <= 64) return 8;
+  return 32;  // <= kHubChunk: at most 16 entries per lane in every class
+}
+
+struct SweepHost {
+  std::vector<int32_t> perm;
+  std::vector<int64_t> prp;
+  std::vector<int32_t> pcol;
+  std::vector<double> pval, pdiag;
+  std::vector<SweepTask> tasks;
+  std::vector<SweepSeg> segs;
+  std::vector<int32_t> hub_first, hub_nchunk;
+  int32_t nparts = 0;
+  int32_t nbar = 0;
+  int levels = 0;
+};
+
+// Level schedule of one sweep: rows grouped by DAG level and length class,
+// permuted into that order, packed into warp tasks; levels classified wide /
+// narrow.
+static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
+                        const std::vector<int32_t>& col, const std::vector<double>& val,
+                        const std::vector<double>& diag, bool forward, SweepHost& h) {
+  std::vector<int32_t> level;
+  h.levels = dag_levels(n, rp, col, forward, level);
+  const int nl = h.levels;
+  std::vector<int64_t> lcount((size_t)nl + 1, 0);
+  for (int64_t i = 0; i < n; ++i) lcount[(size_t)level[(size_t)i] + 1]++;
+  for (int l = 0; l < nl; ++l) lcount[(size_t)l + 1] += lcount[(size_t)l];
+  auto cls = [&](int32_t r) {
+    const int64_t len = rp[(size_t)r + 1] - rp[(size_t)r];
+    return len > kHubChunk ? 64 : lanes_for(len);
+  };
+  h.perm.resize((size_t)n);
+  {
+    std::vector<int64_t> fill(lcount.begin(), lcount.end() - 1);
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t i = forward ? k : n - 1 - k;
+      h.perm[(size_t)fill[(size_t)level[(size_t)i]]++] = (int32_t)i;
+    }
+  }
+  for (int l = 0; l < nl; ++l)
+    std::stable_sort(h.perm.begin() + lcount[(size_t)l], h.perm.begin() + lcount[(size_t)l + 1],
+                     [&](int32_t a, int32_t b) { return cls(a) < cls(b); });
+  h.prp.assign((size_t)n + 1, 0);
+  h.pdiag.resize((size_t)n);
+  for (int64_t p = 0; p < n; ++p) {
+    const int32_t r = h.perm[(size_t)p];
+    h.prp[(size_t)p + 1] = h.prp[(size_t)p] + (rp[(size_t)r + 1] - rp[(size_t)r]);
+    h.pdiag[(size_t)p] = diag[(size_t)r];
+  }
+  h.pcol.resize(col.size());
+  h.pval.resize(val.size());
+  for (int64_t p = 0; p < n; ++p) {
+    const int32_t r = h.perm[(size_t)p];
+    std::copy(col.begin() + rp[(size_t)r], col.begin() + rp[(size_t)r + 1],
+              h.pcol.begin() + h.prp[(size_t)p]);
+    std::copy(val.begin() + rp[(size_t)r], val.begin() + rp[(size_t)r + 1],
+              h.pval.begin() + h.prp[(size_t)p]);
+  }
+  for (int l = 0; l < nl; ++l) {
+    const int32_t t0 = (int32_t)h.tasks.size();
+    int64_t t = lcount[(size_t)l];
+    const int64_t te = lcount[(size_t)l + 1];
+    while (t < te) {
+      const int L = cls(h.perm[(size_t)t]);
+      if (L == 64) {  // hub row: chunk tasks
+        const int64_t len = h.prp[(size_t)t + 1] - h.prp[(size_t)t];
+        const int32_t nch = (int32_t)((len + kHubChunk - 1) / kHubChunk);
+        const int32_t hid = (int32_t)h.hub_first.size();
+        h.hub_first.push_back(h.nparts);
+        h.hub_nchunk.push_back(nch);
+        h.nparts += nch;
+        for (int32_t c = 0; c < nch; ++c) h.tasks.push_back({(int32_t)t, 0, c, hid});
+        ++t;
+        continue;
+      }
+      const int cap = 32 / L;
+      int cnt = 1;
+      while (cnt < cap && t + cnt < te && cls(h.perm[(size_t)(t + cnt)]) == L) ++cnt;
+      h.tasks.push_back({(int32_t)t, (L << 8) | cnt, 0, 0});
+      t += cnt;
+    }
+    const int32_t t1 = (int32_t)h.tasks.size();
+    h.segs.push_back({t0, t1, (t1 - t0) <= kSweepWarps ? 1 : 0, 0});
+  }
+  // barriers: after every wide level, and after the last level of a narrow
+  // run that is followed by a wide level.  None after the final segment.
+  h.nbar = 0;
+  for (size_t sg = 0; sg + 1 < h.segs.size(); ++sg) {
+    if (!h.segs[sg].narrow || !h.segs[sg + 1].narrow) {
+      h.segs[sg].barrier = 1;
+      ++h.nbar;
+    }
+  }
+}
+
+// ----------------------------------------------------------- device side --
+struct SweepArgs {
+  const int64_t* prp;
+  const int32_t* pcol;
+  const double* pval;
+  const int32_t* perm;
+  const double* pdiag;
+  const SweepTask* tasks;
+  const SweepSeg* segs;
+  int32_t nsegs;
+  int32_t nbar;
+  const int32_t* hub_first;
+  const int32_t* hub_nchunk;
+  unsigned* hub_ticket;
+  double* hub_part;
+  unsigned long long* bar;
+  const double* b;
+  double* x;
+  const int* skip;
+};
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar,
+                                             unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1ull);
+    while (ld_relaxed_u64(bar) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int kLaneMax = 16;  // entries per lane per task (any class)
+
+// Everything a lane needs for one task that does not depend on the solve:
+// loaded ahead (before the barrier that precedes the task's level), so after
+// the barrier only the x gathers remain on the critical path.
+struct Staged {
+  int32_t col[kLaneMax];
+  double val[kLaneMax];
+  int32_t row;    // original row (pack) / permuted hub row (chunk)
+  int32_t ne;     // entries held by this lane
+  int32_t info;   // task.b (0: hub chunk)
+  int32_t c, d;   // hub chunk index / id
+  double bv, dg;
+};
+
+__device__ __forceinline__ void stage(const SweepArgs& a, int64_t t, int lane, Staged& st) {
+  const SweepTask tk = a.tasks[t];
+  st.info = tk.b;
+  st.ne = 0;
+  int64_t lo, hi;
+  int step;
+  if (tk.b != 0) {
+    const int L = tk.b >> 8, cnt = tk.b & 0xff;
+    const int g = lane / L, li = lane % L;
+    if (g >= cnt) return;
+    const int64_t p = tk.p + g;
+    lo = a.prp[p] + li;
+    hi = a.prp[p + 1];
+    step = L;
+    st.row = a.perm[p];
+    st.bv = a.b[st.row];
+    st.dg = a.pdiag[p];
+  } else {
+    st.row = tk.p;
+    st.c = tk.c;
+    st.d = tk.d;
+    lo = a.prp[tk.p] + (int64_t)tk.c * kHubChunk;
+    hi = min(a.prp[tk.p + 1], lo + kHubChunk);
+    lo += lane;
+    step = 32;
+  }
+#pragma unroll
+  for (int e = 0; e < kLaneMax; ++e) {
+    const int64_t k = lo + (int64_t)e * step;
+    if (k < hi) {
+      st.col[e] = a.pcol[k];
+      st.val[e] = a.pval[k];
+      st.ne = e + 1;
+    }
+  }
+}
+
+__device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int lane) {
+  double s = 0.0;
+#pragma unroll
+  for (int e = 0; e < kLaneMax; ++e)
+    if (e < st.ne) s += st.val[e] * __ldcg(a.x + st.col[e]);
+  if (st.info != 0) {
+    const int L = st.info >> 8, cnt = st.info & 0xff;
+    for (int o = L >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((lane / L) < cnt && (lane % L) == 0) a.x[st.row] = (st.bv - s) / st.dg;
+    return;
+  }
+  // chunk of a hub row
+  s = warp_sum(s);
+  const int32_t first = a.hub_first[st.d], nch = a.hub_nchunk[st.d];
+  unsigned arrived = 0;
+  if (lane == 0) {
+    a.hub_part[first + st.c] = s;
+    __threadfence();
+    arrived = atomicAdd(a.hub_ticket + st.d, 1u);
+  }
+  arrived = __shfl_sync(0xffffffffu, arrived, 0);
+  if (arrived == (unsigned)nch - 1u) {
+    // last chunk: the whole warp sums the partials (lane-strided, then a
+    // fixed butterfly), so the order does not depend on who finished last
+    __threadfence();
+    double t = 0.0;
+    for (int32_t c = lane; c < nch; c += 32) t += __ldcg(a.hub_part + first + c);
+    t = warp_sum(t);
+    if (lane == 0) {
+      a.hub_ticket[st.d] = 0u;
+      const int32_t row = a.perm[st.row];
+      a.x[row] = (a.b[row] - t) / a.pdiag[st.row];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
+  if (a.skip && *a.skip) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t G = gridDim.x;
+  const int64_t gw = (int64_t)blockIdx.x * kSweepWarps + warp;
+  const int64_t W = G * kSweepWarps;
+  // every launch adds exactly nbar * G arrivals; barrier 0 cannot complete
+  // before this CTA arrives, so rounding down recovers this launch's base
+  __shared__ unsigned long long base_sm;
+  if (threadIdx.x == 0) {
+    const unsigned long long per = (unsigned long long)a.nbar * (unsigned long long)G;
+    const unsigned long long v = ld_relaxed_u64(a.bar);
+    base_sm = per ? (v / per) * per : 0ull;
+  }
+  __syncthreads();
+  const unsigned long long base = base_sm;
+  int nb = 0;
+  Staged st;
+  // first task of segment s for this warp (or -1)
+  auto first_task = [&](const SweepSeg& sg) -> int64_t {
+    int64_t t;
+    if (sg.narrow) {
+      if (blockIdx.x != 0) return -1;
+      t = sg.t0 + warp;
+    } else {
+      t = sg.t0 + gw;
+    }
+    return t < sg.t1 ? t : -1;
+  };
+  int64_t staged_t = a.nsegs > 0 ? first_task(a.segs[0]) : -1;
+  if (staged_t >= 0) stage(a, staged_t, lane, st);
+  for (int s = 0; s < a.nsegs; ++s) {
+    const SweepSeg sg = a.segs[s];
+    const int64_t stride = sg.narrow ? kSweepWarps : W;
+    if (staged_t >= 0) {
+      finish(a, st, lane);
+      for (int64_t t = staged_t + stride; t < sg.t1; t += stride) {
+        stage(a, t, lane, st);
+        finish(a, st, lane);
+      }
+    }
+    // stage the next level's first task before waiting for this one
+    staged_t = (s + 1 < a.nsegs) ? first_task(a.segs[s + 1]) : -1;
+    if (staged_t >= 0) stage(a, staged_t, lane, st);
+    if (sg.narrow && blockIdx.x == 0) __syncthreads();
+    if (sg.barrier) {
+      ++nb;
+      grid_barrier(a.bar, base + (unsigned long long)nb * (unsigned long long)G);
+    }
+  }
+}
+
+static int sweep_blocks_per_sm() {
+  static int occ = -1;
+  if (occ < 0) {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, sweep_kernel, kSweepThreads, 0) !=
+            cudaSuccess ||
+        o < 1)
+      o = 1;
+    occ = std::min(o, 2);
+  }
+  return occ;
+}
+
+template <typename T>
+static bool upload(T** dst, const std::vector<T>& v) {
+  if (v.empty()) return true;
+  if (cudaMalloc((void**)dst, sizeof(T) * v.size()) != cudaSuccess) return false;
+  return cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+}
+
+static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
+                       const std::vector<int32_t>& col, const std::vector<double>& val,
+                       const std::vector<double>& diag, bool forward, SweepDev& d) {
+  SweepHost h;
+  build_sweep(n, rp, col, val, diag, forward, h);
+  d.nsegs = (int32_t)h.segs.size();
+  d.nbar = h.nbar;
+  d.levels = h.levels;
+  bool ok = upload(&d.prp, h.prp) && upload(&d.pcol, h.pcol) && upload(&d.pval, h.pval) &&
+            upload(&d.perm, h.perm) && upload(&d.pdiag, h.pdiag) && upload(&d.tasks, h.tasks) &&
+            upload(&d.segs, h.segs) && upload(&d.hub_first, h.hub_first) &&
+            upload(&d.hub_nchunk, h.hub_nchunk);
+  if (!ok) return false;
+  if (!h.hub_first.empty()) {
+    if (cudaMalloc(&d.hub_ticket, sizeof(unsigned) * h.hub_first.size()) != cudaSuccess ||
+        cudaMemset(d.hub_ticket, 0, sizeof(unsigned) * h.hub_first.size()) != cudaSuccess ||
+        cudaMalloc(&d.hub_part, sizeof(double) * (size_t)h.nparts) != cudaSuccess)
+      return false;
+  }
+  if (cudaMalloc(&d.bar, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemset(d.bar, 0, sizeof(unsigned long long)) != cudaSuccess)
+    return false;
+  return true;
+}
+
+static void free_sweep(SweepDev& d) {
+  cudaFree(d.prp);
+  cudaFree(d.pcol);
+  cudaFree(d.pval);
+  cudaFree(d.perm);
+  cudaFree(d.pdiag);
+  cudaFree(d.tasks);
+  cudaFree(d.segs);
+  cudaFree(d.hub_first);
+  cudaFree(d.hub_nchunk);
+  cudaFree(d.hub_ticket);
+  cudaFree(d.hub_part);
+  cudaFree(d.bar);
+  d = SweepDev();
+}
+
+static SweepArgs sweep_args(const SweepDev& d, const double* b, double* x, const int* skip) {
+  SweepArgs a;
+  a.prp = d.prp;
+  a.pcol = d.pcol;
+  a.pval = d.pval;
+  a.perm = d.perm;
+  a.pdiag = d.pdiag;
+  a.tasks = d.tasks;
+  a.segs = d.segs;
+  a.nsegs = d.nsegs;
+  a.nbar = d.nbar;
+  a.hub_first = d.hub_first;
+  a.hub_nchunk = d.hub_nchunk;
+  a.hub_ticket = d.hub_ticket;
+  a.hub_part = d.hub_part;
+  a.bar = d.bar;
+  a.b = b;
+  a.x = x;
+  a.skip = skip;
+  return a;
+}
+
+}  // namespace lg
+
+using namespace lg;
+
+extern "C" {
+
+int lg_ic0_factorize(int64_t n, const int64_t* rp, const int64_t* col,
+                     const double* val, double shift0, const double* sched,
+                     int nsched, int64_t* l_rp, int64_t* l_col, double* l_val,
+                     double* shift, int* attempts) {
+  if (n < 0 || !rp || (rp[n] > 0 && (!col || !val)) || !l_rp || !shift || !attempts ||
+      nsched < 0 || (nsched > 0 && !sched))
+    return fail(LG_EINVAL, "lg_ic0_factorize: bad argument");
+  // split A into its strictly-lower pattern + diagonal (ic0.py:94-101)
+  std::vector<double> diag((size_t)n, 0.0);
+  std::vector<int64_t> lrp((size_t)n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t c = 0;
+    for (int64_t k = rp[i]; k < rp[i + 1] && col[k] < i; ++k) ++c;
+    lrp[(size_t)i + 1] = lrp[(size_t)i] + c + 1;
+  }
+  const int64_t nl = lrp[(size_t)n];
+  std::vector<int64_t> lcol((size_t)nl);
+  std::vector<double> aval((size_t)nl, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t o = lrp[(size_t)i];
+    int64_t k = rp[i];
+    for (; k < rp[i + 1] && col[k] < i; ++k) {
+      lcol[(size_t)o] = col[k];
+      aval[(size_t)o] = val[k];
+      ++o;
+    }
+    if (k < rp[i + 1] && col[k] == i) diag[(size_t)i] = val[k];
+    lcol[(size_t)o] = i;  // diagonal slot
+  }
+  double dmax = 0.0;
+  for (int64_t i = 0; i < n; ++i) dmax = (i == 0) ? diag[0] : std::max(dmax, diag[(size_t)i]);
+  // shift ladder (ic0.py:98-111)
+  std::vector<double> shifts{shift0};
+  for (int s = 0; s < nsched; ++s)
+    if (sched[s] > shift0) shifts.push_back(sched[s]);
+  const double last = 0.1 * dmax;
+  if (dmax > 0 && (shifts.empty() || last > shifts.back())) shifts.push_back(last);
+  std::vector<double> lval((size_t)nl, 0.0);
+  std::vector<int64_t> stamp((size_t)n), pos((size_t)n);
+  int tries = 0;
+  for (double alpha : shifts) {
+    ++tries;
+    if (ic0_attempt(n, diag, lrp, lcol, aval, alpha, lval, stamp, pos)) {
+      std::memcpy(l_rp, lrp.data(), sizeof(int64_t) * (size_t)(n + 1));
+      std::memcpy(l_col, lcol.data(), sizeof(int64_t) * (size_t)nl);
+      std::memcpy(l_val, lval.data(), sizeof(double) * (size_t)nl);
+      *shift = alpha;
+      *attempts = tries;
+      return LG_OK;
+    }
+  }
+  *attempts = tries;
+  return fail(LG_EBREAKDOWN, "pivot breakdown at every shift");
+}
+
+int lg_ic0_create(int64_t n, const int64_t* l_rp, const int64_t* l_col,
+                  const double* l_val, lg_ic0** out) {
+  if (!out || n < 0 || !l_rp || (n > 0 && (!l_col || !l_val)))
+    return fail(LG_EINVAL, "lg_ic0_create: bad argument");
+  if (n >= ((int64_t)1 << 31)) return fail(LG_EINVAL, "lg_ic0_create: n too large");
+  // validate: lower triangular with the diagonal last in every row
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t lo = l_rp[i], hi = l_rp[i + 1];
+    if (hi <= lo || l_col[hi - 1] != i)
+      return fail(LG_EINVAL, "lg_ic0_create: every row needs its diagonal last");
+    for (int64_t k = lo; k < hi - 1; ++k)
+      if (l_col[k] < 0 || l_col[k] >= i || (k > lo && l_col[k] <= l_col[k - 1]))
+        return fail(LG_EINVAL, "lg_ic0_create: factor must be strictly lower, sorted");
+    if (!(l_val[hi - 1] != 0.0)) return fail(LG_EINVAL, "lg_ic0_create: zero pivot");
+  }
+  const int64_t nnz = n ? l_rp[n] : 0;
+  const int64_t noff = nnz - n;
+  std::vector<int64_t> frp((size_t)n + 1, 0), brp((size_t)n + 1, 0);
+  std::vector<int32_t> fcol((size_t)noff), bcol((size_t)noff);
+  std::vector<double> fval((size_t)noff), bval((size_t)noff), dg((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t lo = l_rp[i], hi = l_rp[i + 1] - 1;
+    frp[(size_t)i + 1] = frp[(size_t)i] + (hi - lo);
+    for (int64_t k = lo; k < hi; ++k) {
+      fcol[(size_t)(frp[(size_t)i] + k - lo)] = (int32_t)l_col[k];
+      fval[(size_t)(frp[(size_t)i] + k - lo)] = l_val[k];
+      brp[(size_t)l_col[k] + 1]++;
+    }
+    dg[(size_t)i] = l_val[hi];
+  }
+  for (int64_t i = 0; i < n; ++i) brp[(size_t)i + 1] += brp[(size_t)i];
+  {
+    // transpose: row j of L^T lists i > j in ascending i
+    std::vector<int64_t> fill(brp.begin(), brp.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = frp[(size_t)i]; k < frp[(size_t)i + 1]; ++k) {
+        int64_t j = fcol[(size_t)k];
+        bcol[(size_t)fill[(size_t)j]] = (int32_t)i;
+        bval[(size_t)fill[(size_t)j]] = fval[(size_t)k];
+        fill[(size_t)j]++;
+      }
+  }
+  lg_ic0* f = new lg_ic0();
+  f->n = n;
+  f->nnz_l = nnz;
+  bool ok = make_sweep(n, frp, fcol, fval, dg, true, f->fwd) &&
+            make_sweep(n, brp, bcol, bval, dg, false, f->bwd) && upload(&f->diag, dg) &&
+            (n == 0 || cudaMalloc(&f->tmp, 8 * (size_t)n) == cudaSuccess);
+  if (!ok) {
+    lg_ic0_destroy(f);
+    return fail(LG_ENOMEM, "lg_ic0_create: device allocation / upload failed");
+  }
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    lg_ic0_destroy(f);
+    return fail(LG_ECUDA, std::string("lg_ic0_create: ") + cudaGetErrorString(err));
+  }
+  f->grid = sweep_blocks_per_sm() * dev_info().sm_count;
+  *out = f;
+  return LG_OK;
+}
+
+int lg_ic0_destroy(lg_ic0* f) {
+  if (!f) return LG_OK;
+  free_sweep(f->fwd);
+  free_sweep(f->bwd);
+  cudaFree(f->diag);
+  cudaFree(f->tmp);
+  delete f;
+  return LG_OK;
+}
+
+int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels) {
+  if (!f) return fail(LG_EINVAL, "lg_ic0_info: NULL handle");
+  if (n) *n = f->n;
+  if (nnz_l) *nnz_l = f->nnz_l;
+  if (levels) *levels = std::max(f->fwd.levels, f->bwd.levels);
+  return LG_OK;
+}
+
+int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
+                 void* stream) {
+  if (!f || !r || !z) return fail(LG_EINVAL, "lg_ic0_apply: NULL argument");
+  if (f->n == 0) return LG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  SweepArgs fa = sweep_args(f->fwd, r, f->tmp, skip);
+  SweepArgs ba = sweep_args(f->bwd, f->tmp, z, skip);
+  void* fargs[] = {&fa};
+  LG_CUDA(cudaLaunchCooperativeKernel((void*)sweep_kernel, dim3(f->grid), dim3(kSweepThreads),
+                                      fargs, 0, s));
+  void* bargs[] = {&ba};
+  LG_CUDA(cudaLaunchCooperativeKernel((void*)sweep_kernel, dim3(f->grid), dim3(kSweepThreads),
+                                      bargs, 0, s));
+  return LG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,498 @@
+// lg_spmv.cu -- CSR upload, nnz-balanced row-block schedule, fused SpMV.
+//
+// Replaces sparse.py:128-139 (y[nz] = add.reduceat(values * x[col_idx], ...)).
+//
+// Design (HBM-bound, arithmetic intensity 2 flops / 12 bytes):
+//   * the matrix is cut at upload time into row blocks of at most kChunk
+//     nonzeros (and kRowCap rows); a row longer than kChunk (power-law hubs:
+//     107,553 nonzeros in C4's largest row) is split into parts of kChunk.
+//     Every block therefore streams the same number of bytes, which is what
+//     balances degree-skewed graphs.
+//   * a persistent grid (CTAs = SMs x resident CTAs) walks the blocks
+//     round-robin.  A normal block first streams its values / column indices
+//     coalesced and stores val*x[col] into shared memory, then reduces rows
+//     from shared memory with 1..32 lanes per row (chosen per block from its
+//     mean row length at upload time).  A long-row part reduces in registers
+//     and publishes one partial; the last part to arrive (atomic ticket) sums
+//     the parts in part order.  Summation order is fixed, so y is bitwise
+//     reproducible.
+//   * the epilogue fuses the theta shift (JD's L - theta I, pcg.py:171-172)
+//     and dot products of y with up to LG_MAXD vectors and a column block Q
+//     (the Q^T y half of the next deflation projection, pcg.py:60).
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "lg_common.cuh"
+
+namespace lg {
+
+constexpr int kChunk = 2048;   // nonzeros per row block (16 KB of products)
+constexpr int kRowCap = 1024;  // rows per normal block
+
+struct SpmvBlock {
+  int64_t nz0, nz1;  // nonzero range
+  int32_t row0;      // first row
+  int32_t nrows;     // rows (normal) / long-row id (long)
+  int32_t lanes;     // lanes per row (normal); 0 marks a long-row part
+  int32_t part;      // compact long-part slot (long)
+};
+
+}  // namespace lg
+
+struct lg_csr {
+  int64_t n = 0, nnz = 0;
+  int64_t* row_ptr = nullptr;  // device [n+1]
+  int32_t* col = nullptr;      // device [nnz]
+  double* val = nullptr;       // device [nnz]
+  lg::SpmvBlock* blocks = nullptr;
+  int64_t nblocks = 0;
+  int64_t nlong = 0;
+  int64_t nparts = 0;              // total long-row parts
+  int32_t* long_nparts = nullptr;  // device [nlong]
+  int64_t* long_first = nullptr;   // device [nlong] slot of part 0
+};
+
+namespace lg {
+
+struct SpmvArgs {
+  int64_t n;
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const double* val;
+  const SpmvBlock* blocks;
+  int64_t nblocks;
+  const int32_t* long_nparts;
+  const int64_t* long_first;
+  const double* x;
+  double* y;
+  double theta_h;
+  const double* theta_d;
+  int theta_neg;
+  int ndots;
+  const double* dvec[LG_MAXD];
+  const double* q;
+  int64_t ldq;
+  int nq;
+  double* out;
+  const int* skip;
+  double* long_part;   // [nparts] partial of each long-row part
+  unsigned* long_ticket;  // [nlong]
+  int64_t nlong;
+};
+
+template <int NA, int M>
+__device__ __forceinline__ void epilogue_row(const SpmvArgs& a, int64_t r,
+                                             double yr, double (&acc)[M]) {
+  if constexpr (NA > 0) {
+#pragma unroll
+    for (int d = 0; d < NA; ++d) {
+      if (d < a.ndots) {
+        const double* v = a.dvec[d];
+        acc[d] += yr * (v ? v[r] : yr);
+      } else if (d < a.ndots + a.nq) {
+        acc[d] += yr * a.q[r + (int64_t)(d - a.ndots) * a.ldq];
+      }
+    }
+  }
+}
+
+template <int NA>
+__global__ void __launch_bounds__(kThreads)
+spmv_kernel(SpmvArgs a, lg_ws ws) {
+  if (a.skip && *a.skip) return;
+  __shared__ double sm[kChunk];
+  __shared__ double red_sm[kWarps * (NA > 0 ? NA : 1)];
+  __shared__ int fin_flag;
+  double acc[NA > 0 ? NA : 1];
+#pragma unroll
+  for (int d = 0; d < (NA > 0 ? NA : 1); ++d) acc[d] = 0.0;
+  double theta = a.theta_h;
+  if (a.theta_d) theta += a.theta_neg ? -*a.theta_d : *a.theta_d;
+  const int tid = threadIdx.x;
+
+  for (int64_t b = blockIdx.x; b < a.nblocks; b += gridDim.x) {
+    const SpmvBlock blk = a.blocks[b];
+    const int cnt = (int)(blk.nz1 - blk.nz0);
+    if (blk.lanes > 0) {
+      // ---- normal block: stream products into shared memory
+#pragma unroll 8
+      for (int e = tid; e < cnt; e += kThreads) {
+        int64_t k = blk.nz0 + e;
+        sm[e] = ld_stream(a.val + k) * __ldg(a.x + ld_stream(a.col + k));
+      }
+      __syncthreads();
+      const int L = blk.lanes;
+      const int groups = kThreads / L;
+      const int g = tid / L, li = tid % L;
+      for (int base = 0; base < blk.nrows; base += groups) {
+        const int rr = base + g;
+        double s = 0.0;
+        int64_t r = blk.row0 + rr;
+        if (rr < blk.nrows) {
+          int lo = (int)(a.row_ptr[r] - blk.nz0);
+          int hi = (int)(a.row_ptr[r + 1] - blk.nz0);
+          for (int e = lo + li; e < hi; e += L) s += sm[e];
+        }
+        for (int o = L >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (rr < blk.nrows && li == 0) {
+          double yr = s;
+          if (theta != 0.0) yr -= theta * a.x[r];
+          a.y[r] = yr;
+          epilogue_row<NA>(a, r, yr, acc);
+        }
+      }
+      __syncthreads();  // sm reused by the next block
+    } else {
+      // ---- part of a long row: register partial, ticket, ordered finish
+      double s = 0.0;
+#pragma unroll 8
+      for (int e = tid; e < cnt; e += kThreads) {
+        int64_t k = blk.nz0 + e;
+        s += ld_stream(a.val + k) * __ldg(a.x + ld_stream(a.col + k));
+      }
+      s = warp_sum(s);
+      if ((tid & 31) == 0) sm[tid >> 5] = s;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kWarps; ++w) t += sm[w];
+        a.long_part[blk.part] = t;
+        __threadfence();
+        const int lr = blk.nrows;
+        unsigned arrived = atomicAdd(a.long_ticket + lr, 1u);
+        fin_flag = (arrived == (unsigned)a.long_nparts[lr] - 1u);
+      }
+      __syncthreads();
+      if (fin_flag && tid < 32) {
+        // the finishing CTA's first warp sums the parts lane-strided and
+        // then by butterfly: fixed order, independent of arrival order
+        __threadfence();
+        const int lr = blk.nrows;
+        const int64_t first = a.long_first[lr];
+        const int np = a.long_nparts[lr];
+        double t = 0.0;
+        for (int p = tid; p < np; p += 32) t += ld_cg(a.long_part + first + p);
+        t = warp_sum(t);
+        if (tid == 0) {
+          const int64_t r = blk.row0;
+          double yr = t;
+          if (theta != 0.0) yr -= theta * a.x[r];
+          a.y[r] = yr;
+          a.long_ticket[lr] = 0u;
+          if constexpr (NA > 0) {
+            // long-row epilogue goes to its own slot: order stays fixed no
+            // matter which CTA finishes the row
+            double la[NA];
+#pragma unroll
+            for (int d = 0; d < NA; ++d) la[d] = 0.0;
+            epilogue_row<NA>(a, r, yr, la);
+            for (int d = 0; d < a.ndots + a.nq; ++d)
+              ws.long_dots[(int64_t)lr * kMaxRedVals + d] = la[d];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if constexpr (NA > 0) {
+    grid_reduce<NA>(acc, a.ndots + a.nq, ws, a.out, red_sm, ws.long_dots,
+                    a.nlong);
+  }
+}
+
+// Build the row-block schedule on the host (O(n)).
+static void build_schedule(int64_t n, const int64_t* rp,
+                           std::vector<SpmvBlock>& blocks,
+                           std::vector<int32_t>& long_nparts,
+                           std::vector<int64_t>& long_first) {
+  int64_t r = 0, part_total = 0;
+  while (r < n) {
+    int64_t len = rp[r + 1] - rp[r];
+    if (len > kChunk) {
+      int32_t np = (int32_t)((len + kChunk - 1) / kChunk);
+      int32_t lr = (int32_t)long_nparts.size();
+      long_nparts.push_back(np);
+      const int64_t slot0 = part_total;
+      part_total += np;
+      long_first.push_back(slot0);
+      for (int32_t p = 0; p < np; ++p) {
+        SpmvBlock b;
+        b.nz0 = rp[r] + (int64_t)p * kChunk;
+        b.nz1 = std::min(rp[r] + (int64_t)(p + 1) * kChunk, rp[r + 1]);
+        b.row0 = (int32_t)r;
+        b.nrows = lr;
+        b.lanes = 0;
+        b.part = (int32_t)(slot0 + p);
+        blocks.push_back(b);
+      }
+      ++r;
+      continue;
+    }
+    int64_t r0 = r, nz = 0;
+    while (r < n && r - r0 < kRowCap) {
+      int64_t l = rp[r + 1] - rp[r];
+      if (l > kChunk || nz + l > kChunk) break;
+      nz += l;
+      ++r;
+    }
+    SpmvBlock b;
+    b.nz0 = rp[r0];
+    b.nz1 = rp[r];
+    b.row0 = (int32_t)r0;
+    b.nrows = (int32_t)(r - r0);
+    double avg = (double)nz / (double)(r - r0);
+    int L = 1;
+    while (L < 32 && 2.0 * L <= avg) L <<= 1;  // lanes <= mean row length
+    b.lanes = L;
+    b.part = 0;
+    blocks.push_back(b);
+  }
+}
+
+static int ensure_long_ws(lg_ws* ws, const lg_csr* a) {
+  if (a->nlong > ws->long_cap) {
+    cudaFree(ws->long_dots);
+    cudaFree(ws->long_ticket);
+    ws->long_dots = nullptr;
+    ws->long_ticket = nullptr;
+    ws->long_cap = 0;
+    LG_CUDA(cudaMalloc(&ws->long_dots,
+                       sizeof(double) * (size_t)a->nlong * kMaxRedVals));
+    LG_CUDA(cudaMalloc(&ws->long_ticket, sizeof(unsigned) * (size_t)a->nlong));
+    LG_CUDA(cudaMemset(ws->long_ticket, 0, sizeof(unsigned) * (size_t)a->nlong));
+    LG_CUDA(cudaDeviceSynchronize());
+    ws->long_cap = a->nlong;
+  }
+  if (a->nparts > ws->part_cap) {
+    cudaFree(ws->long_part);
+    ws->long_part = nullptr;
+    ws->part_cap = 0;
+    LG_CUDA(cudaMalloc(&ws->long_part, sizeof(double) * (size_t)a->nparts));
+    ws->part_cap = a->nparts;
+  }
+  return LG_OK;
+}
+
+template <int NA>
+static int grid_for() {
+  static int occ = -1;
+  if (occ < 0) {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, spmv_kernel<NA>,
+                                                      kThreads, 0) != cudaSuccess ||
+        o < 1)
+      o = 1;
+    occ = o;
+  }
+  return occ * dev_info().sm_count;
+}
+
+template <int NA>
+static int launch(const SpmvArgs& args, lg_ws* ws, cudaStream_t s) {
+  int64_t g = std::min<int64_t>(args.nblocks, grid_for<NA>());
+  if (NA > 0) g = std::min<int64_t>(g, kMaxRedBlocks);
+  if (g < 1) g = 1;
+  spmv_kernel<NA><<<(unsigned)g, kThreads, 0, s>>>(args, *ws);
+  LG_LAUNCH_CHECK("spmv_kernel");
+  return LG_OK;
+}
+
+}  // namespace lg
+
+using namespace lg;
+
+extern "C" {
+
+int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
+                  const double* val, int flags, lg_csr** out) {
+  (void)flags;
+  if (!out) return fail(LG_EINVAL, "lg_csr_create: out is NULL");
+  if (n < 0 || nnz < 0) return fail(LG_EINVAL, "lg_csr_create: negative size");
+  if (n >= ((int64_t)1 << 31))
+    return fail(LG_EINVAL, "lg_csr_create: n >= 2^31 not supported (int32 columns)");
+  if (!rp || (nnz > 0 && (!col || !val)))
+    return fail(LG_EINVAL, "lg_csr_create: NULL array");
+  if (rp[0] != 0 || rp[n] != nnz)
+    return fail(LG_EINVAL, "lg_csr_create: row_ptr must start at 0 and end at nnz");
+  for (int64_t r = 0; r < n; ++r)
+    if (rp[r + 1] < rp[r])
+      return fail(LG_EINVAL, "lg_csr_create: row_ptr must be nondecreasing");
+  std::vector<int32_t> c32((size_t)nnz);
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (col[k] < 0 || col[k] >= n)
+      return fail(LG_EINVAL, "lg_csr_create: column index out of range");
+    c32[(size_t)k] = (int32_t)col[k];
+  }
+  std::vector<SpmvBlock> blocks;
+  std::vector<int32_t> lnp;
+  std::vector<int64_t> lfirst;
+  build_schedule(n, rp, blocks, lnp, lfirst);
+
+  lg_csr* a = new lg_csr();
+  a->n = n;
+  a->nnz = nnz;
+  a->nblocks = (int64_t)blocks.size();
+  a->nlong = (int64_t)lnp.size();
+  for (int32_t v : lnp) a->nparts += v;
+  auto cleanup = [&](const char* what) {
+    lg_csr_destroy(a);
+    return fail(LG_ENOMEM, std::string("lg_csr_create: ") + what);
+  };
+  if (cudaMalloc(&a->row_ptr, sizeof(int64_t) * (size_t)(n + 1)) != cudaSuccess)
+    return cleanup("row_ptr alloc");
+  if (nnz && cudaMalloc(&a->col, sizeof(int32_t) * (size_t)nnz) != cudaSuccess)
+    return cleanup("col alloc");
+  if (nnz && cudaMalloc(&a->val, sizeof(double) * (size_t)nnz) != cudaSuccess)
+    return cleanup("val alloc");
+  if (a->nblocks &&
+      cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess)
+    return cleanup("schedule alloc");
+  if (a->nlong) {
+    if (cudaMalloc(&a->long_nparts, sizeof(int32_t) * (size_t)a->nlong) != cudaSuccess ||
+        cudaMalloc(&a->long_first, sizeof(int64_t) * (size_t)a->nlong) != cudaSuccess)
+      return cleanup("long-row alloc");
+  }
+  cudaMemcpy(a->row_ptr, rp, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice);
+  if (nnz) {
+    cudaMemcpy(a->col, c32.data(), sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice);
+    cudaMemcpy(a->val, val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice);
+  }
+  if (a->nblocks)
+    cudaMemcpy(a->blocks, blocks.data(), sizeof(SpmvBlock) * (size_t)a->nblocks,
+               cudaMemcpyHostToDevice);
+  if (a->nlong) {
+    cudaMemcpy(a->long_nparts, lnp.data(), sizeof(int32_t) * (size_t)a->nlong,
+               cudaMemcpyHostToDevice);
+    cudaMemcpy(a->long_first, lfirst.data(), sizeof(int64_t) * (size_t)a->nlong,
+               cudaMemcpyHostToDevice);
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    lg_csr_destroy(a);
+    return fail(LG_ECUDA, std::string("lg_csr_create: ") + cudaGetErrorString(e));
+  }
+  *out = a;
+  return LG_OK;
+}
+
+int lg_csr_destroy(lg_csr* a) {
+  if (!a) return LG_OK;
+  cudaFree(a->row_ptr);
+  cudaFree(a->col);
+  cudaFree(a->val);
+  cudaFree(a->blocks);
+  cudaFree(a->long_nparts);
+  cudaFree(a->long_first);
+  delete a;
+  return LG_OK;
+}
+
+int lg_csr_info(const lg_csr* a, int64_t* n, int64_t* nnz, int64_t* nblocks,
+                int64_t* nlong, int* packed, int64_t* stream_bytes) {
+  if (!a) return fail(LG_EINVAL, "lg_csr_info: NULL handle");
+  if (n) *n = a->n;
+  if (nnz) *nnz = a->nnz;
+  if (nblocks) *nblocks = a->nblocks;
+  if (nlong) *nlong = a->nlong;
+  if (packed) *packed = 0;
+  // values f64 + int32 columns + int64 row pointers + x read + y written
+  if (stream_bytes)
+    *stream_bytes = 12 * a->nnz + 8 * (a->n + 1) + 16 * a->n;
+  return LG_OK;
+}
+
+int lg_csr_download(const lg_csr* a, int64_t* rp, int64_t* col, double* val) {
+  if (!a) return fail(LG_EINVAL, "lg_csr_download: NULL handle");
+  if (rp)
+    LG_CUDA(cudaMemcpy(rp, a->row_ptr, sizeof(int64_t) * (size_t)(a->n + 1),
+                       cudaMemcpyDeviceToHost));
+  if (col && a->nnz) {
+    std::vector<int32_t> c32((size_t)a->nnz);
+    LG_CUDA(cudaMemcpy(c32.data(), a->col, sizeof(int32_t) * (size_t)a->nnz,
+                       cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < a->nnz; ++k) col[k] = c32[(size_t)k];
+  }
+  if (val && a->nnz)
+    LG_CUDA(cudaMemcpy(val, a->val, sizeof(double) * (size_t)a->nnz,
+                       cudaMemcpyDeviceToHost));
+  return LG_OK;
+}
+
+int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
+            const double* theta_d, int theta_neg, int ndots,
+            const double* const* dvec, const double* q, int64_t ldq, int nq,
+            double* out, lg_ws* ws, const int* skip, void* stream) {
+  if (!a || !x || !y) return fail(LG_EINVAL, "lg_spmv: NULL argument");
+  if (ndots < 0 || ndots > LG_MAXD || nq < 0 || nq > LG_MAXQ)
+    return fail(LG_EINVAL, "lg_spmv: too many epilogue dots");
+  if ((ndots + nq) > 0 && (!out || !ws))
+    return fail(LG_EINVAL, "lg_spmv: epilogue dots need out and ws");
+  if (nq > 0 && (!q || ldq < a->n))
+    return fail(LG_EINVAL, "lg_spmv: bad Q block");
+  if (a->n == 0) return LG_OK;
+  lg_ws local{};
+  if (!ws) ws = &local;
+  if (a->nlong) {
+    if (ws == &local) return fail(LG_EINVAL, "lg_spmv: matrix has long rows; pass a workspace");
+    int rc = ensure_long_ws(ws, a);
+    if (rc) return rc;
+  }
+  SpmvArgs args{};
+  args.n = a->n;
+  args.row_ptr = a->row_ptr;
+  args.col = a->col;
+  args.val = a->val;
+  args.blocks = a->blocks;
+  args.nblocks = a->nblocks;
+  args.long_nparts = a->long_nparts;
+  args.long_first = a->long_first;
+  args.x = x;
+  args.y = y;
+  args.theta_h = theta_h;
+  args.theta_d = theta_d;
+  args.theta_neg = theta_neg;
+  args.ndots = ndots;
+  for (int d = 0; d < ndots; ++d) args.dvec[d] = dvec ? dvec[d] : nullptr;
+  args.q = q;
+  args.ldq = ldq;
+  args.nq = nq;
+  args.out = out;
+  args.skip = skip;
+  args.long_part = ws->long_part;
+  args.long_ticket = ws->long_ticket;
+  args.nlong = a->nlong;
+  cudaStream_t s = (cudaStream_t)stream;
+  int na = ndots + nq;
+  if (na == 0) return launch<0>(args, ws, s);
+  if (na <= 4) return launch<4>(args, ws, s);
+  if (na <= 16) return launch<16>(args, ws, s);
+  return launch<LG_MAXD + LG_MAXQ>(args, ws, s);
+}
+
+int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,
+                 double* yd, void* stream) {
+  if (!a || !x_h || !y_h || !xd || !yd) return fail(LG_EINVAL, "lg_spmv_host: NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t bytes = sizeof(double) * (size_t)a->n;
+  LG_CUDA(cudaMemcpyAsync(xd, x_h, bytes, cudaMemcpyHostToDevice, s));
+  int rc = lg_spmv(a, xd, yd, 0.0, nullptr, 0, 0, nullptr, nullptr, 0, 0,
+                   nullptr, nullptr, nullptr, stream);
+  if (rc) return rc;
+  LG_CUDA(cudaMemcpyAsync(y_h, yd, bytes, cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaStreamSynchronize(s));
+  return LG_OK;
+}
+
+int lg_spmm(const lg_csr* a, const double* x, double* y, int k, void* stream) {
+  if (!a || !x || !y || k < 0) return fail(LG_EINVAL, "lg_spmm: bad argument");
+  for (int j = 0; j < k; ++j) {
+    int rc = lg_spmv(a, x + (int64_t)j * a->n, y + (int64_t)j * a->n, 0.0,
+                     nullptr, 0, 0, nullptr, nullptr, 0, 0, nullptr, nullptr,
+                     nullptr, stream);
+    if (rc) return rc;
+  }
+  return LG_OK;
+}
+
+}  // extern "C"

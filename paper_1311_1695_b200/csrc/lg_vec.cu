@@ -1,0 +1,297 @@
+// lg_vec.cu -- fused streaming vector pass, small tall-skinny GEMM,
+// Jacobi apply.
+//
+// Replaces the n-vector arithmetic of the reference solvers:
+//   DeflationBasis.project_out  v - C (C^T v)            pcg.py:55-60
+//   mgs_orthonormalize sweeps   v -= (q.v) q              kernels.py:42-49
+//   DACG dots / axpys / normalisation                     dacg.py:40-96,172-233
+//   PCG dots / axpys                                      pcg.py:131-155
+// Each of those is a sequence of numpy passes (one pass per dot, per axpy,
+// per GEMV).  lg_fused does any such sequence that has no grid-wide data
+// dependency in ONE pass: up to two outputs (linear combinations of up to
+// four vectors, minus a block combination Q c whose coefficients c were
+// produced by an earlier pass), plus dot products and Q^T v block dots of
+// inputs *and* of the freshly computed outputs.  The projection v - Q(Q^T v)
+// is therefore split across two passes -- the Q^T v half is fused into the
+// pass (or SpMV / SpTRSV epilogue) that produces v, the update half into the
+// pass that consumes it -- so a projection costs no pass of its own.
+#include <algorithm>
+#include <cstring>
+
+#include "lg_common.cuh"
+
+namespace lg {
+
+struct FusedDev {
+  int64_t n;
+  lg_output o[LG_MAXO];
+  int ndots;
+  const double* da[LG_MAXD];
+  const double* db[LG_MAXD];
+  const double* dc[LG_MAXD];
+  int nblocks;
+  lg_block b[LG_MAXB];
+  double* result;
+  const int* skip;
+};
+
+__device__ __forceinline__ double pick(const double* p, int64_t i,
+                                       const double (&o)[LG_MAXO]) {
+  const uintptr_t u = (uintptr_t)p;
+  if (u == 1) return o[0];
+  if (u == 2) return o[1];
+  if (u == 3) return o[2];
+  return p[i];
+}
+
+__device__ __forceinline__ double output_value(const lg_output& o,
+                                               const double* coef,
+                                               const double* uc, int64_t i,
+                                               const double (&ov)[LG_MAXO],
+                                               double post, int pmode) {
+  double v = 0.0;
+#pragma unroll
+  for (int t = 0; t < LG_MAXT; ++t)
+    if (t < o.nterms) v += coef[t] * pick(o.t[t].v, i, ov);
+  if (o.uk > 0) {
+    const double* q = o.uq + i;
+    double s = 0.0;
+    for (int j = 0; j < o.uk; ++j) s += uc[j] * q[(int64_t)j * o.uld];
+    v -= s;
+  }
+  if (pmode == 1) v *= post;
+  else if (pmode == 2) v /= post;
+  return v;
+}
+
+template <int NA>
+__global__ void __launch_bounds__(kThreads, (NA <= 16 ? 4 : 1))
+fused_kernel(FusedDev a, lg_ws ws) {
+  if (a.skip && *a.skip) return;
+  constexpr int M = NA > 0 ? NA : 1;
+  __shared__ double uc_sm[LG_MAXO][LG_MAXQ];
+  __shared__ double red_sm[kWarps * M];
+  double coef[LG_MAXO][LG_MAXT];
+  double post[LG_MAXO] = {1.0, 1.0, 1.0};
+  int pmode[LG_MAXO] = {0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < LG_MAXO; ++k) {
+    const lg_output& o = a.o[k];
+#pragma unroll
+    for (int t = 0; t < LG_MAXT; ++t) {
+      double c = 0.0;
+      if (t < o.nterms) {
+        c = o.t[t].h;
+        if (o.t[t].d) c *= *o.t[t].d;
+      }
+      coef[k][t] = c;
+    }
+    if (o.post_mode) {
+      double p = *o.d_post;
+      post[k] = (o.post_mode == 3) ? sqrt(p) : p;
+      pmode[k] = (o.post_mode == 1) ? 1 : 2;
+    }
+    for (int j = threadIdx.x; j < o.uk; j += blockDim.x)
+      uc_sm[k][j] = o.cscale * o.uc[j];
+  }
+  __syncthreads();
+
+  double acc[M];
+#pragma unroll
+  for (int d = 0; d < M; ++d) acc[d] = 0.0;
+  const int nd = a.ndots;
+  const int k0 = a.nblocks > 0 ? a.b[0].k : 0;
+  const int k1 = a.nblocks > 1 ? a.b[1].k : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += stride) {
+    double ov[LG_MAXO] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < LG_MAXO; ++k) {
+      if (a.o[k].out) {
+        ov[k] = output_value(a.o[k], coef[k], uc_sm[k], i, ov, post[k], pmode[k]);
+        a.o[k].out[i] = ov[k];
+      }
+    }
+    if constexpr (NA > 0) {
+      double bv0 = 0.0, bv1 = 0.0;
+      if (k0) bv0 = pick(a.b[0].v, i, ov);
+      if (k1) bv1 = pick(a.b[1].v, i, ov);
+#pragma unroll
+      for (int s = 0; s < NA; ++s) {
+        if (s < nd) {
+          double x = pick(a.da[s], i, ov);
+          if (a.dc[s]) x -= pick(a.dc[s], i, ov);
+          double y = a.db[s] ? pick(a.db[s], i, ov) : x;
+          acc[s] += x * y;
+        } else if (s < nd + k0) {
+          acc[s] += bv0 * a.b[0].q[i + (int64_t)(s - nd) * a.b[0].ld];
+        } else if (s < nd + k0 + k1) {
+          acc[s] += bv1 * a.b[1].q[i + (int64_t)(s - nd - k0) * a.b[1].ld];
+        }
+      }
+    }
+  }
+  if constexpr (NA > 0) grid_reduce<NA>(acc, nd + k0 + k1, ws, a.result, red_sm);
+}
+
+template <int NA>
+static int launch_fused(const FusedDev& a, lg_ws* ws, cudaStream_t s) {
+  int g = vec_grid(a.n);
+  fused_kernel<NA><<<g, kThreads, 0, s>>>(a, *ws);
+  LG_LAUNCH_CHECK("fused_kernel");
+  return LG_OK;
+}
+
+// ---------------------------------------------------------------- GEMM --
+constexpr int kGemmMaxM = 64;
+constexpr int kGemmMaxP = 32;
+constexpr int kGemmMaxY = 1024;
+struct GemmArgs {
+  int64_t n;
+  const double* in;
+  int64_t ldi;
+  int m;
+  int p;
+  double* out;
+  int64_t ldo;
+  double y[kGemmMaxY];
+};
+
+template <int P>
+__global__ void __launch_bounds__(kThreads) gemm_small_kernel(const __grid_constant__ GemmArgs a) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += stride) {
+    double acc[P];
+#pragma unroll
+    for (int c = 0; c < P; ++c) acc[c] = 0.0;
+    for (int j = 0; j < a.m; ++j) {
+      double v = a.in[i + (int64_t)j * a.ldi];
+#pragma unroll
+      for (int c = 0; c < P; ++c)
+        if (c < a.p) acc[c] += v * a.y[j + c * a.m];
+    }
+#pragma unroll
+    for (int c = 0; c < P; ++c)
+      if (c < a.p) a.out[i + (int64_t)c * a.ldo] = acc[c];
+  }
+}
+
+__global__ void diag_apply_kernel(int64_t n, const double* dinv,
+                                  const double* r, double* z, const int* skip) {
+  if (skip && *skip) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += stride)
+    z[i] = r[i] * dinv[i];
+}
+
+}  // namespace lg
+
+using namespace lg;
+
+extern "C" {
+
+int lg_fused(const lg_fused_args* args, lg_ws* ws, void* stream) {
+  if (!args) return fail(LG_EINVAL, "lg_fused: NULL args");
+  const lg_fused_args& a = *args;
+  if (a.n < 0) return fail(LG_EINVAL, "lg_fused: negative n");
+  if (a.ndots < 0 || a.ndots > LG_MAXD || a.nblocks < 0 || a.nblocks > LG_MAXB)
+    return fail(LG_EINVAL, "lg_fused: too many dots / blocks");
+  int nq = 0;
+  for (int b = 0; b < a.nblocks; ++b) {
+    if (a.b[b].k < 0 || (a.b[b].k > 0 && (!a.b[b].q || !a.b[b].v || a.b[b].ld < a.n)))
+      return fail(LG_EINVAL, "lg_fused: bad block");
+    nq += a.b[b].k;
+  }
+  if (nq > LG_MAXQ) return fail(LG_EINVAL, "lg_fused: more than LG_MAXQ block columns");
+  for (int k = 0; k < LG_MAXO; ++k) {
+    const lg_output& o = a.o[k];
+    if (!o.out) continue;
+    if (o.nterms < 0 || o.nterms > LG_MAXT) return fail(LG_EINVAL, "lg_fused: bad term count");
+    for (int t = 0; t < o.nterms; ++t) {
+      if (!o.t[t].v) return fail(LG_EINVAL, "lg_fused: NULL term vector");
+      uintptr_t u = (uintptr_t)o.t[t].v;
+      if (u >= 1 && u <= LG_MAXO && (int)u > k)
+        return fail(LG_EINVAL, "lg_fused: term references a later output");
+      if (u >= 1 && u <= LG_MAXO && !a.o[u - 1].out)
+        return fail(LG_EINVAL, "lg_fused: term references a disabled output");
+    }
+    if (o.post_mode < 0 || o.post_mode > 3 || (o.post_mode && !o.d_post))
+      return fail(LG_EINVAL, "lg_fused: bad post scaling");
+    if (o.uk < 0 || o.uk > LG_MAXQ || (o.uk > 0 && (!o.uq || !o.uc || o.uld < a.n)))
+      return fail(LG_EINVAL, "lg_fused: bad update block");
+  }
+  for (int d = 0; d < a.ndots; ++d)
+    if (!a.da[d]) return fail(LG_EINVAL, "lg_fused: NULL dot operand");
+  int na = a.ndots + nq;
+  if (na > 0 && (!a.result || !ws)) return fail(LG_EINVAL, "lg_fused: dots need result and ws");
+  if (a.n == 0) {
+    if (na > 0) LG_CUDA(cudaMemsetAsync(a.result, 0, sizeof(double) * na, (cudaStream_t)stream));
+    return LG_OK;
+  }
+  FusedDev d;
+  d.n = a.n;
+  for (int k = 0; k < LG_MAXO; ++k) d.o[k] = a.o[k];
+  d.ndots = a.ndots;
+  for (int k = 0; k < LG_MAXD; ++k) {
+    d.da[k] = a.da[k];
+    d.db[k] = a.db[k];
+    d.dc[k] = a.dc[k];
+  }
+  d.nblocks = a.nblocks;
+  d.b[0] = a.b[0];
+  d.b[1] = a.b[1];
+  for (int b = a.nblocks; b < LG_MAXB; ++b) d.b[b].k = 0;
+  d.result = a.result;
+  d.skip = a.skip;
+  lg_ws dummy{};
+  lg_ws* w = ws ? ws : &dummy;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (na == 0) return launch_fused<0>(d, w, s);
+  if (na <= 4) return launch_fused<4>(d, w, s);
+  if (na <= 8) return launch_fused<8>(d, w, s);
+  if (na <= 16) return launch_fused<16>(d, w, s);
+  if (na <= 32) return launch_fused<32>(d, w, s);
+  return launch_fused<LG_MAXD + LG_MAXQ>(d, w, s);
+}
+
+int lg_gemm_small(int64_t n, const double* in, int64_t ldi, int m,
+                  const double* y_h, int p, double* out, int64_t ldo,
+                  void* stream) {
+  if (n < 0 || m < 0 || p < 0 || m > kGemmMaxM || p > kGemmMaxP || m * p > kGemmMaxY)
+    return fail(LG_EINVAL, "lg_gemm_small: bad shape (m <= 64, p <= 32, m*p <= 1024)");
+  if (n == 0 || p == 0) return LG_OK;
+  if (!out || ldo < n || (m > 0 && (!in || !y_h || ldi < n)))
+    return fail(LG_EINVAL, "lg_gemm_small: bad pointer / leading dimension");
+  static thread_local GemmArgs a;  // large by-value launch parameter (host staging)
+  a.n = n;
+  a.in = in;
+  a.ldi = ldi;
+  a.m = m;
+  a.p = p;
+  a.out = out;
+  a.ldo = ldo;
+  std::memcpy(a.y, y_h, sizeof(double) * (size_t)(m * p));
+  int g = vec_grid(n);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p <= 4) gemm_small_kernel<4><<<g, kThreads, 0, s>>>(a);
+  else if (p <= 8) gemm_small_kernel<8><<<g, kThreads, 0, s>>>(a);
+  else if (p <= 16) gemm_small_kernel<16><<<g, kThreads, 0, s>>>(a);
+  else gemm_small_kernel<32><<<g, kThreads, 0, s>>>(a);
+  LG_LAUNCH_CHECK("gemm_small_kernel");
+  return LG_OK;
+}
+
+int lg_diag_apply(int64_t n, const double* dinv, const double* r, double* z,
+                  const int* skip, void* stream) {
+  if (n < 0 || (n > 0 && (!dinv || !r || !z))) return fail(LG_EINVAL, "lg_diag_apply: bad argument");
+  if (n == 0) return LG_OK;
+  diag_apply_kernel<<<vec_grid(n), kThreads, 0, (cudaStream_t)stream>>>(n, dinv, r, z, skip);
+  LG_LAUNCH_CHECK("diag_apply_kernel");
+  return LG_OK;
+}
+
+}  // extern "C"
