@@ -161,12 +161,17 @@ typedef struct {
   double* out;         /* NULL: output disabled                            */
   int nterms;
   lg_term t[LG_MAXT];
-  /* optional block update: out -= sum_j (cscale * c[j]) Q[:, j]          */
+  /* optional block updates: out -= sum_j (cscale * c[j]) Q[:, j], for up
+   * to two column blocks (uq, uk, uc) and (uq2, uk2, uc2) with ld uld / uld2 */
   const double* uq;
   int64_t uld;
   int uk;
   const double* uc;    /* device coefficients (k of them)                  */
   double cscale;
+  const double* uq2;
+  int64_t uld2;
+  int uk2;
+  const double* uc2;
   /* optional final scaling by a device scalar p = *d_post:
    * post_mode 1: out *= p, 2: out /= p, 3: out /= sqrt(p)               */
   const double* d_post;

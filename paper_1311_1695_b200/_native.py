@@ -51,7 +51,8 @@ class Output(ctypes.Structure):
     _fields_ = [
         ("out", c_p), ("nterms", c_int), ("t", Term * LG_MAXT),
         ("uq", c_p), ("uld", c_i64), ("uk", c_int), ("uc", c_p),
-        ("cscale", c_dbl), ("d_post", c_p), ("post_mode", c_int),
+        ("cscale", c_dbl), ("uq2", c_p), ("uld2", c_i64), ("uk2", c_int), ("uc2", c_p),
+        ("d_post", c_p), ("post_mode", c_int),
     ]
 
 

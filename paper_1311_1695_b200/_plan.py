@@ -42,28 +42,33 @@ def _addr(x):
 class Slots:
     """Named scalar slots (device doubles) and flags (device int32)."""
 
-    NSLOT = 256
+    NSLOT = 256     # addressable by the scalar interpreter (uint8 indices)
     NFLAG = 32
 
-    def __init__(self, names=(), flags=()):
+    def __init__(self, names=(), flags=(), capacity=1024):
         t = dev.torch()
-        self.s = dev.zeros(self.NSLOT)
-        self.f = dev.zeros(self.NFLAG, dtype=t.int32)
+        self.cap = max(capacity, self.NSLOT)
+        # one device buffer: [flags (int32) | slots (double)] so a status
+        # readback is a single copy + synchronisation
+        self.buf = dev.zeros(4 * self.NFLAG + 8 * self.cap, dtype=t.uint8)
+        self.f = self.buf[:4 * self.NFLAG].view(t.int32)
+        self.s = self.buf[4 * self.NFLAG:].view(t.float64)
         self.idx = {}
         self.fidx = {}
         for nm in names:
             self.add(nm)
         for nm in flags:
             self.add_flag(nm)
-        self.pin_s = dev.Pinned(self.s)
-        self.pin_f = dev.Pinned(self.f)
+        self.pin = dev.Pinned(self.buf)
+        self._hf = self.pin.host[:4 * self.NFLAG].view(t.int32).numpy()
+        self._hs = self.pin.host[4 * self.NFLAG:].view(t.float64).numpy()
 
     def add(self, name, count=1):
         """Allocate `count` consecutive slots under `name` (idempotent)."""
         if name in self.idx:
             return self.idx[name]
         base = getattr(self, "_next", 0)
-        if base + count > self.NSLOT:
+        if base + count > self.cap:
             raise ValueError("scalar slot file exhausted")
         self.idx[name] = base
         self._next = base + count
@@ -85,8 +90,9 @@ class Slots:
 
     # host access (synchronising)
     def fetch(self):
-        st = dev.stream_ptr()
-        return self.pin_s.fetch(st), self.pin_f.fetch(st)
+        """(slots, flags) as host arrays after one copy + sync."""
+        self.pin.fetch(dev.stream_ptr())
+        return self._hs, self._hf
 
     def read(self, *names):
         s, _ = self.fetch()
@@ -124,7 +130,10 @@ class Prog:
             return name
         if name not in self.S.idx:
             self.S.add(name)
-        return self.S.idx[name]
+        i = self.S.idx[name]
+        if i >= Slots.NSLOT:
+            raise ValueError(f"slot {name!r} is beyond the interpreter's 256-slot window")
+        return i
 
     def emit(self, op, dst=0, a=0, b=0):
         self.ops.append(OPS[op] | (dst << 8) | (a << 16) | (b << 24))
@@ -208,6 +217,12 @@ class Fused:
                 cs = upd[3] if len(upd) > 3 else 1.0
                 qa, ld = self._qaddr(q)
                 oa.uq, oa.uld, oa.uk, oa.uc, oa.cscale = qa, ld, int(kk), cptr, float(cs)
+            upd2 = o.get("upd2")
+            if upd2 is not None:
+                qa, ld = self._qaddr(upd2[0])
+                oa.uq2, oa.uld2, oa.uk2, oa.uc2 = qa, ld, int(upd2[1]), upd2[2]
+                if upd is None:
+                    oa.cscale = float(upd2[3]) if len(upd2) > 3 else 1.0
             post = o.get("post")
             if post is not None:
                 oa.d_post, oa.post_mode = post[0], int(post[1])
@@ -238,7 +253,7 @@ class Fused:
             return q[0], q[1]
         return q.data_ptr(), q.shape[-1]
 
-    def set_k(self, block=None, upd=None):
+    def set_k(self, block=None, upd=None, upd2=None):
         """Change the live column count of a block dot / update (e.g. after a
         deflation basis grew) without rebuilding."""
         if block is not None:
@@ -247,6 +262,10 @@ class Fused:
         if upd is not None:
             oi, k = upd
             self.args.o[oi].uk = int(k)
+        if upd2 is not None:
+            oi, k = upd2
+            self.args.o[oi].uk2 = int(k)
+        self.nres = self.args.ndots + sum(self.args.b[i].k for i in range(self.args.nblocks))
 
     def __call__(self, ws=None, stream=None):
         ws = ws or dev.workspace()

@@ -46,17 +46,19 @@ __device__ __forceinline__ double pick(const double* p, int64_t i,
 
 __device__ __forceinline__ double output_value(const lg_output& o,
                                                const double* coef,
-                                               const double* uc, int64_t i,
+                                               const double* uc, const double* uc2, int64_t i,
                                                const double (&ov)[LG_MAXO],
                                                double post, int pmode) {
   double v = 0.0;
 #pragma unroll
   for (int t = 0; t < LG_MAXT; ++t)
     if (t < o.nterms) v += coef[t] * pick(o.t[t].v, i, ov);
-  if (o.uk > 0) {
-    const double* q = o.uq + i;
+  if (o.uk > 0 || o.uk2 > 0) {
     double s = 0.0;
+    const double* q = o.uq + i;
     for (int j = 0; j < o.uk; ++j) s += uc[j] * q[(int64_t)j * o.uld];
+    const double* q2 = o.uq2 + i;
+    for (int j = 0; j < o.uk2; ++j) s += uc2[j] * q2[(int64_t)j * o.uld2];
     v -= s;
   }
   if (pmode == 1) v *= post;
@@ -70,6 +72,7 @@ fused_kernel(FusedDev a, lg_ws ws) {
   if (a.skip && *a.skip) return;
   constexpr int M = NA > 0 ? NA : 1;
   __shared__ double uc_sm[LG_MAXO][LG_MAXQ];
+  __shared__ double uc2_sm[LG_MAXO][LG_MAXQ];
   __shared__ double red_sm[kWarps * M];
   double coef[LG_MAXO][LG_MAXT];
   double post[LG_MAXO] = {1.0, 1.0, 1.0};
@@ -93,6 +96,8 @@ fused_kernel(FusedDev a, lg_ws ws) {
     }
     for (int j = threadIdx.x; j < o.uk; j += blockDim.x)
       uc_sm[k][j] = o.cscale * o.uc[j];
+    for (int j = threadIdx.x; j < o.uk2; j += blockDim.x)
+      uc2_sm[k][j] = o.cscale * o.uc2[j];
   }
   __syncthreads();
 
@@ -110,7 +115,7 @@ fused_kernel(FusedDev a, lg_ws ws) {
 #pragma unroll
     for (int k = 0; k < LG_MAXO; ++k) {
       if (a.o[k].out) {
-        ov[k] = output_value(a.o[k], coef[k], uc_sm[k], i, ov, post[k], pmode[k]);
+        ov[k] = output_value(a.o[k], coef[k], uc_sm[k], uc2_sm[k], i, ov, post[k], pmode[k]);
         a.o[k].out[i] = ov[k];
       }
     }
@@ -223,6 +228,8 @@ int lg_fused(const lg_fused_args* args, lg_ws* ws, void* stream) {
       return fail(LG_EINVAL, "lg_fused: bad post scaling");
     if (o.uk < 0 || o.uk > LG_MAXQ || (o.uk > 0 && (!o.uq || !o.uc || o.uld < a.n)))
       return fail(LG_EINVAL, "lg_fused: bad update block");
+    if (o.uk2 < 0 || o.uk2 > LG_MAXQ || (o.uk2 > 0 && (!o.uq2 || !o.uc2 || o.uld2 < a.n)))
+      return fail(LG_EINVAL, "lg_fused: bad second update block");
   }
   for (int d = 0; d < a.ndots; ++d)
     if (!a.da[d]) return fail(LG_EINVAL, "lg_fused: NULL dot operand");
