@@ -1,0 +1,360 @@
+"""Benchmark: Laplacian SpMV GB/s & matvecs/s, and wall time to k smallest
+eigenpairs (DACG / JD), on the BASELINE configuration C4 (weighted
+Chung-Lu, n = 1e6, power-law exponent 2.5, mean degree 10, Geometric(0.5)
+integer weights, largest component: n = 989,777, nnz = 10,907,457).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config C4] [--no-solve]
+
+A "step" is one Laplacian matvec y = L x of the whole graph.  value is
+matvecs/s of the fused device SpMV with inputs resident in HBM (L2 flushed
+between steps by writing a 256 MiB buffer outside the timed events); e2e is
+the same metric through the public API spmv(a, x) with host numpy buffers
+(H2D of x + D2H of y inside the timed region).  roofline uses the SURVEY
+8(d) byte model (12 nnz + 8 (n+1) + 16 n per matvec) against the measured
+HBM copy bandwidth in MEASURED_PEAKS.json.  cpu_baseline times the oracle's
+restatement of the reference SpMV (np.add.reduceat per row,
+sparse.py:128-139) on this host.  The solve block reports DACG and JD wall
+time to 5 eigenpairs at delta = 1e-8 (the configuration of the reference
+runs recorded in tests/golden/config_C4.json).
+
+With N > 1 (torchrun, one rank per GPU) the matrix is row-partitioned by
+nonzeros; every step all-gathers x over NCCL and multiplies the local row
+block (strong scaling: the whole-job value is matvecs/s of the global
+matrix, timed as the max over ranks).
+
+--impl reference runs the CPU reference arm: the oracle's restatement of the
+reference SpMV, row-chunked over all host threads, on rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Laplacian SpMV matvecs/s (C4 weighted Chung-Lu 1M); wall time to k eigenpairs"
+UNIT = "matvecs/s"
+
+
+def _peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def build_graph(config):
+    from paper_1311_1695_b200.generators import config_graph
+    return config_graph(config)
+
+
+from paper_1311_1695_b200.dist import SliceGather, partition_rows  # noqa: E402
+
+
+def cpu_spmv_threads(rp, col, val, x, nthreads, chunks):
+    """Oracle SpMV (reduceat per row, sparse.py:135-139) over row chunks in
+    a thread pool (numpy releases the GIL inside the ufunc loops)."""
+    from concurrent.futures import ThreadPoolExecutor
+    y = np.zeros(len(rp) - 1)
+
+    def work(c):
+        r0, r1 = c
+        lo, hi = rp[r0], rp[r1]
+        seg = val[lo:hi] * x[col[lo:hi]]
+        lens = np.diff(rp[r0:r1 + 1])
+        nz = np.flatnonzero(lens > 0)
+        if nz.size:
+            y[r0 + nz] = np.add.reduceat(seg, (rp[r0:r1] - lo)[nz])
+    if nthreads == 1:
+        for c in chunks:
+            work(c)
+    else:
+        with ThreadPoolExecutor(nthreads) as ex:
+            list(ex.map(work, chunks))
+    return y
+
+
+def reference_arm(args):
+    """CPU reference arm: the oracle restatement of the reference SpMV."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import lapeig_oracle as O
+    g = build_graph(args.config)
+    rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+    n, nnz = g.n_nodes, int(rp[-1])
+    x = np.random.default_rng(0).standard_normal(n)
+    nthreads = os.cpu_count() or 1
+    cuts = partition_rows(rp, nthreads * 4)
+    chunks = [(cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1)]
+    y_ref = O.spmv(O.Csr(n, rp, col, val), x)
+    y = cpu_spmv_threads(rp, col, val, x, nthreads, chunks)
+    assert np.allclose(y, y_ref, rtol=1e-13, atol=1e-12)
+    for _ in range(args.warmup):
+        cpu_spmv_threads(rp, col, val, x, nthreads, chunks)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_spmv_threads(rp, col, val, x, nthreads, chunks)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    value = 1e3 / ms
+    algo = 12 * nnz + 8 * (n + 1) + 16 * n
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: SpMV of the weighted Laplacian",
+                   "n": n, "nnz": nnz},
+        "effective_gbs": algo / (ms * 1e-3) / 1e9,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
+                         "sample": f"{args.steps} full {args.config} matvecs, oracle reduceat "
+                                   f"SpMV row-chunked over {nthreads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_sample(g, seconds=10.0):
+    """Single-thread oracle SpMV (the reference's algorithm) for a bounded
+    sample of ~seconds (rank 0, N = 1 only)."""
+    from oracle import lapeig_oracle as O
+    rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+    a = O.Csr(g.n_nodes, rp, col, val)
+    x = np.random.default_rng(0).standard_normal(a.n)
+    O.spmv(a, x)
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds and reps < 200:
+        O.spmv(a, x)
+        reps += 1
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{reps} oracle matvecs (np.add.reduceat, sparse.py:128-139) in "
+                      f"{reps * dt:.1f} s on one host core"}
+
+
+def solve_block(a, f):
+    """Wall time to 5 eigenpairs (delta 1e-8) with DACG and JD on the device."""
+    import torch
+    import paper_1311_1695_b200 as L
+    ref = {}
+    try:
+        ref = json.loads((ROOT / "tests/golden/config_C4.json").read_text())["solvers"]
+    except Exception:
+        pass
+    out = {}
+    for name, fn in (("dacg", L.dacg_smallest), ("jd", L.jd_smallest)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pairs, rep = fn(a, 5, delta=1e-8, f=f)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        r = ref.get(name, {})
+        err = None
+        if r.get("eigenvalues"):
+            err = float(np.max(np.abs(pairs.values - r["eigenvalues"]) /
+                               np.abs(r["eigenvalues"])))
+        out[name] = {"wall_s": wall, "mvp": rep.mvp, "neig": 5, "delta": 1e-8,
+                     "eig_relerr_vs_reference": err,
+                     "reference_wall_s_build_container": r.get("wall_seconds"),
+                     "reference_mvp": r.get("mvp")}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200.sparse import DeviceCsr
+
+    g = build_graph(args.config)
+    a = L.build_laplacian(g)
+    n, nnz = a.n, a.nnz
+    cuts = partition_rows(a.row_ptr, world)
+    r0, r1 = cuts[rank], cuts[rank + 1]
+    if world == 1:
+        d = a.device()
+    else:
+        lo, hi = int(a.row_ptr[r0]), int(a.row_ptr[r1])
+        # local row block as a rectangular operator: rows r0..r1, all columns
+        # (square n x n CSR with empty rows outside the block)
+        rp = np.zeros(n + 1, dtype=np.int64)
+        rp[r0 + 1:r1 + 1] = a.row_ptr[r0 + 1:r1 + 1] - lo
+        rp[r1 + 1:] = hi - lo
+        d = DeviceCsr(n, rp, a.col_idx[lo:hi], a.values[lo:hi])
+    x = dev.to_device(np.random.default_rng(0).standard_normal(n))
+    y = dev.empty(n)
+    counts = [cuts[i + 1] - cuts[i] for i in range(world)]
+    gather = SliceGather(dist, counts, rank, x) if world > 1 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if gather is not None:
+            # exchange: every rank owns rows r0..r1 of the iterate; the
+            # matvec needs all of x
+            gather(x)
+        d.matvec(x, y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)            # evict L2 between steps (not timed)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = float(np.mean(step_ms))
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = 1e3 / ms
+    algo = 12 * nnz + 8 * (n + 1) + 16 * n
+    # kernel-only roofline (the SpMV launch of this rank)
+    local_nnz = int(a.row_ptr[r1] - a.row_ptr[r0])
+    local_rows = r1 - r0
+    local_algo = 12 * local_nnz + 8 * (local_rows + 1) + 16 * local_rows + 8 * (n - local_rows)
+    peaks, peak_kind = _peaks()
+    # e2e through the public API with host buffers (rank 0 replica path)
+    xh = np.random.default_rng(1).standard_normal(n)
+    e2e = None
+    if world == 1:
+        for _ in range(3):
+            L.spmv(a, xh)
+        torch.cuda.synchronize()
+        reps = max(5, min(args.steps, 30))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            L.spmv(a, xh)
+        e2e_s = (time.perf_counter() - t0) / reps
+        e2e = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n,
+               "path": "paper_1311_1695_b200.spmv(a, numpy x) -> numpy y"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: one SpMV of the weighted Laplacian "
+                               f"(BASELINE configs[3], LCC)", "n": n, "nnz": nnz,
+                   "l2": "flushed between steps (256 MiB write, untimed)",
+                   "parallelism": f"rows{world}" if world > 1 else "single"},
+        "effective_gbs": algo / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": local_algo / (ms * 1e-3) / 1e9,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": local_algo / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                     "traffic": None, "peak_kind": peak_kind,
+                     "bytes_per_launch": local_algo,
+                     "bytes_model": "12 nnz + 8 (n+1) + 16 n (SURVEY 8(d))"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_solve:
+        f = L.ic0_factorize(a)
+        line["solve"] = solve_block(a, f)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_sample(g)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -96,6 +96,8 @@ def to_device(x):
         x = x.to(device=device(), dtype=t.float64)
         return x.contiguous()
     arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if not arr.flags.writeable:
+        arr = arr.copy()
     return t.from_numpy(arr).to(device())
 
 

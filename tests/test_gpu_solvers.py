@@ -1,0 +1,188 @@
+"""Device eigensolvers vs the reference (golden results of the reference
+run in the build container).
+
+Bars (north star): eigenvalues within 1e-8 relative of the reference's;
+residual ||L u - theta u|| / theta within the solver tolerance for every
+returned pair; orthonormal vectors; MVP counts identical for DACG / IRLM
+and within 5 % for JD (roundoff reorders JD's inner stopping).
+"""
+
+import numpy as np
+import pytest
+
+from tests.conftest import golden_config, kat_edges
+
+pytestmark = pytest.mark.gpu
+
+KAT = ["P3", "P4", "P10w", "C4", "C7", "K3", "K6", "S4", "S9", "grid4x5", "rand15",
+       "rand50", "rand200", "geo1000"]
+
+
+@pytest.fixture(scope="module")
+def L():
+    import paper_1311_1695_b200 as lib
+    return lib
+
+
+def solver(L, name):
+    return {"dacg": L.dacg_smallest, "jd": L.jd_smallest, "irlm": L.irlm_smallest}[name]
+
+
+def check_pairs(L, a, pairs, want, delta):
+    vals = pairs.values
+    assert np.max(np.abs(vals - want) / np.abs(want)) <= 1e-8
+    th, rs = L.rayleigh_residuals(a, pairs.vectors)
+    assert np.all(rs <= delta * 1.0000001)
+    assert pairs.gram_defect() <= 1e-8
+    assert pairs.kernel_overlap() <= 1e-8
+
+
+@pytest.mark.parametrize("name", KAT)
+@pytest.mark.parametrize("sv", ["dacg", "jd", "irlm"])
+def test_kat_graphs(L, kat, name, sv):
+    graphs, _, results = kat
+    info = results[name]
+    ref = info["solvers"][sv]
+    n, i, j, w = kat_edges(graphs, name)
+    a = L.build_laplacian(L.graphs.EdgeList.from_canonical(n, i, j, w))
+    f = L.ic0_factorize(a)
+    c = L.MvpCounter()
+    pairs, rep = solver(L, sv)(a, info["neig"], delta=info["delta"], f=f, counter=c)
+    check_pairs(L, a, pairs, np.asarray(ref["eigenvalues"]), info["delta"])
+    assert rep.mvp == c.count
+    if sv == "jd":
+        assert abs(rep.mvp - ref["mvp"]) <= max(2, 0.05 * ref["mvp"])
+    else:
+        assert abs(rep.mvp - ref["mvp"]) <= max(2, 0.002 * ref["mvp"])
+
+
+def test_known_answers(L):
+    p3 = L.build_laplacian(L.path_graph(3))
+    for sv in ("dacg", "jd", "irlm"):
+        pairs, _ = solver(L, sv)(p3, 1, delta=1e-10)
+        assert pairs.values[0] == pytest.approx(1.0, abs=1e-10)
+        v = pairs.vectors[:, 0] * np.sign(pairs.vectors[0, 0])
+        assert np.allclose(v, [1 / np.sqrt(2), 0, -1 / np.sqrt(2)], atol=1e-8)
+    for g, want in ((L.complete_graph(3), [3, 3]), (L.star_graph(3), [1, 1, 4]),
+                    (L.cycle_graph(4), [2, 2])):
+        a = L.build_laplacian(g)
+        for sv in ("dacg", "jd", "irlm"):
+            pairs, _ = solver(L, sv)(a, len(want), delta=1e-10)
+            assert np.allclose(pairs.values, want, rtol=1e-9)
+
+
+def test_accounting_identities(L, kat):
+    graphs, _, _ = kat
+    n, i, j, w = kat_edges(graphs, "rand50")
+    a = L.build_laplacian(L.graphs.EdgeList.from_canonical(n, i, j, w))
+    _, rep = L.dacg_smallest(a, 4, delta=1e-8)
+    cfg = rep.config
+    assert rep.mvp == cfg["mvp_setup"] + cfg["mvp_verify"] + rep.inner_its_total
+    _, rep = L.jd_smallest(a, 4, delta=1e-8)
+    assert rep.mvp == rep.config["mvp_outer"] + rep.config["mvp_verify"] + rep.inner_its_total
+    _, rep = L.irlm_smallest(a, 4, delta=1e-8)
+    assert rep.mvp == rep.inner_its_total + rep.config["mvp_verify"]
+
+
+def test_deterministic_for_fixed_seed(L, kat):
+    graphs, _, _ = kat
+    n, i, j, w = kat_edges(graphs, "rand200")
+    a = L.build_laplacian(L.graphs.EdgeList.from_canonical(n, i, j, w))
+    for sv in ("dacg", "jd", "irlm"):
+        p1, r1 = solver(L, sv)(a, 3, delta=1e-8, seed=4)
+        p2, r2 = solver(L, sv)(a, 3, delta=1e-8, seed=4)
+        assert np.array_equal(p1.values, p2.values) and r1.mvp == r2.mvp
+        assert np.array_equal(p1.vectors, p2.vectors)
+
+
+def test_errors_mirror_reference(L):
+    a = L.build_laplacian(L.path_graph(4))
+    for sv in ("dacg", "jd", "irlm"):
+        with pytest.raises(ValueError):
+            solver(L, sv)(a, 4)
+        with pytest.raises(ValueError):
+            solver(L, sv)(a, 0)
+    g = L.build_laplacian(L.config_graph("C1"))
+    with pytest.raises(L.SolverError) as exc:
+        L.dacg_smallest(g, 2, delta=1e-12, maxit_per_pair=3)
+    assert exc.value.stalled_pair == 0 and len(exc.value.partial) == 0
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_baseline_small_configs(L, cfg):
+    ref = golden_config(cfg)
+    a = L.build_laplacian(L.config_graph(cfg))
+    f = L.ic0_factorize(a)
+    for sv, rr in ref["solvers"].items():
+        pairs, rep = solver(L, sv)(a, ref["neig"], delta=ref["delta"], f=f)
+        check_pairs(L, a, pairs, np.asarray(rr["eigenvalues"]), ref["delta"])
+        if sv == "jd":
+            assert abs(rep.mvp - rr["mvp"]) <= 0.05 * rr["mvp"]
+        else:
+            assert rep.mvp == rr["mvp"]
+    vecs = np.load(f"tests/golden/config_{cfg}_vecs.npz")["dacg"]
+    pairs, _ = L.dacg_smallest(a, ref["neig"], delta=ref["delta"], f=f)
+    # subspace angles against the reference eigenvectors
+    s = np.linalg.svd(vecs.T @ pairs.vectors, compute_uv=False)
+    assert np.min(s) >= np.cos(1e-6)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_baseline_large_configs(L, cfg):
+    ref = golden_config(cfg)
+    a = L.build_laplacian(L.config_graph(cfg))
+    f = L.ic0_factorize(a)
+    for sv, rr in ref["solvers"].items():
+        pairs, rep = solver(L, sv)(a, ref["neig"], delta=ref["delta"], f=f)
+        check_pairs(L, a, pairs, np.asarray(rr["eigenvalues"]), ref["delta"])
+        assert abs(rep.mvp - rr["mvp"]) <= 0.05 * rr["mvp"]
+
+
+def test_generic_pcg_and_projection_api(L, rng):
+    import torch
+    from tests.conftest import ROOT  # noqa: F401
+    n = 60
+    dense = rng.standard_normal((n, n))
+    dense = dense @ dense.T + n * np.eye(n)
+    r, c = np.nonzero(dense)
+    a = L.CsrMatrix.from_coo(n, r, c, dense[r, c], symmetric=True)
+    b = rng.standard_normal(n)
+    out = L.pcg_solve(lambda x, cnt: L.spmv(a, x, cnt), None, b, 1e-12, 10 * n)
+    assert out.converged
+    assert np.linalg.norm(out.solution - np.linalg.solve(dense, b)) <= 1e-8 * np.linalg.norm(b)
+    basis = L.DeflationBasis(np.linalg.qr(rng.standard_normal((12, 4)))[0])
+    v = rng.standard_normal(12)
+    w = basis.project_out(v)
+    assert np.abs(basis.columns.T @ w).max() <= 1e-12
+    wd = basis.project_out(torch.from_numpy(v).cuda())
+    assert wd.is_cuda and np.allclose(wd.cpu().numpy(), w, atol=1e-15)
+    u, nrm = L.mgs_orthonormalize(rng.standard_normal(12), basis.columns)
+    assert abs(np.linalg.norm(u) - 1) <= 1e-14 and np.abs(basis.columns.T @ u).max() <= 1e-13
+    with pytest.raises(L.GramSchmidtBreakdown):
+        L.mgs_orthonormalize(basis.columns[:, 0] * 3.0, basis.columns)
+
+
+def test_jd_and_irlm_seams(L):
+    from paper_1311_1695_b200.irlm import LanczosState, inverse_lanczos_step
+    from paper_1311_1695_b200.jd import JdWorkspace, jd_restart, rayleigh_ritz_extract
+    a = L.build_laplacian(L.path_graph(6))
+    ws = JdWorkspace(6, 2, 4)
+    e = np.eye(6)
+    for k in (1, 2, 3):
+        ws.append(e[:, k], L.spmv(a, e[:, k]))
+    dense = a.toarray()
+    assert np.allclose(ws.h, dense[1:4, 1:4])
+    theta, u, r = rayleigh_ritz_extract(ws)
+    assert np.allclose(r, dense @ u - theta * u, atol=1e-12)
+    jd_restart(ws)
+    assert ws.m == 2 and np.allclose(ws.v.T @ ws.v, np.eye(2), atol=1e-12)
+    f = L.ic0_factorize(a)
+    null = L.kernel_basis(6)
+    v1, _ = L.mgs_orthonormalize(np.arange(6.0), null.columns)
+    st = LanczosState(v1, 5)
+    c = L.MvpCounter()
+    inverse_lanczos_step(st, a, f, 1e-12, null, counter=c)
+    assert st.m == 1 and c.count == st.last_inner_its > 0
+    B = st.basis_matrix()
+    assert np.allclose(B.T @ B, np.eye(B.shape[1]), atol=1e-12)

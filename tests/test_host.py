@@ -1,0 +1,183 @@
+"""Host-side logic that needs no GPU: the C ABI library loads and exports
+its header, the bit-exact host IC(0) factorization, input validation that
+mirrors the reference, generators, and the no-fallback guarantee."""
+
+import hashlib
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT, cuda_ok, golden_config, kat_edges
+
+
+def header_symbols():
+    text = (ROOT / "include" / "lapb200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(lg_\w+)\(", text, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    import ctypes
+    from paper_1311_1695_b200 import _native
+    lib = _native.load()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), f"{s} missing from liblapb200.so"
+    assert set(syms) == set(_native.EXPORTED)
+    assert lib.lg_version() >= 100
+    assert isinstance(ctypes.CDLL(str(_native.LIB_PATH)), ctypes.CDLL)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    from paper_1311_1695_b200 import _native
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_native.LIB_PATH)],
+                         capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.parametrize("name", ["P4", "grid4x5", "rand50", "rand200", "geo1000"])
+def test_host_ic0_factor_bit_exact(kat, name):
+    """lg_ic0_factorize (host C++) reproduces the reference factor bit for bit."""
+    from paper_1311_1695_b200.ic0 import ic0_factorize
+    from paper_1311_1695_b200.sparse import CsrMatrix
+    graphs, arrays, results = kat
+    n = int(graphs[name + "_n"][0])
+    a = CsrMatrix(n, arrays[name + "_rp"], arrays[name + "_col"], arrays[name + "_val"],
+                  symmetric=True)
+    f = ic0_factorize(a)
+    assert np.array_equal(f.l.row_ptr, arrays[name + "_lrp"])
+    assert np.array_equal(f.l.col_idx, arrays[name + "_lcol"])
+    assert np.array_equal(f.l.values.view(np.int64), arrays[name + "_lval"].view(np.int64))
+    assert f.shift == results[name]["ic0_shift"]
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_host_ic0_factor_configs(cfg):
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200.generators import config_graph
+    from paper_1311_1695_b200.ic0 import ic0_factorize
+    from paper_1311_1695_b200.sparse import CsrMatrix
+    ref = golden_config(cfg)
+    g = config_graph(cfg)
+    rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+    f = ic0_factorize(CsrMatrix(g.n_nodes, rp, col, val, symmetric=True))
+    h = hashlib.sha256()
+    for x in (f.l.row_ptr, f.l.col_idx, f.l.values):
+        h.update(np.ascontiguousarray(x).tobytes())
+    assert h.hexdigest() == ref["ic0_sha256"]
+
+
+def test_ic0_shift_ladder_and_breakdown():
+    from paper_1311_1695_b200.ic0 import Ic0Error, ic0_factorize
+    from paper_1311_1695_b200.sparse import CsrMatrix
+    # an indefinite symmetric matrix: every shift fails until 0.1 * max diag
+    dense = np.array([[1.0, 1.05], [1.05, 1.0]])
+    r, c = np.nonzero(dense)
+    a = CsrMatrix.from_coo(2, r, c, dense[r, c], symmetric=True)
+    f = ic0_factorize(a)
+    assert f.attempts == 7 and f.shift == pytest.approx(0.1)
+    f2 = ic0_factorize(a, shift0=0.2)
+    assert f2.attempts == 1 and f2.shift == 0.2
+    neg = CsrMatrix.from_coo(2, [0, 1], [0, 1], [-1.0, -1.0], symmetric=True)
+    with pytest.raises(Ic0Error):
+        ic0_factorize(neg)
+    with pytest.raises(ValueError):
+        ic0_factorize(CsrMatrix.identity(3).__class__(3, [0, 1, 2, 3], [0, 1, 2], [1, 1, 1]))
+
+
+def test_csr_validation_mirrors_reference():
+    from paper_1311_1695_b200.sparse import CsrMatrix, MvpCounter
+    with pytest.raises(ValueError):
+        CsrMatrix(2, [0, 1], [0], [1.0])
+    with pytest.raises(ValueError):
+        CsrMatrix(2, [1, 1, 2], [0, 1], [1.0, 1.0])
+    with pytest.raises(ValueError):
+        CsrMatrix(2, [0, 2, 1], [0, 1], [1.0, 1.0])
+    with pytest.raises(ValueError):
+        CsrMatrix(2, [0, 2, 2], [1, 0], [1.0, 1.0])
+    with pytest.raises(ValueError):
+        CsrMatrix(2, [0, 1, 2], [0, 5], [1.0, 1.0])
+    with pytest.raises(ValueError):
+        CsrMatrix.from_coo(2, [0, 0], [1, 1], [1.0, 2.0])
+    a = CsrMatrix.from_coo(3, [2, 0, 1], [0, 2, 1], [1.0, 2.0, 3.0])
+    assert a.nnz == 3 and np.allclose(a.toarray(), [[0, 0, 2], [0, 3, 0], [1, 0, 0]])
+    assert np.allclose(a.diagonal(), [0, 3, 0])
+    c = MvpCounter()
+    c.increment()
+    c.increment(4)
+    assert c.count == 5 and "5" in repr(c)
+
+
+def test_edgelist_canonicalisation_and_errors():
+    from paper_1311_1695_b200.graphs import EdgeList
+    g = EdgeList(4, [3, 1, 0], [1, 2, 2], [1.0, 2.0, 3.0])
+    assert g.i.tolist() == [0, 1, 1] and g.j.tolist() == [2, 2, 3]
+    for bad in ([(0, 0, 1.0)], [(0, 1, 0.0)], [(0, 1, 1.0), (1, 0, 2.0)], [(0, 9, 1.0)]):
+        with pytest.raises(ValueError):
+            EdgeList.from_pairs(4, bad)
+    with pytest.raises(ValueError):
+        EdgeList(0, [], [], [])
+
+
+def test_components_and_lcc():
+    from paper_1311_1695_b200.graphs import EdgeList, connected_components, largest_component
+    g = EdgeList(7, [0, 1, 3, 4, 5], [1, 2, 4, 5, 6], np.ones(5))
+    count, labels = connected_components(g)
+    assert count == 2 and labels[0] == 0 and labels[3] == 1
+    sub, node_map = largest_component(g)
+    assert sub.n_nodes == 4 and node_map[0] == -1 and node_map[3] == 0
+
+
+def test_generators_match_baseline_sizes():
+    from paper_1311_1695_b200.generators import config_graph
+    for cfg in ("C1", "C2"):
+        ref = golden_config(cfg)
+        g = config_graph(cfg)
+        assert (g.n_nodes, g.m) == (ref["n"], ref["m"])
+
+
+def test_dense_eig_and_ncv():
+    from paper_1311_1695_b200.irlm import ncv_for
+    from paper_1311_1695_b200.kernels import dense_sym_eig, tridiag_eig
+    rng = np.random.default_rng(0)
+    h = rng.standard_normal((6, 6))
+    h = h + h.T
+    w, v = dense_sym_eig(h)
+    assert np.allclose(w, np.linalg.eigvalsh(h)) and np.allclose(v.T @ v, np.eye(6))
+    with pytest.raises(ValueError):
+        dense_sym_eig(np.triu(h) + 1.0)
+    with pytest.raises(ValueError):
+        dense_sym_eig(np.eye(3), max_dim=2)
+    w, _ = tridiag_eig([2.0, 2.0, 2.0], [-1.0, -1.0])
+    assert np.allclose(w, 2 - 2 * np.cos(np.pi * np.arange(1, 4) / 4))
+    assert [ncv_for(k) for k in (1, 5, 20, 50, 60)] == [15, 30, 60, 120, 140]
+    with pytest.raises(ValueError):
+        ncv_for(0)
+
+
+def test_deflation_basis_validation():
+    from paper_1311_1695_b200.pcg import DeflationBasis, kernel_basis
+    with pytest.raises(ValueError):
+        DeflationBasis(np.ones((4, 2)))
+    with pytest.raises(ValueError):
+        DeflationBasis.single(np.zeros(3))
+    kb = kernel_basis(5, labels=np.array([0, 0, 1, 1, 1]))
+    assert kb.k == 2 and np.allclose(kb.columns[:2, 0], 1 / np.sqrt(2))
+    assert np.allclose(kernel_basis(4).columns[:, 0], 0.5)
+
+
+@pytest.mark.skipif(cuda_ok(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback():
+    """Every compute entry point raises without a CUDA device."""
+    from paper_1311_1695_b200.sparse import CsrMatrix, spmv
+    a = CsrMatrix.identity(3)
+    with pytest.raises(RuntimeError):
+        spmv(a, np.ones(3))
+    from paper_1311_1695_b200.graphs import EdgeList, build_laplacian
+    with pytest.raises(RuntimeError):
+        build_laplacian(EdgeList(2, [0], [1], [1.0]))
