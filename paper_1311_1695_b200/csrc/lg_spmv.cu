@@ -19,6 +19,14 @@
 //   * the epilogue fuses the theta shift (JD's L - theta I, pcg.py:171-172)
 //     and dot products of y with up to LG_MAXD vectors and a column block Q
 //     (the Q^T y half of the next deflation projection, pcg.py:60).
+//   * packed Laplacian format (default when it applies): a graph Laplacian's
+//     off-diagonal values are -w for a handful of distinct weights (unit
+//     graphs: one; C4's Geometric(0.5) counts: 30), so each off-diagonal
+//     nonzero is one 32-bit word -- column in the low cbits, index into a
+//     value table (shared memory) in the high bits -- and the diagonal is a
+//     separate n-vector.  4 bytes per nonzero instead of 12 (f64 value +
+//     int32 column): the SpMV streams 2.2x fewer bytes on C4 and the value
+//     actually multiplied is bit-identical to the stored one.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -29,12 +37,13 @@ namespace lg {
 
 constexpr int kChunk = 2048;   // nonzeros per row block (16 KB of products)
 constexpr int kRowCap = 1024;  // rows per normal block
+constexpr int kShortRow = 32;  // rows up to this length: one thread each
 
 struct SpmvBlock {
   int64_t nz0, nz1;  // nonzero range
   int32_t row0;      // first row
   int32_t nrows;     // rows (normal) / long-row id (long)
-  int32_t lanes;     // lanes per row (normal); 0 marks a long-row part
+  int32_t lshift;    // log2(lanes per row) (normal); -1 marks a long-row part
   int32_t part;      // compact long-part slot (long)
 };
 
@@ -49,17 +58,33 @@ struct lg_csr {
   int64_t nblocks = 0;
   int64_t nlong = 0;
   int64_t nparts = 0;              // total long-row parts
+  // packed Laplacian format (see header)
+  int packed = 0;
+  int cbits = 0;
+  int nvals = 0;
+  int64_t noff = 0;                // off-diagonal nonzeros
+  int64_t* prp = nullptr;          // off-diagonal row pointers [n+1]
+  uint32_t* pcol = nullptr;        // col | vidx << cbits
+  double* pdiag = nullptr;         // diagonal [n]
+  double* table = nullptr;         // distinct off-diagonal values [nvals]
   int32_t* long_nparts = nullptr;  // device [nlong]
   int64_t* long_first = nullptr;   // device [nlong] slot of part 0
 };
 
 namespace lg {
 
+constexpr int kMaxTable = 2048;   // value-table entries kept in shared memory
+
 struct SpmvArgs {
   int64_t n;
-  const int64_t* row_ptr;
+  const int64_t* row_ptr;   // plain: row_ptr; packed: off-diagonal row ptr
   const int32_t* col;
   const double* val;
+  const uint32_t* pcol;     // packed entries (NULL: plain format)
+  const double* pdiag;
+  const double* table;
+  int nvals;
+  int cbits;
   const SpmvBlock* blocks;
   int64_t nblocks;
   const int32_t* long_nparts;
@@ -97,49 +122,102 @@ __device__ __forceinline__ void epilogue_row(const SpmvArgs& a, int64_t r,
   }
 }
 
-template <int NA>
+template <bool PACKED>
+__device__ __forceinline__ double product(const SpmvArgs& a, int64_t k,
+                                          const double* tab, uint32_t cmask) {
+  if constexpr (PACKED) {
+    const uint32_t w = __ldcs(a.pcol + k);
+    return tab[w >> a.cbits] * __ldg(a.x + (w & cmask));
+  } else {
+    return ld_stream(a.val + k) * __ldg(a.x + ld_stream(a.col + k));
+  }
+}
+
+template <bool PACKED>
+__device__ __forceinline__ double finish_row(const SpmvArgs& a, int64_t r, double s,
+                                             double theta) {
+  if constexpr (PACKED) s += a.pdiag[r] * __ldg(a.x + r);
+  if (theta != 0.0) s -= theta * __ldg(a.x + r);
+  return s;
+}
+
+template <int NA, bool PACKED>
 __global__ void __launch_bounds__(kThreads)
 spmv_kernel(SpmvArgs a, lg_ws ws) {
   if (a.skip && *a.skip) return;
   __shared__ double sm[kChunk];
+  extern __shared__ double tab_sm[];   // packed value table (nvals)
   __shared__ double red_sm[kWarps * (NA > 0 ? NA : 1)];
   __shared__ int fin_flag;
+  __shared__ int wcnt_sm[kWarps];
+  __shared__ int list_sm[kRowCap];
   double acc[NA > 0 ? NA : 1];
 #pragma unroll
   for (int d = 0; d < (NA > 0 ? NA : 1); ++d) acc[d] = 0.0;
   double theta = a.theta_h;
   if (a.theta_d) theta += a.theta_neg ? -*a.theta_d : *a.theta_d;
   const int tid = threadIdx.x;
+  const uint32_t cmask = PACKED ? ((1u << a.cbits) - 1u) : 0u;
+  if constexpr (PACKED) {
+    for (int i = tid; i < a.nvals; i += kThreads) tab_sm[i] = a.table[i];
+    __syncthreads();
+  }
 
   for (int64_t b = blockIdx.x; b < a.nblocks; b += gridDim.x) {
     const SpmvBlock blk = a.blocks[b];
     const int cnt = (int)(blk.nz1 - blk.nz0);
-    if (blk.lanes > 0) {
+    if (blk.lshift >= 0) {
       // ---- normal block: stream products into shared memory
 #pragma unroll 8
-      for (int e = tid; e < cnt; e += kThreads) {
-        int64_t k = blk.nz0 + e;
-        sm[e] = ld_stream(a.val + k) * __ldg(a.x + ld_stream(a.col + k));
-      }
+      for (int e = tid; e < cnt; e += kThreads)
+        sm[e] = product<PACKED>(a, blk.nz0 + e, tab_sm, cmask);
       __syncthreads();
-      const int L = blk.lanes;
-      const int groups = kThreads / L;
-      const int g = tid / L, li = tid % L;
-      for (int base = 0; base < blk.nrows; base += groups) {
-        const int rr = base + g;
-        double s = 0.0;
-        int64_t r = blk.row0 + rr;
+      // phase A: one thread per row for rows of at most kShortRow entries;
+      // longer rows are compacted (in row order, via ballots) into a list
+      int nlist = 0;
+      for (int base = 0; base < blk.nrows; base += kThreads) {
+        const int rr = base + tid;
+        bool is_long = false;
         if (rr < blk.nrows) {
-          int lo = (int)(a.row_ptr[r] - blk.nz0);
-          int hi = (int)(a.row_ptr[r + 1] - blk.nz0);
-          for (int e = lo + li; e < hi; e += L) s += sm[e];
+          const int64_t r = blk.row0 + rr;
+          const int lo = (int)(a.row_ptr[r] - blk.nz0);
+          const int hi = (int)(a.row_ptr[r + 1] - blk.nz0);
+          if (hi - lo <= kShortRow) {
+            double sacc = 0.0;
+            for (int e = lo; e < hi; ++e) sacc += sm[e];
+            const double yr = finish_row<PACKED>(a, r, sacc, theta);
+            a.y[r] = yr;
+            epilogue_row<NA>(a, r, yr, acc);
+          } else {
+            is_long = true;
+          }
         }
-        for (int o = L >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (rr < blk.nrows && li == 0) {
-          double yr = s;
-          if (theta != 0.0) yr -= theta * a.x[r];
-          a.y[r] = yr;
-          epilogue_row<NA>(a, r, yr, acc);
+        const unsigned ball = __ballot_sync(0xffffffffu, is_long);
+        const int lane = tid & 31, warp = tid >> 5;
+        if (lane == 0) wcnt_sm[warp] = __popc(ball);
+        __syncthreads();
+        int off = nlist;
+        for (int w = 0; w < warp; ++w) off += wcnt_sm[w];
+        if (is_long) list_sm[off + __popc(ball & ((1u << lane) - 1u))] = rr;
+        for (int w = 0; w < kWarps; ++w) nlist += wcnt_sm[w];
+        __syncthreads();
+      }
+      // phase B: one warp per long row (lane-strided, then butterfly)
+      {
+        const int lane = tid & 31, warp = tid >> 5;
+        for (int i = warp; i < nlist; i += kWarps) {
+          const int rr = list_sm[i];
+          const int64_t r = blk.row0 + rr;
+          const int lo = (int)(a.row_ptr[r] - blk.nz0);
+          const int hi = (int)(a.row_ptr[r + 1] - blk.nz0);
+          double sacc = 0.0;
+          for (int e = lo + lane; e < hi; e += 32) sacc += sm[e];
+          sacc = warp_sum(sacc);
+          if (lane == 0) {
+            const double yr = finish_row<PACKED>(a, r, sacc, theta);
+            a.y[r] = yr;
+            epilogue_row<NA>(a, r, yr, acc);
+          }
         }
       }
       __syncthreads();  // sm reused by the next block
@@ -147,10 +225,8 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
       // ---- part of a long row: register partial, ticket, ordered finish
       double s = 0.0;
 #pragma unroll 8
-      for (int e = tid; e < cnt; e += kThreads) {
-        int64_t k = blk.nz0 + e;
-        s += ld_stream(a.val + k) * __ldg(a.x + ld_stream(a.col + k));
-      }
+      for (int e = tid; e < cnt; e += kThreads)
+        s += product<PACKED>(a, blk.nz0 + e, tab_sm, cmask);
       s = warp_sum(s);
       if ((tid & 31) == 0) sm[tid >> 5] = s;
       __syncthreads();
@@ -176,8 +252,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
         t = warp_sum(t);
         if (tid == 0) {
           const int64_t r = blk.row0;
-          double yr = t;
-          if (theta != 0.0) yr -= theta * a.x[r];
+          const double yr = finish_row<PACKED>(a, r, t, theta);
           a.y[r] = yr;
           a.long_ticket[lr] = 0u;
           if constexpr (NA > 0) {
@@ -196,8 +271,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
     }
   }
   if constexpr (NA > 0) {
-    grid_reduce<NA>(acc, a.ndots + a.nq, ws, a.out, red_sm, ws.long_dots,
-                    a.nlong);
+    grid_reduce<NA>(acc, a.ndots + a.nq, ws, a.out, red_sm, ws.long_dots, a.nlong);
   }
 }
 
@@ -222,7 +296,7 @@ static void build_schedule(int64_t n, const int64_t* rp,
         b.nz1 = std::min(rp[r] + (int64_t)(p + 1) * kChunk, rp[r + 1]);
         b.row0 = (int32_t)r;
         b.nrows = lr;
-        b.lanes = 0;
+        b.lshift = -1;
         b.part = (int32_t)(slot0 + p);
         blocks.push_back(b);
       }
@@ -241,10 +315,14 @@ static void build_schedule(int64_t n, const int64_t* rp,
     b.nz1 = rp[r];
     b.row0 = (int32_t)r0;
     b.nrows = (int32_t)(r - r0);
-    double avg = (double)nz / (double)(r - r0);
-    int L = 1;
-    while (L < 32 && 2.0 * L <= avg) L <<= 1;  // lanes <= mean row length
-    b.lanes = L;
+    // lanes per row: one pass over the block's rows with every thread busy
+    // when rows are few (long), one thread per row when they are many --
+    // never more lanes than the mean row length
+    const int64_t nr = r - r0;
+    const double avg = (double)nz / (double)nr;
+    int sh = 0;
+    while (sh < 5 && (nr << (sh + 1)) <= kThreads && (double)(2 << sh) <= 2.0 * avg) ++sh;
+    b.lshift = sh;
     b.part = 0;
     blocks.push_back(b);
   }
@@ -274,28 +352,105 @@ static int ensure_long_ws(lg_ws* ws, const lg_csr* a) {
   return LG_OK;
 }
 
-template <int NA>
-static int grid_for() {
-  static int occ = -1;
-  if (occ < 0) {
+template <int NA, bool PACKED>
+static int grid_for(size_t dyn) {
+  static thread_local size_t last_dyn = (size_t)-1;
+  static thread_local int occ = 1;
+  if (dyn != last_dyn) {
     int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, spmv_kernel<NA>,
-                                                      kThreads, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, spmv_kernel<NA, PACKED>,
+                                                      kThreads, dyn) != cudaSuccess ||
         o < 1)
       o = 1;
     occ = o;
+    last_dyn = dyn;
   }
   return occ * dev_info().sm_count;
 }
 
-template <int NA>
-static int launch(const SpmvArgs& args, lg_ws* ws, cudaStream_t s) {
-  int64_t g = std::min<int64_t>(args.nblocks, grid_for<NA>());
+template <int NA, bool PACKED>
+static int launch_t(const SpmvArgs& args, lg_ws* ws, cudaStream_t s) {
+  const size_t dyn = PACKED ? sizeof(double) * (size_t)args.nvals : 0;
+  int64_t g = std::min<int64_t>(args.nblocks, grid_for<NA, PACKED>(dyn));
   if (NA > 0) g = std::min<int64_t>(g, kMaxRedBlocks);
   if (g < 1) g = 1;
-  spmv_kernel<NA><<<(unsigned)g, kThreads, 0, s>>>(args, *ws);
+  spmv_kernel<NA, PACKED><<<(unsigned)g, kThreads, dyn, s>>>(args, *ws);
   LG_LAUNCH_CHECK("spmv_kernel");
   return LG_OK;
+}
+
+template <int NA>
+static int launch(const SpmvArgs& args, lg_ws* ws, cudaStream_t s, bool packed) {
+  return packed ? launch_t<NA, true>(args, ws, s) : launch_t<NA, false>(args, ws, s);
+}
+
+// Packed Laplacian format eligibility: every row stores its diagonal, the
+// distinct off-diagonal values fit the bits left above the column index and
+// the shared-memory table.
+static bool make_packed(int64_t n, const int64_t* rp, const int64_t* col, const double* val,
+                        std::vector<int64_t>& prp, std::vector<uint32_t>& pcol,
+                        std::vector<double>& diag, std::vector<double>& table, int& cbits) {
+  if (n < 1) return false;
+  cbits = 1;
+  while (((int64_t)1 << cbits) < n) ++cbits;
+  if (cbits > 31) return false;
+  const int vbits = 32 - cbits;
+  const int64_t maxvals = std::min<int64_t>((int64_t)1 << vbits, kMaxTable);
+  std::vector<uint64_t> uniq;
+  {
+    std::vector<uint64_t> bitsv;
+    bitsv.reserve(1024);
+    // collect distinct values incrementally (stop early when too many)
+    std::vector<uint64_t> tmp;
+    for (int64_t r = 0; r < n; ++r) {
+      bool has_diag = false;
+      for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+        if (col[k] == r) {
+          has_diag = true;
+          continue;
+        }
+        uint64_t bv;
+        std::memcpy(&bv, val + k, 8);
+        tmp.push_back(bv);
+        if (tmp.size() >= 4096) {
+          tmp.insert(tmp.end(), uniq.begin(), uniq.end());
+          std::sort(tmp.begin(), tmp.end());
+          tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+          uniq.swap(tmp);
+          tmp.clear();
+          if ((int64_t)uniq.size() > maxvals) return false;
+        }
+      }
+      if (!has_diag) return false;
+    }
+    tmp.insert(tmp.end(), uniq.begin(), uniq.end());
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    uniq.swap(tmp);
+    if ((int64_t)uniq.size() > maxvals) return false;
+  }
+  table.resize(uniq.size());
+  for (size_t i = 0; i < uniq.size(); ++i) std::memcpy(&table[i], &uniq[i], 8);
+  prp.assign((size_t)n + 1, 0);
+  diag.assign((size_t)n, 0.0);
+  const int64_t noff = rp[n] - n;
+  pcol.resize((size_t)std::max<int64_t>(noff, 0));
+  int64_t o = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+      if (col[k] == r) {
+        diag[(size_t)r] = val[k];
+        continue;
+      }
+      uint64_t bv;
+      std::memcpy(&bv, val + k, 8);
+      const uint32_t idx =
+          (uint32_t)(std::lower_bound(uniq.begin(), uniq.end(), bv) - uniq.begin());
+      pcol[(size_t)o++] = (uint32_t)col[k] | (idx << cbits);
+    }
+    prp[(size_t)r + 1] = o;
+  }
+  return true;
 }
 
 }  // namespace lg
@@ -324,16 +479,25 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
       return fail(LG_EINVAL, "lg_csr_create: column index out of range");
     c32[(size_t)k] = (int32_t)col[k];
   }
+  std::vector<int64_t> prp;
+  std::vector<uint32_t> pcol;
+  std::vector<double> pdiag, table;
+  int cbits = 0;
+  const bool packed = !(flags & 1) && make_packed(n, rp, col, val, prp, pcol, pdiag, table, cbits);
   std::vector<SpmvBlock> blocks;
   std::vector<int32_t> lnp;
   std::vector<int64_t> lfirst;
-  build_schedule(n, rp, blocks, lnp, lfirst);
+  build_schedule(n, packed ? prp.data() : rp, blocks, lnp, lfirst);
 
   lg_csr* a = new lg_csr();
   a->n = n;
   a->nnz = nnz;
   a->nblocks = (int64_t)blocks.size();
   a->nlong = (int64_t)lnp.size();
+  a->packed = packed ? 1 : 0;
+  a->cbits = cbits;
+  a->nvals = (int)table.size();
+  a->noff = packed ? (int64_t)pcol.size() : 0;
   for (int32_t v : lnp) a->nparts += v;
   auto cleanup = [&](const char* what) {
     lg_csr_destroy(a);
@@ -348,6 +512,21 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
   if (a->nblocks &&
       cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess)
     return cleanup("schedule alloc");
+  if (packed) {
+    if (cudaMalloc(&a->prp, sizeof(int64_t) * (size_t)(n + 1)) != cudaSuccess ||
+        (a->noff && cudaMalloc(&a->pcol, sizeof(uint32_t) * (size_t)a->noff) != cudaSuccess) ||
+        cudaMalloc(&a->pdiag, sizeof(double) * (size_t)n) != cudaSuccess ||
+        (a->nvals && cudaMalloc(&a->table, sizeof(double) * (size_t)a->nvals) != cudaSuccess))
+      return cleanup("packed alloc");
+    cudaMemcpy(a->prp, prp.data(), sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice);
+    if (a->noff)
+      cudaMemcpy(a->pcol, pcol.data(), sizeof(uint32_t) * (size_t)a->noff,
+                 cudaMemcpyHostToDevice);
+    cudaMemcpy(a->pdiag, pdiag.data(), sizeof(double) * (size_t)n, cudaMemcpyHostToDevice);
+    if (a->nvals)
+      cudaMemcpy(a->table, table.data(), sizeof(double) * (size_t)a->nvals,
+                 cudaMemcpyHostToDevice);
+  }
   if (a->nlong) {
     if (cudaMalloc(&a->long_nparts, sizeof(int32_t) * (size_t)a->nlong) != cudaSuccess ||
         cudaMalloc(&a->long_first, sizeof(int64_t) * (size_t)a->nlong) != cudaSuccess)
@@ -384,6 +563,10 @@ int lg_csr_destroy(lg_csr* a) {
   cudaFree(a->blocks);
   cudaFree(a->long_nparts);
   cudaFree(a->long_first);
+  cudaFree(a->prp);
+  cudaFree(a->pcol);
+  cudaFree(a->pdiag);
+  cudaFree(a->table);
   delete a;
   return LG_OK;
 }
@@ -395,10 +578,13 @@ int lg_csr_info(const lg_csr* a, int64_t* n, int64_t* nnz, int64_t* nblocks,
   if (nnz) *nnz = a->nnz;
   if (nblocks) *nblocks = a->nblocks;
   if (nlong) *nlong = a->nlong;
-  if (packed) *packed = 0;
-  // values f64 + int32 columns + int64 row pointers + x read + y written
+  if (packed) *packed = a->packed;
+  // bytes one SpMV streams: plain = f64 values + int32 columns + int64 row
+  // pointers + x read + y written; packed = 32-bit words per off-diagonal +
+  // int64 row pointers + diagonal + x + y
   if (stream_bytes)
-    *stream_bytes = 12 * a->nnz + 8 * (a->n + 1) + 16 * a->n;
+    *stream_bytes = a->packed ? 4 * a->noff + 8 * (a->n + 1) + 8 * a->n + 16 * a->n
+                              : 12 * a->nnz + 8 * (a->n + 1) + 16 * a->n;
   return LG_OK;
 }
 
@@ -440,9 +626,14 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
   }
   SpmvArgs args{};
   args.n = a->n;
-  args.row_ptr = a->row_ptr;
+  args.row_ptr = a->packed ? a->prp : a->row_ptr;
   args.col = a->col;
   args.val = a->val;
+  args.pcol = a->packed ? a->pcol : nullptr;
+  args.pdiag = a->pdiag;
+  args.table = a->table;
+  args.nvals = a->nvals;
+  args.cbits = a->cbits;
   args.blocks = a->blocks;
   args.nblocks = a->nblocks;
   args.long_nparts = a->long_nparts;
@@ -464,10 +655,11 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
   args.nlong = a->nlong;
   cudaStream_t s = (cudaStream_t)stream;
   int na = ndots + nq;
-  if (na == 0) return launch<0>(args, ws, s);
-  if (na <= 4) return launch<4>(args, ws, s);
-  if (na <= 16) return launch<16>(args, ws, s);
-  return launch<LG_MAXD + LG_MAXQ>(args, ws, s);
+  const bool pk = a->packed != 0;
+  if (na == 0) return launch<0>(args, ws, s, pk);
+  if (na <= 4) return launch<4>(args, ws, s, pk);
+  if (na <= 16) return launch<16>(args, ws, s, pk);
+  return launch<LG_MAXD + LG_MAXQ>(args, ws, s, pk);
 }
 
 int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,

@@ -272,3 +272,20 @@ def test_jacobi_variant(L):
     jf = L.JacobiFactor(a)
     x = np.random.default_rng(0).standard_normal(a.n)
     assert np.allclose(jf.apply(x), x / a.diagonal(), rtol=1e-15)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C4"])
+def test_plain_and_packed_formats_agree(L, cfg):
+    import torch
+    from paper_1311_1695_b200.sparse import DeviceCsr
+    from paper_1311_1695_b200 import _device as dev
+    a = L.build_laplacian(L.config_graph(cfg))
+    plain = DeviceCsr(a.n, a.row_ptr, a.col_idx, a.values, flags=1)
+    packed = DeviceCsr(a.n, a.row_ptr, a.col_idx, a.values)
+    assert not plain.packed and packed.packed
+    assert packed.stream_bytes < plain.stream_bytes
+    x = torch.randn(a.n, dtype=torch.float64, device="cuda")
+    y0, y1 = dev.empty(a.n), dev.empty(a.n)
+    plain.matvec(x, y0, theta=0.3)
+    packed.matvec(x, y1, theta=0.3)
+    assert float((y0 - y1).abs().max()) <= 1e-13 * float(y0.abs().max())
