@@ -136,6 +136,13 @@ int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels);
  * one stream.  z may alias r. */
 int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
                  void* stream);
+/* Debug instrumentation of the sweeps: enable != 0 allocates a timestamp
+ * buffer written after every level segment (CTA 0's view); host_out (cap
+ * entries) receives the last apply's timestamps.  Returns the number of
+ * segments (forward + backward). */
+int lg_ic0_trace(lg_ic0* f, int enable, unsigned long long* host_out, int cap);
+/* Debug: per-segment {tasks, narrow, barrier, 0} of one sweep. */
+int lg_ic0_schedule(const lg_ic0* f, int backward, int* host_out, int cap);
 /* Jacobi (diagonal) apply z = r / diag, a flagged non-reference variant. */
 int lg_diag_apply(int64_t n, const double* dinv, const double* r, double* z,
                   const int* skip, void* stream);

@@ -78,6 +78,7 @@ struct SweepDev {
 
 struct lg_ic0 {
   int64_t n = 0, nnz_l = 0;  // nnz_l counts the diagonal
+  unsigned long long* trace = nullptr;  // debug timestamps (fwd segs, bwd segs)
   lg::SweepDev fwd, bwd;
   double* diag = nullptr;
   double* tmp = nullptr;     // forward result
@@ -287,6 +288,7 @@ struct SweepArgs {
   const double* b;
   double* x;
   const int* skip;
+  unsigned long long* trace;  // optional: globaltimer after every segment (CTA 0)
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -437,13 +439,35 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
         finish(a, st, lane);
       }
     }
-    // stage the next level's first task before waiting for this one
-    staged_t = (s + 1 < a.nsegs) ? first_task(a.segs[s + 1]) : -1;
-    if (staged_t >= 0) stage(a, staged_t, lane, st);
-    if (sg.narrow && blockIdx.x == 0) __syncthreads();
+    // split-phase barrier: arrive, stage the next level's first task (its
+    // loads depend only on static data), then wait -- the staging latency
+    // hides behind the barrier instead of adding to it
+    const int64_t next_t = (s + 1 < a.nsegs) ? first_task(a.segs[s + 1]) : -1;
     if (sg.barrier) {
       ++nb;
-      grid_barrier(a.bar, base + (unsigned long long)nb * (unsigned long long)G);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(a.bar, 1ull);
+      }
+      staged_t = next_t;
+      if (staged_t >= 0) stage(a, staged_t, lane, st);
+      if (threadIdx.x == 0) {
+        const unsigned long long target = base + (unsigned long long)nb * (unsigned long long)G;
+        while (ld_relaxed_u64(a.bar) < target) {
+        }
+        __threadfence();
+      }
+      __syncthreads();
+    } else {
+      staged_t = next_t;
+      if (staged_t >= 0) stage(a, staged_t, lane, st);
+      if (sg.narrow && blockIdx.x == 0) __syncthreads();
+    }
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[s] = t;
     }
   }
 }
@@ -528,6 +552,7 @@ static SweepArgs sweep_args(const SweepDev& d, const double* b, double* x, const
   a.b = b;
   a.x = x;
   a.skip = skip;
+  a.trace = nullptr;
   return a;
 }
 
@@ -654,8 +679,47 @@ int lg_ic0_create(int64_t n, const int64_t* l_rp, const int64_t* l_col,
   return LG_OK;
 }
 
+// Debug: record a device timestamp after every level segment of both sweeps
+// (CTA 0's view) into a host array of fwd.nsegs + bwd.nsegs entries.
+int lg_ic0_trace(lg_ic0* f, int enable, unsigned long long* host_out, int cap) {
+  if (!f) return fail(LG_EINVAL, "lg_ic0_trace: NULL handle");
+  const int total = f->fwd.nsegs + f->bwd.nsegs;
+  if (enable && !f->trace) {
+    if (cudaMalloc(&f->trace, sizeof(unsigned long long) * (size_t)std::max(total, 1)) !=
+        cudaSuccess)
+      return fail(LG_ENOMEM, "lg_ic0_trace: alloc");
+  }
+  if (host_out && f->trace) {
+    LG_CUDA(cudaDeviceSynchronize());
+    LG_CUDA(cudaMemcpy(host_out, f->trace, sizeof(unsigned long long) * (size_t)std::min(cap, total),
+                       cudaMemcpyDeviceToHost));
+  }
+  if (!enable && f->trace) {
+    cudaFree(f->trace);
+    f->trace = nullptr;
+  }
+  return total;
+}
+
+// Debug: per-segment schedule statistics {tasks, rows, entries, narrow}
+int lg_ic0_schedule(const lg_ic0* f, int backward, int* host_out, int cap) {
+  if (!f) return fail(LG_EINVAL, "lg_ic0_schedule: NULL handle");
+  const SweepDev& d = backward ? f->bwd : f->fwd;
+  std::vector<SweepSeg> segs((size_t)d.nsegs);
+  if (d.nsegs)
+    cudaMemcpy(segs.data(), d.segs, sizeof(SweepSeg) * (size_t)d.nsegs, cudaMemcpyDeviceToHost);
+  for (int i = 0; i < d.nsegs && 4 * i + 3 < cap; ++i) {
+    host_out[4 * i] = segs[(size_t)i].t1 - segs[(size_t)i].t0;
+    host_out[4 * i + 1] = segs[(size_t)i].narrow;
+    host_out[4 * i + 2] = segs[(size_t)i].barrier;
+    host_out[4 * i + 3] = 0;
+  }
+  return d.nsegs;
+}
+
 int lg_ic0_destroy(lg_ic0* f) {
   if (!f) return LG_OK;
+  cudaFree(f->trace);
   free_sweep(f->fwd);
   free_sweep(f->bwd);
   cudaFree(f->diag);
@@ -679,6 +743,10 @@ int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
   cudaStream_t s = (cudaStream_t)stream;
   SweepArgs fa = sweep_args(f->fwd, r, f->tmp, skip);
   SweepArgs ba = sweep_args(f->bwd, f->tmp, z, skip);
+  if (f->trace) {
+    fa.trace = f->trace;
+    ba.trace = f->trace + f->fwd.nsegs;
+  }
   void* fargs[] = {&fa};
   LG_CUDA(cudaLaunchCooperativeKernel((void*)sweep_kernel, dim3(f->grid), dim3(kSweepThreads),
                                       fargs, 0, s));

@@ -122,14 +122,44 @@ __device__ __forceinline__ void epilogue_row(const SpmvArgs& a, int64_t r,
   }
 }
 
+constexpr int kPer = kChunk / kThreads;  // stream words per thread per block
+
+// Stream words of one block held in registers: issued one block ahead so the
+// DRAM latency of the column / value stream overlaps the current block's
+// gathers and row reductions (software pipelining across blocks).
 template <bool PACKED>
-__device__ __forceinline__ double product(const SpmvArgs& a, int64_t k,
+struct Staged {
+  uint32_t w[kPer];                 // packed: col | vidx << cbits; plain: col
+  double v[PACKED ? 1 : kPer];      // plain: values
+};
+
+template <bool PACKED>
+__device__ __forceinline__ void stage(const SpmvArgs& a, const SpmvBlock& blk, int tid,
+                                      Staged<PACKED>& st) {
+  const int cnt = (int)(blk.nz1 - blk.nz0);
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int e = tid + j * kThreads;
+    if (e < cnt) {
+      const int64_t k = blk.nz0 + e;
+      if constexpr (PACKED) {
+        st.w[j] = __ldcs(a.pcol + k);
+      } else {
+        st.w[j] = (uint32_t)__ldcs(a.col + k);
+        st.v[j] = __ldcs(a.val + k);
+      }
+    }
+  }
+}
+
+template <bool PACKED>
+__device__ __forceinline__ double product(const SpmvArgs& a, const Staged<PACKED>& st, int j,
                                           const double* tab, uint32_t cmask) {
   if constexpr (PACKED) {
-    const uint32_t w = __ldcs(a.pcol + k);
+    const uint32_t w = st.w[j];
     return tab[w >> a.cbits] * __ldg(a.x + (w & cmask));
   } else {
-    return ld_stream(a.val + k) * __ldg(a.x + ld_stream(a.col + k));
+    return st.v[j] * __ldg(a.x + st.w[j]);
   }
 }
 
@@ -162,15 +192,36 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
     for (int i = tid; i < a.nvals; i += kThreads) tab_sm[i] = a.table[i];
     __syncthreads();
   }
+  int64_t b = blockIdx.x;
+  if (b >= a.nblocks) {
+    if constexpr (NA > 0)
+      grid_reduce<NA>(acc, a.ndots + a.nq, ws, a.out, red_sm, ws.long_dots, a.nlong);
+    return;
+  }
+  SpmvBlock blk = a.blocks[b];
+  Staged<PACKED> cur;
+  stage<PACKED>(a, blk, tid, cur);
 
-  for (int64_t b = blockIdx.x; b < a.nblocks; b += gridDim.x) {
-    const SpmvBlock blk = a.blocks[b];
+  while (b < a.nblocks) {
+    const int64_t bn = b + gridDim.x;
+    SpmvBlock nblk;
+    if (bn < a.nblocks) nblk = a.blocks[bn];
     const int cnt = (int)(blk.nz1 - blk.nz0);
     if (blk.lshift >= 0) {
-      // ---- normal block: stream products into shared memory
-#pragma unroll 8
-      for (int e = tid; e < cnt; e += kThreads)
-        sm[e] = product<PACKED>(a, blk.nz0 + e, tab_sm, cmask);
+      // ---- normal block: products into shared memory
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int e = tid + j * kThreads;
+        if (e < cnt) sm[e] = product<PACKED>(a, cur, j, tab_sm, cmask);
+      }
+      // row bounds of this thread's first row (independent of the products)
+      int lo0 = 0, hi0 = 0;
+      if (tid < blk.nrows) {
+        lo0 = (int)(a.row_ptr[blk.row0 + tid] - blk.nz0);
+        hi0 = (int)(a.row_ptr[blk.row0 + tid + 1] - blk.nz0);
+      }
+      Staged<PACKED> nxt;
+      if (bn < a.nblocks) stage<PACKED>(a, nblk, tid, nxt);
       __syncthreads();
       // phase A: one thread per row for rows of at most kShortRow entries;
       // longer rows are compacted (in row order, via ballots) into a list
@@ -180,8 +231,11 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
         bool is_long = false;
         if (rr < blk.nrows) {
           const int64_t r = blk.row0 + rr;
-          const int lo = (int)(a.row_ptr[r] - blk.nz0);
-          const int hi = (int)(a.row_ptr[r + 1] - blk.nz0);
+          int lo = lo0, hi = hi0;
+          if (base) {
+            lo = (int)(a.row_ptr[r] - blk.nz0);
+            hi = (int)(a.row_ptr[r + 1] - blk.nz0);
+          }
           if (hi - lo <= kShortRow) {
             double sacc = 0.0;
             for (int e = lo; e < hi; ++e) sacc += sm[e];
@@ -221,12 +275,17 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
         }
       }
       __syncthreads();  // sm reused by the next block
+      cur = nxt;
     } else {
       // ---- part of a long row: register partial, ticket, ordered finish
       double s = 0.0;
-#pragma unroll 8
-      for (int e = tid; e < cnt; e += kThreads)
-        s += product<PACKED>(a, blk.nz0 + e, tab_sm, cmask);
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int e = tid + j * kThreads;
+        if (e < cnt) s += product<PACKED>(a, cur, j, tab_sm, cmask);
+      }
+      Staged<PACKED> nxt;
+      if (bn < a.nblocks) stage<PACKED>(a, nblk, tid, nxt);
       s = warp_sum(s);
       if ((tid & 31) == 0) sm[tid >> 5] = s;
       __syncthreads();
@@ -268,7 +327,10 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
         }
       }
       __syncthreads();
+      cur = nxt;
     }
+    blk = nblk;
+    b = bn;
   }
   if constexpr (NA > 0) {
     grid_reduce<NA>(acc, a.ndots + a.nq, ws, a.out, red_sm, ws.long_dots, a.nlong);
