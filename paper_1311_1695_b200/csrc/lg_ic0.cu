@@ -29,6 +29,8 @@
 // bitwise reproducible.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -39,6 +41,7 @@ namespace lg {
 constexpr int kSweepThreads = 512;          // 16 warps per CTA
 constexpr int kSweepWarps = kSweepThreads / 32;
 constexpr int kHubChunk = 512;              // nonzeros per hub-row chunk task
+constexpr int kSegSmem = 1024;              // level segments kept in shared memory
 
 struct SweepTask {
   int32_t p;  // pack: first permuted row          | chunk: permuted hub row
@@ -49,8 +52,10 @@ struct SweepTask {
 
 struct SweepSeg {
   int32_t t0, t1;   // task range
-  int32_t narrow;   // 1: run by CTA 0 alone
-  int32_t barrier;  // 1: a grid barrier follows this segment
+  int32_t narrow;   // 1: run by the first cluster alone
+  int32_t barrier;  // 1: grid barrier follows, 2: cluster barrier follows
+  int32_t run_t1;   // end task of the maximal run of same-mode segments
+  int32_t pad;
 };
 
 // Device data of one sweep direction.  Rows are stored PERMUTED into
@@ -63,6 +68,8 @@ struct SweepDev {
   int32_t* perm = nullptr;   // permuted position -> original row
   double* pdiag = nullptr;   // diagonal in permuted order
   SweepTask* tasks = nullptr;
+  int64_t* tbase = nullptr;
+  uint16_t* lanetab = nullptr;
   SweepSeg* segs = nullptr;
   int32_t* hub_first = nullptr;   // first partial slot of each hub row
   int32_t* hub_nchunk = nullptr;
@@ -182,6 +189,8 @@ struct SweepHost {
   std::vector<int32_t> pcol;
   std::vector<double> pval, pdiag;
   std::vector<SweepTask> tasks;
+  std::vector<int64_t> tbase;     // first entry of each task
+  std::vector<uint16_t> lanetab;  // per task x lane: rel_start << 5 | count
   std::vector<SweepSeg> segs;
   std::vector<int32_t> hub_first, hub_nchunk;
   int32_t nparts = 0;
@@ -190,11 +199,14 @@ struct SweepHost {
 };
 
 // Level schedule of one sweep: rows grouped by DAG level and length class,
-// permuted into that order, packed into warp tasks; levels classified wide /
-// narrow.
+// permuted into that order, packed into warp tasks; every task carries a
+// 32-lane table of (start, count) so staging a task is one level of
+// independent loads.  Levels with at most `narrow_tasks` tasks run on the
+// first cluster only.
 static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
                         const std::vector<int32_t>& col, const std::vector<double>& val,
-                        const std::vector<double>& diag, bool forward, SweepHost& h) {
+                        const std::vector<double>& diag, bool forward, int narrow_tasks,
+                        SweepHost& h) {
   std::vector<int32_t> level;
   h.levels = dag_levels(n, rp, col, forward, level);
   const int nl = h.levels;
@@ -232,37 +244,69 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
     std::copy(val.begin() + rp[(size_t)r], val.begin() + rp[(size_t)r + 1],
               h.pval.begin() + h.prp[(size_t)p]);
   }
+  auto push_task = [&](SweepTask tk, int64_t base, const uint16_t* lanes) {
+    h.tasks.push_back(tk);
+    h.tbase.push_back(base);
+    h.lanetab.insert(h.lanetab.end(), lanes, lanes + 32);
+  };
   for (int l = 0; l < nl; ++l) {
     const int32_t t0 = (int32_t)h.tasks.size();
     int64_t t = lcount[(size_t)l];
     const int64_t te = lcount[(size_t)l + 1];
     while (t < te) {
       const int L = cls(h.perm[(size_t)t]);
-      if (L == 64) {  // hub row: chunk tasks
+      uint16_t lanes[32];
+      if (L == 64) {  // hub row: chunk tasks of kHubChunk entries
         const int64_t len = h.prp[(size_t)t + 1] - h.prp[(size_t)t];
         const int32_t nch = (int32_t)((len + kHubChunk - 1) / kHubChunk);
         const int32_t hid = (int32_t)h.hub_first.size();
         h.hub_first.push_back(h.nparts);
         h.hub_nchunk.push_back(nch);
         h.nparts += nch;
-        for (int32_t c = 0; c < nch; ++c) h.tasks.push_back({(int32_t)t, 0, c, hid});
+        for (int32_t c = 0; c < nch; ++c) {
+          const int64_t lo = h.prp[(size_t)t] + (int64_t)c * kHubChunk;
+          const int64_t hi = std::min<int64_t>(h.prp[(size_t)t + 1], lo + kHubChunk);
+          for (int ln = 0; ln < 32; ++ln) {
+            const int64_t cntl = hi - (lo + ln) > 0 ? (hi - (lo + ln) + 31) / 32 : 0;
+            lanes[ln] = (uint16_t)((ln << 5) | (int)cntl);
+          }
+          push_task({(int32_t)t, 0, c, hid}, lo, lanes);
+        }
         ++t;
         continue;
       }
       const int cap = 32 / L;
       int cnt = 1;
       while (cnt < cap && t + cnt < te && cls(h.perm[(size_t)(t + cnt)]) == L) ++cnt;
-      h.tasks.push_back({(int32_t)t, (L << 8) | cnt, 0, 0});
+      const int64_t base = h.prp[(size_t)t];
+      for (int ln = 0; ln < 32; ++ln) {
+        const int g = ln / L, li = ln % L;
+        int cntl = 0, rel = 0;
+        if (g < cnt) {
+          const int64_t lo = h.prp[(size_t)(t + g)] + li, hi = h.prp[(size_t)(t + g) + 1];
+          cntl = lo < hi ? (int)((hi - lo + L - 1) / L) : 0;
+          rel = (int)(lo - base);
+        }
+        lanes[ln] = (uint16_t)((rel << 5) | cntl);
+      }
+      push_task({(int32_t)t, (L << 8) | cnt, 0, 0}, base, lanes);
       t += cnt;
     }
     const int32_t t1 = (int32_t)h.tasks.size();
-    h.segs.push_back({t0, t1, (t1 - t0) <= kSweepWarps ? 1 : 0, 0});
+    h.segs.push_back({t0, t1, (t1 - t0) <= narrow_tasks ? 1 : 0, 0, 0, 0});
   }
-  // barriers: after every wide level, and after the last level of a narrow
-  // run that is followed by a wide level.  None after the final segment.
+  for (size_t sg = h.segs.size(); sg-- > 0;) {
+    const bool same = sg + 1 < h.segs.size() && h.segs[sg + 1].narrow == h.segs[sg].narrow;
+    h.segs[sg].run_t1 = same ? h.segs[sg + 1].run_t1 : h.segs[sg].t1;
+  }
+  // barrier flags: 2 = cluster barrier (narrow -> narrow), 1 = grid barrier
+  // (after a wide level, or a narrow run followed by a wide level); none
+  // after the final segment
   h.nbar = 0;
   for (size_t sg = 0; sg + 1 < h.segs.size(); ++sg) {
-    if (!h.segs[sg].narrow || !h.segs[sg + 1].narrow) {
+    if (h.segs[sg].narrow && h.segs[sg + 1].narrow) {
+      h.segs[sg].barrier = 2;
+    } else {
       h.segs[sg].barrier = 1;
       ++h.nbar;
     }
@@ -277,9 +321,12 @@ struct SweepArgs {
   const int32_t* perm;
   const double* pdiag;
   const SweepTask* tasks;
+  const int64_t* tbase;
+  const uint16_t* lanetab;
   const SweepSeg* segs;
   int32_t nsegs;
   int32_t nbar;
+  int32_t csize;           // CTAs per cluster (1: no clusters)
   const int32_t* hub_first;
   const int32_t* hub_nchunk;
   unsigned* hub_ticket;
@@ -289,6 +336,7 @@ struct SweepArgs {
   double* x;
   const int* skip;
   unsigned long long* trace;  // optional: globaltimer after every segment (CTA 0)
+  int dbg;                    // timing experiments only (LG_SWEEP_DBG)
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -297,69 +345,73 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   return v;
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar,
-                                             unsigned long long target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1ull);
-    while (ld_relaxed_u64(bar) < target) {
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 constexpr int kLaneMax = 16;  // entries per lane per task (any class)
 
-// Everything a lane needs for one task that does not depend on the solve:
-// loaded ahead (before the barrier that precedes the task's level), so after
-// the barrier only the x gathers remain on the critical path.
+// Everything a lane needs for one task that does not depend on the solve;
+// loaded between barrier arrive and wait of the previous level.
 struct Staged {
   int32_t col[kLaneMax];
   double val[kLaneMax];
-  int32_t row;    // original row (pack) / permuted hub row (chunk)
+  int32_t row;    // original row of this lane's group (pack) / permuted hub row
   int32_t ne;     // entries held by this lane
   int32_t info;   // task.b (0: hub chunk)
   int32_t c, d;   // hub chunk index / id
   double bv, dg;
 };
 
-__device__ __forceinline__ void stage(const SweepArgs& a, int64_t t, int lane, Staged& st) {
-  const SweepTask tk = a.tasks[t];
+// Staging is split in two phases so that neither blocks the warp: phase 1
+// loads the task descriptor and this lane's (start, count) word; phase 2
+// (at least one barrier later, when those have arrived) loads the lane's
+// entries and its row's diagonal / right-hand side.
+struct Stage1 {
+  SweepTask tk;
+  int64_t base;
+  uint32_t lt;
+};
+
+__device__ __forceinline__ void stage1(const SweepArgs& a, int64_t t, int lane, Stage1& s1) {
+  s1.tk = a.tasks[t];
+  s1.base = a.tbase[t];
+  s1.lt = a.lanetab[t * 32 + lane];
+}
+
+__device__ __forceinline__ void stage2(const SweepArgs& a, const Stage1& s1, int lane,
+                                       Staged& st) {
+  const SweepTask tk = s1.tk;
   st.info = tk.b;
-  st.ne = 0;
-  int64_t lo, hi;
+  st.ne = s1.lt & 31;
+  const int64_t lo = s1.base + (s1.lt >> 5);
   int step;
   if (tk.b != 0) {
     const int L = tk.b >> 8, cnt = tk.b & 0xff;
-    const int g = lane / L, li = lane % L;
-    if (g >= cnt) return;
-    const int64_t p = tk.p + g;
-    lo = a.prp[p] + li;
-    hi = a.prp[p + 1];
+    const int g = lane / L;
     step = L;
-    st.row = a.perm[p];
-    st.bv = a.b[st.row];
-    st.dg = a.pdiag[p];
+    if (g < cnt) {
+      const int64_t p = tk.p + g;
+      st.row = a.perm[p];
+      st.dg = a.pdiag[p];
+      st.bv = a.b[st.row];
+    }
   } else {
     st.row = tk.p;
     st.c = tk.c;
     st.d = tk.d;
-    lo = a.prp[tk.p] + (int64_t)tk.c * kHubChunk;
-    hi = min(a.prp[tk.p + 1], lo + kHubChunk);
-    lo += lane;
     step = 32;
   }
 #pragma unroll
   for (int e = 0; e < kLaneMax; ++e) {
-    const int64_t k = lo + (int64_t)e * step;
-    if (k < hi) {
+    if (e < st.ne) {
+      const int64_t k = lo + (int64_t)e * step;
       st.col[e] = a.pcol[k];
       st.val[e] = a.pval[k];
-      st.ne = e + 1;
     }
   }
+}
+
+__device__ __forceinline__ void stage(const SweepArgs& a, int64_t t, int lane, Staged& st) {
+  Stage1 s1;
+  stage1(a, t, lane, s1);
+  stage2(a, s1, lane, st);
 }
 
 __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int lane) {
@@ -373,7 +425,8 @@ __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int
     if ((lane / L) < cnt && (lane % L) == 0) a.x[st.row] = (st.bv - s) / st.dg;
     return;
   }
-  // chunk of a hub row
+  // chunk of a hub row: publish the partial; the last chunk sums all of
+  // them lane-strided + butterfly (fixed order whoever arrives last)
   s = warp_sum(s);
   const int32_t first = a.hub_first[st.d], nch = a.hub_nchunk[st.d];
   unsigned arrived = 0;
@@ -384,8 +437,6 @@ __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int
   }
   arrived = __shfl_sync(0xffffffffu, arrived, 0);
   if (arrived == (unsigned)nch - 1u) {
-    // last chunk: the whole warp sums the partials (lane-strided, then a
-    // fixed butterfly), so the order does not depend on who finished last
     __threadfence();
     double t = 0.0;
     for (int32_t c = lane; c < nch; c += 32) t += __ldcg(a.hub_part + first + c);
@@ -398,60 +449,121 @@ __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int
   }
 }
 
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
   if (a.skip && *a.skip) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t G = gridDim.x;
   const int64_t gw = (int64_t)blockIdx.x * kSweepWarps + warp;
   const int64_t W = G * kSweepWarps;
+  const int csize = a.csize;
+  const bool first_cluster = blockIdx.x < (unsigned)csize;
+  const int64_t cw = (int64_t)blockIdx.x * kSweepWarps + warp;   // valid in cluster 0
+  const int64_t CW = (int64_t)csize * kSweepWarps;
   // every launch adds exactly nbar * G arrivals; barrier 0 cannot complete
   // before this CTA arrives, so rounding down recovers this launch's base
   __shared__ unsigned long long base_sm;
+  __shared__ SweepSeg seg_sm[kSegSmem];
   if (threadIdx.x == 0) {
     const unsigned long long per = (unsigned long long)a.nbar * (unsigned long long)G;
     const unsigned long long v = ld_relaxed_u64(a.bar);
     base_sm = per ? (v / per) * per : 0ull;
   }
+  const bool segs_in_smem = a.nsegs <= kSegSmem;
+  if (segs_in_smem)
+    for (int i = threadIdx.x; i < a.nsegs; i += blockDim.x) seg_sm[i] = a.segs[i];
   __syncthreads();
+  const SweepSeg* segs = segs_in_smem ? seg_sm : a.segs;
   const unsigned long long base = base_sm;
   int nb = 0;
   Staged st;
-  // first task of segment s for this warp (or -1)
-  auto first_task = [&](const SweepSeg& sg) -> int64_t {
-    int64_t t;
-    if (sg.narrow) {
-      if (blockIdx.x != 0) return -1;
-      t = sg.t0 + warp;
-    } else {
-      t = sg.t0 + gw;
-    }
-    return t < sg.t1 ? t : -1;
+  // Task t of a segment belongs to the warp with index t mod stride (grid
+  // warps for wide segments, first-cluster warps for narrow ones).  Tasks
+  // are numbered consecutively across levels, so consecutive small levels
+  // land on different warps and a warp can stage its next task many levels
+  // before that level opens: after a barrier only the x gathers remain.
+  // my_t: my next task in the current run of same-mode segments (tasks
+  // t == id mod stride); only a mode switch needs a modulo (32-bit).
+  const int icw = (int)cw, iCW = (int)CW, igw = (int)gw, iW = (int)W;
+  auto mine_from = [&](int t, bool narrow) -> int {
+    const int id = narrow ? icw : igw, st_ = narrow ? iCW : iW;
+    int r = (id - t) % st_;
+    if (r < 0) r += st_;
+    return t + r;
   };
-  int64_t staged_t = a.nsegs > 0 ? first_task(a.segs[0]) : -1;
-  if (staged_t >= 0) stage(a, staged_t, lane, st);
+  // staging state of my next task: 0 none, 1 phase 1 issued, 2 staged
+  int sstate = 0;
+  int sttask = -1;
+  Stage1 s1;
+  int my_t = -1;
+  if (a.nsegs > 0) {
+    const SweepSeg s0 = segs[0];
+    if (!s0.narrow || first_cluster) {
+      my_t = mine_from(s0.t0, s0.narrow);
+      if (my_t < s0.run_t1) {
+        stage(a, my_t, lane, st);
+        sttask = my_t;
+        sstate = 2;
+      }
+    } else {
+      my_t = 0x7fffffff;
+    }
+  }
   for (int s = 0; s < a.nsegs; ++s) {
-    const SweepSeg sg = a.segs[s];
-    const int64_t stride = sg.narrow ? kSweepWarps : W;
-    if (staged_t >= 0) {
-      finish(a, st, lane);
-      for (int64_t t = staged_t + stride; t < sg.t1; t += stride) {
-        stage(a, t, lane, st);
-        finish(a, st, lane);
+    const SweepSeg sg = segs[s];
+    const bool part = !sg.narrow || first_cluster;
+    if (part) {
+      const int stride = sg.narrow ? iCW : iW;
+      for (; my_t < sg.t1; my_t += stride) {
+        if (sttask != my_t || sstate != 2) {
+          if (sttask == my_t && sstate == 1) {
+            if (!(a.dbg & 2)) stage2(a, s1, lane, st);
+          } else if (!(a.dbg & 2)) {
+            stage(a, my_t, lane, st);
+          }
+          if (a.trace && lane == 0) atomicAdd(a.trace + a.nsegs, 1ull);
+        }
+        if (!(a.dbg & 1)) finish(a, st, lane);
+        sstate = 0;
+        sttask = -1;
       }
     }
-    // split-phase barrier: arrive, stage the next level's first task (its
-    // loads depend only on static data), then wait -- the staging latency
-    // hides behind the barrier instead of adding to it
-    const int64_t next_t = (s + 1 < a.nsegs) ? first_task(a.segs[s + 1]) : -1;
-    if (sg.barrier) {
+    // entering a new run (mode change): my first task there
+    if (s + 1 < a.nsegs && sg.run_t1 == sg.t1) {
+      const SweepSeg sn = segs[s + 1];
+      sstate = 0;
+      sttask = -1;
+      my_t = (!sn.narrow || first_cluster) ? mine_from(sn.t0, sn.narrow) : 0x7fffffff;
+    }
+    const int run_end = (s + 1 < a.nsegs) ? segs[s + 1].run_t1 : 0;
+    // advance the staging pipeline of my next task by one phase; neither
+    // phase stalls the warp (phase 2 uses data loaded a barrier earlier)
+    auto advance = [&]() {
+      if (my_t >= run_end || (a.dbg & 2)) return;
+      if (sstate == 0) {
+        stage1(a, my_t, lane, s1);
+        sttask = my_t;
+        sstate = 1;
+      } else if (sstate == 1 && sttask == my_t) {
+        stage2(a, s1, lane, st);
+        sstate = 2;
+      }
+    };
+    if (sg.barrier == 1) {
+      // split-phase grid barrier: arrive, advance staging, wait
       ++nb;
       __syncthreads();
       if (threadIdx.x == 0) {
         __threadfence();
         atomicAdd(a.bar, 1ull);
       }
-      staged_t = next_t;
-      if (staged_t >= 0) stage(a, staged_t, lane, st);
+      advance();
       if (threadIdx.x == 0) {
         const unsigned long long target = base + (unsigned long long)nb * (unsigned long long)G;
         while (ld_relaxed_u64(a.bar) < target) {
@@ -459,10 +571,15 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
         __threadfence();
       }
       __syncthreads();
+    } else if (sg.barrier == 2) {
+      if (first_cluster) {
+        if (csize > 1) cluster_arrive();
+        advance();
+        if (csize > 1) cluster_wait();
+        else __syncthreads();
+      }
     } else {
-      staged_t = next_t;
-      if (staged_t >= 0) stage(a, staged_t, lane, st);
-      if (sg.narrow && blockIdx.x == 0) __syncthreads();
+      advance();
     }
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
       unsigned long long t;
@@ -472,19 +589,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
   }
 }
 
-static int sweep_blocks_per_sm() {
-  static int occ = -1;
-  if (occ < 0) {
-    int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, sweep_kernel, kSweepThreads, 0) !=
-            cudaSuccess ||
-        o < 1)
-      o = 1;
-    occ = std::min(o, 2);
-  }
-  return occ;
-}
-
 template <typename T>
 static bool upload(T** dst, const std::vector<T>& v) {
   if (v.empty()) return true;
@@ -492,16 +596,71 @@ static bool upload(T** dst, const std::vector<T>& v) {
   return cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice) == cudaSuccess;
 }
 
+// Launch configuration: clusters of kCluster CTAs (one CTA per SM) when the
+// device allows a cooperative clustered launch, else plain cooperative.
+struct SweepLaunch {
+  int grid = 0;
+  int csize = 1;
+  bool probed = false;
+};
+
+static SweepLaunch& sweep_launch() {
+  static SweepLaunch L;
+  if (L.probed) return L;
+  L.probed = true;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_kernel, kSweepThreads, 0) !=
+          cudaSuccess ||
+      occ < 1)
+    occ = 1;
+  occ = std::min(occ, 1);
+  L.grid = occ * dev_info().sm_count;
+  L.csize = 1;
+  const char* env = getenv("LG_SWEEP_CLUSTER");
+  int want = env ? atoi(env) : 16;
+  for (int cs : {want, 8}) {
+    if (cs <= 1) break;
+    if (cs > 8 && cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                       1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kSweepThreads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, sweep_kernel, &cfg) == cudaSuccess &&
+        nclusters >= 1) {
+      L.csize = cs;
+      L.grid = nclusters * cs;
+      break;
+    }
+    cudaGetLastError();
+  }
+  if (getenv("LG_DEBUG"))
+    fprintf(stderr, "[lapb200] sweep launch: grid %d, cluster %d\n", L.grid, L.csize);
+  return L;
+}
+
 static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
                        const std::vector<int32_t>& col, const std::vector<double>& val,
                        const std::vector<double>& diag, bool forward, SweepDev& d) {
   SweepHost h;
-  build_sweep(n, rp, col, val, diag, forward, h);
+  const SweepLaunch& L = sweep_launch();
+  build_sweep(n, rp, col, val, diag, forward, L.csize * kSweepWarps, h);
   d.nsegs = (int32_t)h.segs.size();
   d.nbar = h.nbar;
   d.levels = h.levels;
   bool ok = upload(&d.prp, h.prp) && upload(&d.pcol, h.pcol) && upload(&d.pval, h.pval) &&
             upload(&d.perm, h.perm) && upload(&d.pdiag, h.pdiag) && upload(&d.tasks, h.tasks) &&
+            upload(&d.tbase, h.tbase) && upload(&d.lanetab, h.lanetab) &&
             upload(&d.segs, h.segs) && upload(&d.hub_first, h.hub_first) &&
             upload(&d.hub_nchunk, h.hub_nchunk);
   if (!ok) return false;
@@ -524,6 +683,8 @@ static void free_sweep(SweepDev& d) {
   cudaFree(d.perm);
   cudaFree(d.pdiag);
   cudaFree(d.tasks);
+  cudaFree(d.tbase);
+  cudaFree(d.lanetab);
   cudaFree(d.segs);
   cudaFree(d.hub_first);
   cudaFree(d.hub_nchunk);
@@ -541,9 +702,12 @@ static SweepArgs sweep_args(const SweepDev& d, const double* b, double* x, const
   a.perm = d.perm;
   a.pdiag = d.pdiag;
   a.tasks = d.tasks;
+  a.tbase = d.tbase;
+  a.lanetab = d.lanetab;
   a.segs = d.segs;
   a.nsegs = d.nsegs;
   a.nbar = d.nbar;
+  a.csize = sweep_launch().csize;
   a.hub_first = d.hub_first;
   a.hub_nchunk = d.hub_nchunk;
   a.hub_ticket = d.hub_ticket;
@@ -553,7 +717,33 @@ static SweepArgs sweep_args(const SweepDev& d, const double* b, double* x, const
   a.x = x;
   a.skip = skip;
   a.trace = nullptr;
+  const char* dbg = getenv("LG_SWEEP_DBG");
+  a.dbg = dbg ? atoi(dbg) : 0;
   return a;
+}
+
+static int launch_sweep(SweepArgs& args, cudaStream_t s) {
+  const SweepLaunch& L = sweep_launch();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(L.grid);
+  cfg.blockDim = dim3(kSweepThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeCooperative;
+  at[na].val.cooperative = 1;
+  ++na;
+  if (L.csize > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = L.csize;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_kernel, args));
+  return LG_OK;
 }
 
 }  // namespace lg
@@ -674,7 +864,7 @@ int lg_ic0_create(int64_t n, const int64_t* l_rp, const int64_t* l_col,
     lg_ic0_destroy(f);
     return fail(LG_ECUDA, std::string("lg_ic0_create: ") + cudaGetErrorString(err));
   }
-  f->grid = sweep_blocks_per_sm() * dev_info().sm_count;
+  f->grid = sweep_launch().grid;
   *out = f;
   return LG_OK;
 }
@@ -685,13 +875,14 @@ int lg_ic0_trace(lg_ic0* f, int enable, unsigned long long* host_out, int cap) {
   if (!f) return fail(LG_EINVAL, "lg_ic0_trace: NULL handle");
   const int total = f->fwd.nsegs + f->bwd.nsegs;
   if (enable && !f->trace) {
-    if (cudaMalloc(&f->trace, sizeof(unsigned long long) * (size_t)std::max(total, 1)) !=
-        cudaSuccess)
+    if (cudaMalloc(&f->trace, sizeof(unsigned long long) * (size_t)(total + 2)) != cudaSuccess)
       return fail(LG_ENOMEM, "lg_ic0_trace: alloc");
+    cudaMemset(f->trace, 0, sizeof(unsigned long long) * (size_t)(total + 2));
   }
   if (host_out && f->trace) {
     LG_CUDA(cudaDeviceSynchronize());
-    LG_CUDA(cudaMemcpy(host_out, f->trace, sizeof(unsigned long long) * (size_t)std::min(cap, total),
+    LG_CUDA(cudaMemcpy(host_out, f->trace,
+                       sizeof(unsigned long long) * (size_t)std::min(cap, total + 2),
                        cudaMemcpyDeviceToHost));
   }
   if (!enable && f->trace) {
@@ -744,16 +935,13 @@ int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
   SweepArgs fa = sweep_args(f->fwd, r, f->tmp, skip);
   SweepArgs ba = sweep_args(f->bwd, f->tmp, z, skip);
   if (f->trace) {
+    // layout: fwd segs, fwd inline-stage counter, bwd segs, bwd counter
     fa.trace = f->trace;
-    ba.trace = f->trace + f->fwd.nsegs;
+    ba.trace = f->trace + f->fwd.nsegs + 1;
   }
-  void* fargs[] = {&fa};
-  LG_CUDA(cudaLaunchCooperativeKernel((void*)sweep_kernel, dim3(f->grid), dim3(kSweepThreads),
-                                      fargs, 0, s));
-  void* bargs[] = {&ba};
-  LG_CUDA(cudaLaunchCooperativeKernel((void*)sweep_kernel, dim3(f->grid), dim3(kSweepThreads),
-                                      bargs, 0, s));
-  return LG_OK;
+  int rc = launch_sweep(fa, s);
+  if (rc) return rc;
+  return launch_sweep(ba, s);
 }
 
 }  // extern "C"

@@ -11,17 +11,18 @@ for name in sys.argv[1:] or ["C3"]:
     x = dev.to_device(np.random.default_rng(0).standard_normal(a.n)); z = dev.empty(a.n)
     for _ in range(3): d.apply(x, z)
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * tot)()
-    lib.lg_ic0_trace(d.handle, 1, buf, tot)
-    ts = np.array(buf[:], dtype=np.float64)
+    buf = (ctypes.c_ulonglong * (tot + 2))()
+    lib.lg_ic0_trace(d.handle, 1, buf, tot + 2)
+    raw = np.array(buf[:], dtype=np.float64)
     sch = (ctypes.c_int * (4 * tot))()
     nf = lib.lg_ic0_schedule(d.handle, 0, sch, 4 * tot)
     sf = np.array(sch[:4 * nf]).reshape(nf, 4)
     nb = lib.lg_ic0_schedule(d.handle, 1, sch, 4 * tot)
     sb = np.array(sch[:4 * nb]).reshape(nb, 4)
-    for lab, t, sc in (("fwd", ts[:nf], sf), ("bwd", ts[nf:nf + nb], sb)):
+    for lab, t, sc, cnt in (("fwd", raw[:nf], sf, raw[nf]), ("bwd", raw[nf + 1:nf + 1 + nb], sb, raw[nf + 1 + nb])):
         dt = np.diff(t) / 1e3
-        print(name, lab, "segments", len(t), "total %.1f us" % ((t[-1] - t[0]) / 1e3))
+        print(name, lab, "segments", len(t), "total %.1f us" % ((t[-1] - t[0]) / 1e3),
+              "inline stages (4 applies)", int(cnt))
         for kind in (0, 1):
             m = sc[1:, 1] == kind
             if m.any():
