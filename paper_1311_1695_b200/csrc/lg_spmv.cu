@@ -35,9 +35,17 @@
 
 namespace lg {
 
-constexpr int kChunk = 2048;   // nonzeros per row block (16 KB of products)
+#ifndef LG_SPMV_THREADS
+#define LG_SPMV_THREADS 128
+#endif
+constexpr int kST = LG_SPMV_THREADS;       // CTA size of the SpMV
+constexpr int kSW = kST / 32;
+constexpr int kChunk = kST * 8;            // nonzeros per row block
 constexpr int kRowCap = 1024;  // rows per normal block
 constexpr int kShortRow = 32;  // rows up to this length: one thread each
+#ifndef LG_SPMV_MINB
+#define LG_SPMV_MINB 12
+#endif
 
 struct SpmvBlock {
   int64_t nz0, nz1;  // nonzero range
@@ -122,7 +130,7 @@ __device__ __forceinline__ void epilogue_row(const SpmvArgs& a, int64_t r,
   }
 }
 
-constexpr int kPer = kChunk / kThreads;  // stream words per thread per block
+constexpr int kPer = kChunk / kST;  // stream words per thread per block
 
 // Stream words of one block held in registers: issued one block ahead so the
 // DRAM latency of the column / value stream overlaps the current block's
@@ -139,7 +147,7 @@ __device__ __forceinline__ void stage(const SpmvArgs& a, const SpmvBlock& blk, i
   const int cnt = (int)(blk.nz1 - blk.nz0);
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    const int e = tid + j * kThreads;
+    const int e = tid + j * kST;
     if (e < cnt) {
       const int64_t k = blk.nz0 + e;
       if constexpr (PACKED) {
@@ -172,14 +180,14 @@ __device__ __forceinline__ double finish_row(const SpmvArgs& a, int64_t r, doubl
 }
 
 template <int NA, bool PACKED>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kST, (NA == 0 ? LG_SPMV_MINB : 1))
 spmv_kernel(SpmvArgs a, lg_ws ws) {
   if (a.skip && *a.skip) return;
   __shared__ double sm[kChunk];
   extern __shared__ double tab_sm[];   // packed value table (nvals)
-  __shared__ double red_sm[kWarps * (NA > 0 ? NA : 1)];
+  __shared__ double red_sm[kSW * (NA > 0 ? NA : 1)];
   __shared__ int fin_flag;
-  __shared__ int wcnt_sm[kWarps];
+  __shared__ int wcnt_sm[kSW];
   __shared__ int list_sm[kRowCap];
   double acc[NA > 0 ? NA : 1];
 #pragma unroll
@@ -189,7 +197,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
   const int tid = threadIdx.x;
   const uint32_t cmask = PACKED ? ((1u << a.cbits) - 1u) : 0u;
   if constexpr (PACKED) {
-    for (int i = tid; i < a.nvals; i += kThreads) tab_sm[i] = a.table[i];
+    for (int i = tid; i < a.nvals; i += kST) tab_sm[i] = a.table[i];
     __syncthreads();
   }
   int64_t b = blockIdx.x;
@@ -211,7 +219,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
       // ---- normal block: products into shared memory
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
-        const int e = tid + j * kThreads;
+        const int e = tid + j * kST;
         if (e < cnt) sm[e] = product<PACKED>(a, cur, j, tab_sm, cmask);
       }
       // row bounds of this thread's first row (independent of the products)
@@ -226,7 +234,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
       // phase A: one thread per row for rows of at most kShortRow entries;
       // longer rows are compacted (in row order, via ballots) into a list
       int nlist = 0;
-      for (int base = 0; base < blk.nrows; base += kThreads) {
+      for (int base = 0; base < blk.nrows; base += kST) {
         const int rr = base + tid;
         bool is_long = false;
         if (rr < blk.nrows) {
@@ -253,13 +261,13 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
         int off = nlist;
         for (int w = 0; w < warp; ++w) off += wcnt_sm[w];
         if (is_long) list_sm[off + __popc(ball & ((1u << lane) - 1u))] = rr;
-        for (int w = 0; w < kWarps; ++w) nlist += wcnt_sm[w];
+        for (int w = 0; w < kSW; ++w) nlist += wcnt_sm[w];
         __syncthreads();
       }
       // phase B: one warp per long row (lane-strided, then butterfly)
       {
         const int lane = tid & 31, warp = tid >> 5;
-        for (int i = warp; i < nlist; i += kWarps) {
+        for (int i = warp; i < nlist; i += kSW) {
           const int rr = list_sm[i];
           const int64_t r = blk.row0 + rr;
           const int lo = (int)(a.row_ptr[r] - blk.nz0);
@@ -281,7 +289,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
       double s = 0.0;
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
-        const int e = tid + j * kThreads;
+        const int e = tid + j * kST;
         if (e < cnt) s += product<PACKED>(a, cur, j, tab_sm, cmask);
       }
       Staged<PACKED> nxt;
@@ -291,7 +299,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
       __syncthreads();
       if (tid == 0) {
         double t = 0.0;
-        for (int w = 0; w < kWarps; ++w) t += sm[w];
+        for (int w = 0; w < kSW; ++w) t += sm[w];
         a.long_part[blk.part] = t;
         __threadfence();
         const int lr = blk.nrows;
@@ -383,7 +391,7 @@ static void build_schedule(int64_t n, const int64_t* rp,
     const int64_t nr = r - r0;
     const double avg = (double)nz / (double)nr;
     int sh = 0;
-    while (sh < 5 && (nr << (sh + 1)) <= kThreads && (double)(2 << sh) <= 2.0 * avg) ++sh;
+    while (sh < 5 && (nr << (sh + 1)) <= kST && (double)(2 << sh) <= 2.0 * avg) ++sh;
     b.lshift = sh;
     b.part = 0;
     blocks.push_back(b);
@@ -421,7 +429,7 @@ static int grid_for(size_t dyn) {
   if (dyn != last_dyn) {
     int o = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, spmv_kernel<NA, PACKED>,
-                                                      kThreads, dyn) != cudaSuccess ||
+                                                      kST, dyn) != cudaSuccess ||
         o < 1)
       o = 1;
     occ = o;
@@ -436,7 +444,7 @@ static int launch_t(const SpmvArgs& args, lg_ws* ws, cudaStream_t s) {
   int64_t g = std::min<int64_t>(args.nblocks, grid_for<NA, PACKED>(dyn));
   if (NA > 0) g = std::min<int64_t>(g, kMaxRedBlocks);
   if (g < 1) g = 1;
-  spmv_kernel<NA, PACKED><<<(unsigned)g, kThreads, dyn, s>>>(args, *ws);
+  spmv_kernel<NA, PACKED><<<(unsigned)g, kST, dyn, s>>>(args, *ws);
   LG_LAUNCH_CHECK("spmv_kernel");
   return LG_OK;
 }
