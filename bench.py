@@ -193,8 +193,10 @@ def cpu_baseline_sample(g, seconds=10.0):
                       f"{reps * dt:.1f} s on one host core"}
 
 
-def solve_block(a, f):
-    """Wall time to 5 eigenpairs (delta 1e-8) with DACG and JD on the device."""
+def solve_block(a, f, f_mc=None):
+    """Wall time to 5 eigenpairs (delta 1e-8) with DACG and JD on the device,
+    with the reference's IC(0) (parity mode) and, flagged separately, with
+    the multicolour-reordered IC(0) variant."""
     import torch
     import paper_1311_1695_b200 as L
     ref = {}
@@ -203,18 +205,23 @@ def solve_block(a, f):
     except Exception:
         pass
     out = {}
-    for name, fn in (("dacg", L.dacg_smallest), ("jd", L.jd_smallest)):
+    runs = [("dacg", L.dacg_smallest, f, "ic0 (reference)"), ("jd", L.jd_smallest, f, "ic0 (reference)")]
+    if f_mc is not None:
+        runs += [("dacg_multicolor", L.dacg_smallest, f_mc, "multicolour ic0 (flagged variant)"),
+                 ("jd_multicolor", L.jd_smallest, f_mc, "multicolour ic0 (flagged variant)")]
+    for name, fn, prec, label in runs:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        pairs, rep = fn(a, 5, delta=1e-8, f=f)
+        pairs, rep = fn(a, 5, delta=1e-8, f=prec)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        r = ref.get(name, {})
+        r = ref.get(name.split("_")[0], {})
         err = None
         if r.get("eigenvalues"):
             err = float(np.max(np.abs(pairs.values - r["eigenvalues"]) /
                                np.abs(r["eigenvalues"])))
         out[name] = {"wall_s": wall, "mvp": rep.mvp, "neig": 5, "delta": 1e-8,
+                     "preconditioner": label,
                      "eig_relerr_vs_reference": err,
                      "reference_wall_s_build_container": r.get("wall_seconds"),
                      "reference_mvp": r.get("mvp")}
@@ -356,7 +363,7 @@ def main():
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_solve:
         f = L.ic0_factorize(a)
-        line["solve"] = solve_block(a, f)
+        line["solve"] = solve_block(a, f, L.ic0_factorize_multicolor(a))
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(g)
     if rank == 0:

@@ -128,7 +128,15 @@ typedef struct lg_ic0 lg_ic0;
  * for the backward sweep. */
 int lg_ic0_create(int64_t n, const int64_t* l_row_ptr_h, const int64_t* l_col_h,
                   const double* l_val_h, lg_ic0** out);
+/* Same for the factor of P A P^T (a reordered matrix): perm_h[i] is the
+ * original index of factor row i.  lg_ic0_apply then reads r and writes z in
+ * the original numbering (the permutation is folded into the sweeps). */
+int lg_ic0_create_perm(int64_t n, const int64_t* l_rp, const int64_t* l_col,
+                       const double* l_val, const int64_t* perm_h, lg_ic0** out);
 int lg_ic0_destroy(lg_ic0* f);
+/* Greedy colouring in smallest-last order (host).  color[v] in [0, ncolors). */
+int lg_color_smallest_last(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
+                           int32_t* color, int32_t* ncolors);
 int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels);
 /* z = (L L^T)^{-1} r: sync-free forward sweep on L then backward sweep on
  * L^T, one cooperative persistent kernel each.  The forward result lives in

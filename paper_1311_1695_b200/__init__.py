@@ -22,7 +22,14 @@ from .generators import (
     star_graph,
 )
 from .graphs import EdgeList, build_laplacian, connected_components, largest_component
-from .ic0 import Ic0Error, Ic0Factor, ic0_factorize, identity_factor
+from .ic0 import (
+    Ic0Error,
+    Ic0Factor,
+    MulticolorIc0Factor,
+    ic0_factorize,
+    ic0_factorize_multicolor,
+    identity_factor,
+)
 from .irlm import irlm_smallest, ncv_for
 from .jd import jd_smallest
 from .kernels import GramSchmidtBreakdown, dense_sym_eig, mgs_orthonormalize, tridiag_eig
@@ -35,7 +42,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CsrMatrix", "DeflationBasis", "EdgeList", "EigenPairSet", "GramSchmidtBreakdown",
-    "Ic0Error", "Ic0Factor", "JacobiFactor", "MvpCounter", "PcgOutcome", "SolverError",
+    "Ic0Error", "Ic0Factor", "JacobiFactor", "MulticolorIc0Factor", "ic0_factorize_multicolor", "MvpCounter", "PcgOutcome", "SolverError",
     "SolverReport", "ba_graph", "build_laplacian", "chung_lu_graph", "complete_graph",
     "config_graph", "connected_components", "cycle_graph", "dacg_smallest", "dense_sym_eig",
     "grid_graph", "ic0_factorize", "identity_factor", "irlm_smallest", "jd_correction_solve",

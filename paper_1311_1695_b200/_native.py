@@ -89,7 +89,9 @@ _SIGS = {
     "lg_ic0_factorize": (c_int, [c_i64, c_p, c_p, c_p, c_dbl, c_p, c_int, c_p,
                                  c_p, c_p, c_p, c_p]),
     "lg_ic0_create": (c_int, [c_i64, c_p, c_p, c_p, c_p]),
+    "lg_ic0_create_perm": (c_int, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "lg_ic0_destroy": (c_int, [c_p]),
+    "lg_color_smallest_last": (c_int, [c_i64, c_p, c_p, c_p, c_p]),
     "lg_ic0_info": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_ic0_apply": (c_int, [c_p, c_p, c_p, c_p, c_p]),
     "lg_ic0_trace": (c_int, [c_p, c_int, c_p, c_int]),

@@ -89,6 +89,8 @@ struct lg_ic0 {
   lg::SweepDev fwd, bwd;
   double* diag = nullptr;
   double* tmp = nullptr;     // forward result
+  int32_t* omap = nullptr;   // permuted factor: factor row -> original row
+  double* zp = nullptr;      // permuted factor: backward result (factor numbering)
   int grid = 0;
 };
 
@@ -334,6 +336,9 @@ struct SweepArgs {
   unsigned long long* bar;
   const double* b;
   double* x;
+  const int32_t* bmap;   // b index of a row (permuted factor: original row) or NULL
+  double* out2;          // second output in original numbering (or NULL)
+  const int32_t* omap;   // original index of a row for out2
   const int* skip;
   unsigned long long* trace;  // optional: globaltimer after every segment (CTA 0)
   int dbg;                    // timing experiments only (LG_SWEEP_DBG)
@@ -390,7 +395,7 @@ __device__ __forceinline__ void stage2(const SweepArgs& a, const Stage1& s1, int
       const int64_t p = tk.p + g;
       st.row = a.perm[p];
       st.dg = a.pdiag[p];
-      st.bv = a.b[st.row];
+      st.bv = a.b[a.bmap ? a.bmap[st.row] : st.row];
     }
   } else {
     st.row = tk.p;
@@ -422,7 +427,11 @@ __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int
   if (st.info != 0) {
     const int L = st.info >> 8, cnt = st.info & 0xff;
     for (int o = L >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((lane / L) < cnt && (lane % L) == 0) a.x[st.row] = (st.bv - s) / st.dg;
+    if ((lane / L) < cnt && (lane % L) == 0) {
+      const double v = (st.bv - s) / st.dg;
+      a.x[st.row] = v;
+      if (a.out2) a.out2[a.omap[st.row]] = v;
+    }
     return;
   }
   // chunk of a hub row: publish the partial; the last chunk sums all of
@@ -444,7 +453,9 @@ __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int
     if (lane == 0) {
       a.hub_ticket[st.d] = 0u;
       const int32_t row = a.perm[st.row];
-      a.x[row] = (a.b[row] - t) / a.pdiag[st.row];
+      const double v = (a.b[a.bmap ? a.bmap[row] : row] - t) / a.pdiag[st.row];
+      a.x[row] = v;
+      if (a.out2) a.out2[a.omap[row]] = v;
     }
   }
 }
@@ -715,6 +726,9 @@ static SweepArgs sweep_args(const SweepDev& d, const double* b, double* x, const
   a.bar = d.bar;
   a.b = b;
   a.x = x;
+  a.bmap = nullptr;
+  a.out2 = nullptr;
+  a.omap = nullptr;
   a.skip = skip;
   a.trace = nullptr;
   const char* dbg = getenv("LG_SWEEP_DBG");
@@ -809,6 +823,11 @@ int lg_ic0_factorize(int64_t n, const int64_t* rp, const int64_t* col,
 
 int lg_ic0_create(int64_t n, const int64_t* l_rp, const int64_t* l_col,
                   const double* l_val, lg_ic0** out) {
+  return lg_ic0_create_perm(n, l_rp, l_col, l_val, nullptr, out);
+}
+
+int lg_ic0_create_perm(int64_t n, const int64_t* l_rp, const int64_t* l_col,
+                       const double* l_val, const int64_t* perm_h, lg_ic0** out) {
   if (!out || n < 0 || !l_rp || (n > 0 && (!l_col || !l_val)))
     return fail(LG_EINVAL, "lg_ic0_create: bad argument");
   if (n >= ((int64_t)1 << 31)) return fail(LG_EINVAL, "lg_ic0_create: n too large");
@@ -855,6 +874,19 @@ int lg_ic0_create(int64_t n, const int64_t* l_rp, const int64_t* l_col,
   bool ok = make_sweep(n, frp, fcol, fval, dg, true, f->fwd) &&
             make_sweep(n, brp, bcol, bval, dg, false, f->bwd) && upload(&f->diag, dg) &&
             (n == 0 || cudaMalloc(&f->tmp, 8 * (size_t)n) == cudaSuccess);
+  if (ok && perm_h) {
+    std::vector<int32_t> om((size_t)n);
+    std::vector<char> seen((size_t)n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (perm_h[i] < 0 || perm_h[i] >= n || seen[(size_t)perm_h[i]]) {
+        lg_ic0_destroy(f);
+        return fail(LG_EINVAL, "lg_ic0_create_perm: perm is not a permutation");
+      }
+      seen[(size_t)perm_h[i]] = 1;
+      om[(size_t)i] = (int32_t)perm_h[i];
+    }
+    ok = upload(&f->omap, om) && cudaMalloc(&f->zp, 8 * (size_t)n) == cudaSuccess;
+  }
   if (!ok) {
     lg_ic0_destroy(f);
     return fail(LG_ENOMEM, "lg_ic0_create: device allocation / upload failed");
@@ -908,6 +940,77 @@ int lg_ic0_schedule(const lg_ic0* f, int backward, int* host_out, int cap) {
   return d.nsegs;
 }
 
+// Greedy colouring in smallest-last order (Matula-Beck degeneracy order with
+// a bucket queue, then first-fit in reverse removal order).  Used by the
+// flagged multicolour IC(0) variant: ordering nodes by (colour, id) makes the
+// factor's sweeps take #colours levels.
+int lg_color_smallest_last(int64_t n, const int64_t* rp, const int64_t* col, int32_t* color,
+                           int32_t* ncolors) {
+  if (n < 0 || (n > 0 && (!rp || !color || !ncolors)))
+    return fail(LG_EINVAL, "lg_color_smallest_last: bad argument");
+  std::vector<int64_t> deg((size_t)n);
+  int64_t maxd = 0;
+  for (int64_t v = 0; v < n; ++v) {
+    int64_t d = 0;
+    for (int64_t k = rp[v]; k < rp[v + 1]; ++k) d += (col[k] != v);
+    deg[(size_t)v] = d;
+    maxd = std::max(maxd, d);
+  }
+  // bucket queue: doubly linked lists per degree
+  std::vector<int64_t> head((size_t)maxd + 1, -1), nxt((size_t)n, -1), prv((size_t)n, -1);
+  auto push = [&](int64_t v) {
+    const int64_t d = deg[(size_t)v];
+    nxt[(size_t)v] = head[(size_t)d];
+    prv[(size_t)v] = -1;
+    if (head[(size_t)d] >= 0) prv[(size_t)head[(size_t)d]] = v;
+    head[(size_t)d] = v;
+  };
+  auto unlink = [&](int64_t v) {
+    const int64_t d = deg[(size_t)v];
+    if (prv[(size_t)v] >= 0) nxt[(size_t)prv[(size_t)v]] = nxt[(size_t)v];
+    else head[(size_t)d] = nxt[(size_t)v];
+    if (nxt[(size_t)v] >= 0) prv[(size_t)nxt[(size_t)v]] = prv[(size_t)v];
+  };
+  for (int64_t v = n - 1; v >= 0; --v) push(v);
+  std::vector<char> removed((size_t)n, 0);
+  std::vector<int64_t> order;
+  order.reserve((size_t)n);
+  int64_t cur = 0;
+  for (int64_t it = 0; it < n; ++it) {
+    if (cur > 0) --cur;
+    while (head[(size_t)cur] < 0) ++cur;
+    const int64_t v = head[(size_t)cur];
+    unlink(v);
+    removed[(size_t)v] = 1;
+    order.push_back(v);
+    for (int64_t k = rp[v]; k < rp[v + 1]; ++k) {
+      const int64_t u = col[k];
+      if (u == v || removed[(size_t)u]) continue;
+      unlink(u);
+      --deg[(size_t)u];
+      push(u);
+    }
+  }
+  std::vector<int32_t> c((size_t)n, -1);
+  std::vector<int64_t> mark;
+  int32_t nc = 0;
+  for (int64_t it = n - 1; it >= 0; --it) {
+    const int64_t v = order[(size_t)it];
+    if ((int64_t)mark.size() < nc + 1) mark.resize((size_t)nc + 1, -1);
+    for (int64_t k = rp[v]; k < rp[v + 1]; ++k) {
+      const int64_t u = col[k];
+      if (u != v && c[(size_t)u] >= 0) mark[(size_t)c[(size_t)u]] = v;
+    }
+    int32_t cc = 0;
+    while (cc < nc && mark[(size_t)cc] == v) ++cc;
+    c[(size_t)v] = cc;
+    if (cc == nc) ++nc;
+  }
+  for (int64_t v = 0; v < n; ++v) color[v] = c[(size_t)v];
+  *ncolors = nc;
+  return LG_OK;
+}
+
 int lg_ic0_destroy(lg_ic0* f) {
   if (!f) return LG_OK;
   cudaFree(f->trace);
@@ -915,6 +1018,8 @@ int lg_ic0_destroy(lg_ic0* f) {
   free_sweep(f->bwd);
   cudaFree(f->diag);
   cudaFree(f->tmp);
+  cudaFree(f->omap);
+  cudaFree(f->zp);
   delete f;
   return LG_OK;
 }
@@ -933,7 +1038,13 @@ int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
   if (f->n == 0) return LG_OK;
   cudaStream_t s = (cudaStream_t)stream;
   SweepArgs fa = sweep_args(f->fwd, r, f->tmp, skip);
-  SweepArgs ba = sweep_args(f->bwd, f->tmp, z, skip);
+  SweepArgs ba = sweep_args(f->bwd, f->tmp, f->omap ? f->zp : z, skip);
+  if (f->omap) {
+    // permuted factor: read r at original rows, write z at original rows
+    fa.bmap = f->omap;
+    ba.out2 = z;
+    ba.omap = f->omap;
+  }
   if (f->trace) {
     // layout: fwd segs, fwd inline-stage counter, bwd segs, bwd counter
     fa.trace = f->trace;

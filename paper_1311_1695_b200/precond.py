@@ -96,10 +96,10 @@ class CallablePrec:
 
 def device_preconditioner(f, n):
     """Device preconditioner for the solver seam `f`."""
-    from .ic0 import DeviceIc0, Ic0Factor
+    from .ic0 import DeviceIc0, Ic0Factor, MulticolorIc0Factor
     if f is None:
         return IdentityPrec(n)
-    if isinstance(f, Ic0Factor):
+    if isinstance(f, (Ic0Factor, MulticolorIc0Factor)):
         return f.device()
     if isinstance(f, JacobiFactor):
         return f

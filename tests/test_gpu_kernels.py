@@ -289,3 +289,25 @@ def test_plain_and_packed_formats_agree(L, cfg):
     plain.matvec(x, y0, theta=0.3)
     packed.matvec(x, y1, theta=0.3)
     assert float((y0 - y1).abs().max()) <= 1e-13 * float(y0.abs().max())
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+def test_multicolor_ic0_variant(L, cfg):
+    """Flagged variant: IC(0) of the colour-reordered matrix.  Its factor is
+    the oracle's IC(0) of P A P^T bit for bit, the sweeps take #colours
+    levels, and the apply (permutation folded into the sweeps) matches
+    P^T (L L^T)^{-1} P r."""
+    from paper_1311_1695_b200.ic0 import permuted_matrix
+    a = L.build_laplacian(L.config_graph(cfg))
+    f = L.ic0_factorize_multicolor(a)
+    pa = permuted_matrix(a, f.perm)
+    oa = O.Csr(a.n, pa.row_ptr, pa.col_idx, pa.values)
+    lrp, lcol, lval, _, _ = O.ic0_factorize(oa, use_c=True)
+    assert np.array_equal(f.l.values.view(np.int64), lval.view(np.int64))
+    assert f.device().levels <= f.ncolors
+    x = np.random.default_rng(0).standard_normal(a.n)
+    zp = O.Ic0(a.n, lrp, lcol, lval).apply(x[f.perm])
+    want = np.empty(a.n)
+    want[f.perm] = zp
+    z = f.apply(x)
+    assert np.max(np.abs(z - want)) <= 1e-12 * np.max(np.abs(want))

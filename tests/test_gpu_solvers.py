@@ -186,3 +186,13 @@ def test_jd_and_irlm_seams(L):
     assert st.m == 1 and c.count == st.last_inner_its > 0
     B = st.basis_matrix()
     assert np.allclose(B.T @ B, np.eye(B.shape[1]), atol=1e-12)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_multicolor_variant_converges_to_same_pairs(L, cfg):
+    ref = golden_config(cfg)
+    a = L.build_laplacian(L.config_graph(cfg))
+    f = L.ic0_factorize_multicolor(a)
+    for sv in ("dacg", "jd"):
+        pairs, rep = solver(L, sv)(a, ref["neig"], delta=ref["delta"], f=f)
+        check_pairs(L, a, pairs, np.asarray(ref["solvers"][sv]["eigenvalues"]), ref["delta"])
