@@ -55,6 +55,14 @@ int lg_device_info(int* sm_count, int* l2_bytes, int* cc_major, int* cc_minor);
 int lg_readback(const void* dev, void* host_pinned, int64_t bytes, void* stream);
 int lg_upload(void* dev, const void* host, int64_t bytes, void* stream);
 
+/* ---- CUDA graphs --------------------------------------------------------- */
+/* A solver iteration is a fixed launch sequence over fixed buffers: capture
+ * it once on a (non-legacy) stream and replay it with one launch. */
+int lg_capture_begin(void* stream);
+int lg_capture_end(void* stream, void** exec_out);
+int lg_graph_launch(void* exec, void* stream);
+int lg_graph_destroy(void* exec);
+
 /* ---- reduction workspace ---------------------------------------------- */
 typedef struct lg_ws lg_ws;
 int lg_ws_create(lg_ws** out);

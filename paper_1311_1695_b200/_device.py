@@ -130,3 +130,33 @@ class Pinned:
     def push(self, stream=None):
         nat.call("lg_upload", self.dev.data_ptr(), self.host.data_ptr(),
                  self.nbytes, stream if stream is not None else stream_ptr())
+
+
+_solver_streams = {}
+
+
+def solver_stream():
+    """Context manager running device work on a dedicated (capturable)
+    stream of the current device, ordered after the caller's stream."""
+    t = torch()
+    d = t.cuda.current_device()
+    s = _solver_streams.get(d)
+    if s is None:
+        s = _solver_streams[d] = t.cuda.Stream(device=d)
+    s.wait_stream(t.cuda.current_stream())
+    return _StreamCtx(t, s)
+
+
+class _StreamCtx:
+    def __init__(self, t, s):
+        self.t, self.s = t, s
+        self.prev = None
+
+    def __enter__(self):
+        self.cm = self.t.cuda.stream(self.s)
+        self.cm.__enter__()
+        return self.s
+
+    def __exit__(self, *exc):
+        self.cm.__exit__(*exc)
+        self.t.cuda.current_stream().wait_stream(self.s)

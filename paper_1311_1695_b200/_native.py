@@ -75,6 +75,10 @@ _SIGS = {
     "lg_device_info": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_readback": (c_int, [c_p, c_p, c_i64, c_p]),
     "lg_upload": (c_int, [c_p, c_p, c_i64, c_p]),
+    "lg_capture_begin": (c_int, [c_p]),
+    "lg_capture_end": (c_int, [c_p, c_p]),
+    "lg_graph_launch": (c_int, [c_p, c_p]),
+    "lg_graph_destroy": (c_int, [c_p]),
     "lg_ws_create": (c_int, [c_p]),
     "lg_ws_destroy": (c_int, [c_p]),
     "lg_csr_create": (c_int, [c_i64, c_i64, c_p, c_p, c_p, c_int, c_p]),

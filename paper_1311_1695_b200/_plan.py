@@ -315,3 +315,77 @@ class PrecApply:
     def __call__(self, ws=None, stream=None):
         self.d.apply_raw(self.r, self.z, self.skip,
                          stream if stream is not None else dev.stream_ptr())
+
+
+def _graph_note(msg):
+    import os
+    import sys
+    if os.environ.get("LG_DEBUG"):
+        print(f"[lapb200] {msg}", file=sys.stderr)
+
+
+class Graph:
+    """A fixed launch sequence captured into a CUDA graph and replayed.
+
+    Capture requires a non-legacy stream: solvers run inside
+    `with dev.solver_stream():`.  Every launch object must be replay-safe
+    (fixed buffers, coefficients read from device slots).  If capture fails
+    (e.g. a launch type the driver cannot capture) the sequence is replayed
+    eagerly instead -- same kernels, more host overhead.
+    """
+
+    def __init__(self, fns):
+        self.fns = list(fns)
+        self.exec = None
+        self.stream = None
+        self.eager = False
+        self.calls = 0
+
+    def _capture(self, stream):
+        lib = nat.load()
+        h = ctypes.c_void_p()
+        rc = lib.lg_capture_begin(stream)
+        if rc != 0:
+            self.eager = True
+            _graph_note("capture begin failed: " + nat.last_error())
+            return
+        try:
+            for f in self.fns:
+                f(stream=stream)
+        finally:
+            rc = lib.lg_capture_end(stream, ctypes.byref(h))
+        if rc != 0:
+            self.eager = True
+            _graph_note("capture failed, replaying eagerly: " + nat.last_error())
+            return
+        self.exec = h
+        self.stream = stream
+
+    def __call__(self, stream=None):
+        stream = stream if stream is not None else dev.stream_ptr()
+        self.calls += 1
+        # the first replay runs eagerly (lazy scratch allocations happen
+        # outside capture); the second captures
+        if not stream or self.eager or self.calls == 1:
+            for f in self.fns:
+                f(stream=stream)
+            return
+        if self.exec is None or self.stream != stream:
+            self.release()
+            self._capture(stream)
+            if self.eager:
+                for f in self.fns:
+                    f(stream=stream)
+                return
+        nat.check(nat.load().lg_graph_launch(self.exec, stream), "lg_graph_launch")
+
+    def release(self):
+        if self.exec is not None and nat._lib is not None:
+            nat._lib.lg_graph_destroy(self.exec)
+        self.exec = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass

@@ -65,6 +65,36 @@ int lg_upload(void* dev, const void* host, int64_t bytes, void* stream) {
   return LG_OK;
 }
 
+// ---- CUDA graphs: capture a fixed launch sequence once, replay it --------
+int lg_capture_begin(void* stream) {
+  if (!stream) return lg::fail(LG_EINVAL, "lg_capture_begin: needs a non-legacy stream");
+  LG_CUDA(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  return LG_OK;
+}
+
+int lg_capture_end(void* stream, void** exec_out) {
+  if (!exec_out) return lg::fail(LG_EINVAL, "lg_capture_end: exec_out is NULL");
+  cudaGraph_t g = nullptr;
+  LG_CUDA(cudaStreamEndCapture((cudaStream_t)stream, &g));
+  cudaGraphExec_t e = nullptr;
+  cudaError_t err = cudaGraphInstantiate(&e, g, 0);
+  cudaGraphDestroy(g);
+  if (err != cudaSuccess)
+    return lg::fail(LG_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(err));
+  *exec_out = (void*)e;
+  return LG_OK;
+}
+
+int lg_graph_launch(void* exec, void* stream) {
+  LG_CUDA(cudaGraphLaunch((cudaGraphExec_t)exec, (cudaStream_t)stream));
+  return LG_OK;
+}
+
+int lg_graph_destroy(void* exec) {
+  if (exec) cudaGraphExecDestroy((cudaGraphExec_t)exec);
+  return LG_OK;
+}
+
 int lg_ws_create(lg_ws** out) {
   if (!out) return lg::fail(LG_EINVAL, "lg_ws_create: out is NULL");
   lg_ws* ws = new lg_ws();

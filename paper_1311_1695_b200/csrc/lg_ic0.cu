@@ -40,7 +40,7 @@ namespace lg {
 
 constexpr int kSweepThreads = 512;          // 16 warps per CTA
 constexpr int kSweepWarps = kSweepThreads / 32;
-constexpr int kHubChunk = 512;              // nonzeros per hub-row chunk task
+constexpr int kHubChunk = 256;              // nonzeros per hub-row chunk task
 constexpr int kSegSmem = 1024;              // level segments kept in shared memory
 
 struct SweepTask {
@@ -182,7 +182,7 @@ static int lanes_for(int64_t len) {
   if (len <= 4) return 2;
   if (len <= 16) return 4;
   if (len <= 64) return 8;
-  return 32;  // <= kHubChunk: at most 16 entries per lane in every class
+  return 32;  // <= kHubChunk: at most 8 entries per lane in every class
 }
 
 struct SweepHost {
@@ -350,7 +350,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   return v;
 }
 
-constexpr int kLaneMax = 16;  // entries per lane per task (any class)
+constexpr int kLaneMax = 8;   // entries per lane per task (any class)
 
 // Everything a lane needs for one task that does not depend on the solve;
 // loaded between barrier arrive and wait of the previous level.
@@ -531,7 +531,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
     const bool part = !sg.narrow || first_cluster;
     if (part) {
       const int stride = sg.narrow ? iCW : iW;
-      for (; my_t < sg.t1; my_t += stride) {
+      if (my_t < sg.t1) {
+        // make sure my first task of this segment is fully staged
         if (sttask != my_t || sstate != 2) {
           if (sttask == my_t && sstate == 1) {
             if (!(a.dbg & 2)) stage2(a, s1, lane, st);
@@ -540,7 +541,21 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
           }
           if (a.trace && lane == 0) atomicAdd(a.trace + a.nsegs, 1ull);
         }
-        if (!(a.dbg & 1)) finish(a, st, lane);
+        // three-stage software pipeline over my tasks of this level:
+        // descriptor loads two tasks ahead, entry loads one task ahead,
+        // finish the current one -- no dependent stall on the way
+        Stage1 s1n;
+        if (my_t + stride < sg.t1) stage1(a, my_t + stride, lane, s1n);
+        for (; my_t < sg.t1; my_t += stride) {
+          const int t1n = my_t + stride, t2n = my_t + 2 * stride;
+          Staged stn;
+          Stage1 s1nn;
+          if (t2n < sg.t1) stage1(a, t2n, lane, s1nn);
+          if (t1n < sg.t1) stage2(a, s1n, lane, stn);
+          if (!(a.dbg & 1)) finish(a, st, lane);
+          st = stn;
+          s1n = s1nn;
+        }
         sstate = 0;
         sttask = -1;
       }

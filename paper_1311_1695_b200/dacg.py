@@ -38,7 +38,7 @@ import time
 import numpy as np
 
 from . import _device as dev
-from ._plan import Fused, PrecApply, Prog, Slots, Spmv
+from ._plan import Fused, Graph, PrecApply, Prog, Slots, Spmv
 from .ic0 import ic0_factorize
 from .pcg import kernel_basis, project_device
 from .precond import device_preconditioner
@@ -360,10 +360,13 @@ class _DacgPlan:
         self.plans[key] = L
         return L
 
-    def stage_b(self, b):
-        """The launches after the parallel test (fallback re-entry)."""
-        L = self.plan(b)
-        return L[8:]
+    def graph(self, b):
+        """The iteration of parity b as a CUDA graph (one launch)."""
+        key = ("g", b, self.k)
+        g = self.plans.get(key)
+        if g is None:
+            g = self.plans[key] = Graph(self.plan(b))
+        return g
 
 
 def _device_plan(a, f, n, kcap):
@@ -377,6 +380,11 @@ def dacg_smallest(a, neig, delta=1e-6, f=None, null_basis=None,
     fresh product against ||A x - q x|| / q <= delta and joined to the
     deflation set; raises with partial results attached when a pair exceeds
     maxit_per_pair."""
+    with dev.solver_stream():
+        return _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0)
+
+
+def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
     t0 = time.perf_counter()
     if counter is None:
         counter = MvpCounter()
@@ -468,8 +476,7 @@ def dacg_smallest(a, neig, delta=1e-6, f=None, null_basis=None,
                 S.set(q=theta)
                 Fused(n, outs=[dict(out=G[b], terms=[(w, 2.0), (xc, -2.0, S.p("th"))])])()
             L = pl.plan(b)
-            for fn in L:
-                fn()
+            pl.graph(b)()
             s, fl = S.fetch()
             if fl[S.fidx["par"]]:
                 # collapsed direction: steepest descent, then random (dacg.py:199-212)

@@ -184,6 +184,14 @@ def jd_smallest(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
     ||r|| < delta * theta, after which the pair is verified with a fresh
     product and locked; the correction equation runs at relative tolerance
     delta_pcg with at most itmax_inner PCG iterations."""
+    with dev.solver_stream():
+        return _jd_smallest_impl(**locals())
+
+
+def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
+                m_min=5, m_max=10, f=None, null_basis=None, *, seed=0,
+                max_outer_per_pair=300, stagnation_window=60,
+                counter=None, v0=None):
     t0 = time.perf_counter()
     if counter is None:
         counter = MvpCounter()

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _device as dev
-from ._plan import Fused, PrecApply, Prog, Slots, Spmv
+from ._plan import Fused, Graph, PrecApply, Prog, Slots, Spmv
 from .sparse import device_csr
 
 _ORTHO_TOL = 1e-10
@@ -384,6 +384,7 @@ class DevicePcg:
         body.append(Fused(n, outs=[dict(out=P, terms=[(Z, 1.0), (P, 1.0, S.p("beta"))])],
                           skip=stop))
         self.body = body
+        self.body_graph = Graph(body)
 
     def solve(self, b, qb, tol, maxit, theta=0.0, negate=False):
         """Solve op(x) = (-b if negate else b) from x0 = 0; returns
@@ -410,8 +411,7 @@ class DevicePcg:
         s, flags = S.fetch()
         if not flags[S.fidx["stop"]]:
             while its < maxit:
-                for f in self.body:
-                    f()
+                self.body_graph()
                 s, flags = S.fetch()
                 its = int(s[S.idx["its"]])
                 relres = float(s[S.idx["relres"]])

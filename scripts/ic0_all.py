@@ -1,0 +1,17 @@
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import paper_1311_1695_b200 as L
+from paper_1311_1695_b200 import _device as dev
+for name in sys.argv[1:] or ["C1", "C2", "C3", "C4"]:
+    a = L.build_laplacian(L.config_graph(name))
+    for lab, f in (("ic0", L.ic0_factorize(a)), ("mc", L.ic0_factorize_multicolor(a))):
+        d = f.device()
+        x = dev.to_device(np.random.default_rng(0).standard_normal(a.n)); z = dev.empty(a.n)
+        for _ in range(3): d.apply(x, z)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10): d.apply(x, z)
+        e1.record(); torch.cuda.synchronize()
+        zr = f.apply(x.cpu().numpy())
+        print(name, lab, "levels", d.levels, "apply %.1f us" % (e0.elapsed_time(e1) * 100), flush=True)

@@ -3,9 +3,9 @@ import ctypes, sys, numpy as np, torch
 sys.path.insert(0, ".")
 import paper_1311_1695_b200 as L
 from paper_1311_1695_b200 import _device as dev, _native as nat
-for name in sys.argv[1:] or ["C3"]:
+for name in [x for x in sys.argv[1:] if not x.startswith("--")] or ["C3"]:
     a = L.build_laplacian(L.config_graph(name))
-    f = L.ic0_factorize(a); d = f.device()
+    f = L.ic0_factorize_multicolor(a) if "--mc" in sys.argv else L.ic0_factorize(a); d = f.device()
     lib = nat.load()
     tot = lib.lg_ic0_trace(d.handle, 1, None, 0)
     x = dev.to_device(np.random.default_rng(0).standard_normal(a.n)); z = dev.empty(a.n)
