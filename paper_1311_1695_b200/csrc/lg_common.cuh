@@ -46,7 +46,7 @@ const DevInfo& dev_info();
 
 constexpr int kThreads = 256;                  // CTA size of vector kernels
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxRedBlocks = 148 * 8;         // upper bound on reducing CTAs
+constexpr int kMaxRedBlocks = 4096;            // upper bound on reducing CTAs
 constexpr int kMaxRedVals = LG_MAXD + LG_MAXQ; // values reduced per launch
 
 }  // namespace lg
@@ -84,7 +84,11 @@ __device__ __forceinline__ double warp_sum(double v) {
 // the machine (4 CTAs of 256 threads per SM) but never more than the rows
 // need.  Depends on n only, so the reduction tree is fixed per size.
 inline int vec_grid(int64_t n) {
-  int64_t want = (n + kThreads * 4 - 1) / (kThreads * 4);
+  // at least two elements per thread for small n; at most 4 CTAs per SM
+  // (the grid-stride loop is unrolled with non-coherent loads, so a
+  // thread keeps several elements in flight and the final cross-CTA
+  // reduction stays short)
+  int64_t want = (n + kThreads * 2 - 1) / (kThreads * 2);
   int64_t cap = (int64_t)dev_info().sm_count * 4;
   if (want < 1) want = 1;
   if (want > cap) want = cap;
@@ -113,6 +117,16 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NA], int na,
     }
   }
   __syncthreads();
+  if (gridDim.x == 1 && nextra == 0) {
+    // single CTA: the block sum is the result (same tree order as below)
+    if ((int)threadIdx.x < na) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += smem[w * NA + threadIdx.x];
+      // a one-element partial list summed lane-strided + butterfly equals s
+      result[threadIdx.x] = s + 0.0;
+    }
+    return;
+  }
   if ((int)threadIdx.x < na) {
     double s = 0.0;
     for (int w = 0; w < nw; ++w) s += smem[w * NA + threadIdx.x];

@@ -41,7 +41,11 @@ __device__ __forceinline__ double pick(const double* p, int64_t i,
   if (u == 1) return o[0];
   if (u == 2) return o[1];
   if (u == 3) return o[2];
-  return p[i];
+  // Non-coherent load: an element is read and then written only by its own
+  // thread, and never re-read after the write, so in-place passes stay
+  // correct while the compiler may hoist loads of later grid-stride steps
+  // above earlier stores (several elements in flight per thread).
+  return __ldg(p + i);
 }
 
 __device__ __forceinline__ double output_value(const lg_output& o,
@@ -56,9 +60,9 @@ __device__ __forceinline__ double output_value(const lg_output& o,
   if (o.uk > 0 || o.uk2 > 0) {
     double s = 0.0;
     const double* q = o.uq + i;
-    for (int j = 0; j < o.uk; ++j) s += uc[j] * q[(int64_t)j * o.uld];
+    for (int j = 0; j < o.uk; ++j) s += uc[j] * __ldg(q + (int64_t)j * o.uld);
     const double* q2 = o.uq2 + i;
-    for (int j = 0; j < o.uk2; ++j) s += uc2[j] * q2[(int64_t)j * o.uld2];
+    for (int j = 0; j < o.uk2; ++j) s += uc2[j] * __ldg(q2 + (int64_t)j * o.uld2);
     v -= s;
   }
   if (pmode == 1) v *= post;
@@ -109,6 +113,7 @@ fused_kernel(FusedDev a, lg_ws ws) {
   const int k1 = a.nblocks > 1 ? a.b[1].k : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
 
+#pragma unroll 2
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
        i += stride) {
     double ov[LG_MAXO] = {0.0, 0.0, 0.0};
@@ -131,9 +136,9 @@ fused_kernel(FusedDev a, lg_ws ws) {
           double y = a.db[s] ? pick(a.db[s], i, ov) : x;
           acc[s] += x * y;
         } else if (s < nd + k0) {
-          acc[s] += bv0 * a.b[0].q[i + (int64_t)(s - nd) * a.b[0].ld];
+          acc[s] += bv0 * __ldg(a.b[0].q + i + (int64_t)(s - nd) * a.b[0].ld);
         } else if (s < nd + k0 + k1) {
-          acc[s] += bv1 * a.b[1].q[i + (int64_t)(s - nd - k0) * a.b[1].ld];
+          acc[s] += bv1 * __ldg(a.b[1].q + i + (int64_t)(s - nd - k0) * a.b[1].ld);
         }
       }
     }
