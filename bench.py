@@ -228,6 +228,46 @@ def solve_block(a, f, f_mc=None):
     return out
 
 
+def c5_block(peaks, steps=10):
+    """BASELINE configs[4] (R-MAT scale 26, edge factor 16, ~2.1e9 nonzeros):
+    device-side ingest (sampling, dedupe, largest component, packed
+    Laplacian) and the SpMV on it.  Not buildable by the reference (SURVEY
+    0.8); reported next to the headline, not as it."""
+    import torch
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    A = rmat_laplacian_device(26, 16, seed=0)
+    torch.cuda.synchronize()
+    build = time.perf_counter() - t0
+    d = A.device()
+    x = dev.to_device(np.random.default_rng(0).standard_normal(A.n))
+    y = dev.empty(A.n)
+    for _ in range(3):
+        d.matvec(x, y)
+    torch.cuda.synchronize()
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for i in range(steps):
+        e0[i].record()
+        d.matvec(x, y)
+        e1[i].record()
+    torch.cuda.synchronize()
+    ms = float(np.mean([p.elapsed_time(q) for p, q in zip(e0, e1)]))
+    out = {"workload": "C5: R-MAT scale 26 ef 16 (a,b,c)=(.57,.19,.19), LCC, unit weights, "
+                       "device-built (counter-based RNG)",
+           "n": A.n, "m": A.m, "nnz": A.nnz, "build_s": build, "spmv_ms": ms,
+           "matvecs_per_s": 1e3 / ms,
+           "stream_gbs": d.stream_bytes / (ms * 1e-3) / 1e9,
+           "effective_gbs": d.algo_bytes / (ms * 1e-3) / 1e9,
+           "frac_stream_of_hbm": d.stream_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+           "l2": "x (262 MB) exceeds L2; not flushed"}
+    del A, d, x, y
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -237,6 +277,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c5", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -364,6 +405,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_solve:
         f = L.ic0_factorize(a)
         line["solve"] = solve_block(a, f, L.ic0_factorize_multicolor(a))
+    if rank == 0 and world == 1 and not args.no_c5:
+        line["c5"] = c5_block(peaks)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(g)
     if rank == 0:

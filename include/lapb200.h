@@ -116,6 +116,23 @@ int lg_build_laplacian(int64_t n, int64_t m, const int64_t* i_h,
                        const int64_t* j_h, const double* w_h,
                        int64_t* row_ptr_h, int64_t* col_h, double* val_h);
 
+/* ---- device-side ingest for C5-scale graphs (no reference counterpart) --- */
+/* R-MAT sampling (scale, edge_factor, a, b, c, seed) with a counter-based
+ * RNG, canonicalised (i < j, sorted, unique, no self-loops) on the device.
+ * *d_i / *d_j are cudaMalloc'ed int32 arrays (free with lg_free). */
+int lg_rmat_device(int scale, int edge_factor, double a, double b, double c,
+                   uint64_t seed, int32_t** d_i, int32_t** d_j, int64_t* m_out);
+/* Largest connected component of a canonical device edge list (nodes
+ * renumbered in increasing order, edges compacted in place of the input). */
+int lg_lcc_device(int64_t n, int64_t m, int32_t** d_i, int32_t** d_j,
+                  int64_t* n_out, int64_t* m_out);
+/* Unit-weight Laplacian of a canonical device edge list, built directly in
+ * the packed SpMV format on the device (no host copy of the matrix). */
+int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
+                            const int32_t* d_j, lg_csr** out);
+int lg_csr_diagonal(const lg_csr* a, double* d_out);
+int lg_free(void* p);
+
 /* ---- IC(0) factorization (ic0.py:48-116), host, bit-exact -------------- */
 /* Factor A + alpha diag(A) on the lower pattern of A, trying shift0 and then
  * every schedule entry > shift0, then 0.1 * max diag (ic0.py:98-111).

@@ -31,6 +31,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "lg_common.cuh"
 
 namespace lg {
@@ -660,6 +662,7 @@ int lg_csr_info(const lg_csr* a, int64_t* n, int64_t* nnz, int64_t* nblocks,
 
 int lg_csr_download(const lg_csr* a, int64_t* rp, int64_t* col, double* val) {
   if (!a) return fail(LG_EINVAL, "lg_csr_download: NULL handle");
+  if (!a->row_ptr) return fail(LG_EINVAL, "lg_csr_download: device-only matrix");
   if (rp)
     LG_CUDA(cudaMemcpy(rp, a->row_ptr, sizeof(int64_t) * (size_t)(a->n + 1),
                        cudaMemcpyDeviceToHost));
@@ -754,6 +757,181 @@ int lg_spmm(const lg_csr* a, const double* x, double* y, int k, void* stream) {
                      nullptr, stream);
     if (rc) return rc;
   }
+  return LG_OK;
+}
+
+// ---- device-built unit-weight Laplacian (C5 scale) -------------------------
+namespace {
+
+__global__ void dl_count(int64_t m, const int32_t* ei, const int32_t* ej, int32_t* up,
+                         int32_t* lo) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    atomicAdd(up + ei[e], 1);
+    atomicAdd(lo + ej[e], 1);
+  }
+}
+
+__global__ void dl_len(int64_t n, const int32_t* up, const int32_t* lo, int64_t* len,
+                       int64_t* up64, double* diag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride) {
+    len[v] = (int64_t)up[v] + lo[v];
+    up64[v] = up[v];
+    diag[v] = (double)((int64_t)up[v] + lo[v]);   // unit weights: exact
+  }
+}
+
+// row v: lower neighbours (ascending) then upper neighbours (ascending)
+__global__ void dl_scatter_upper(int64_t m, const int32_t* ei, const int32_t* ej,
+                                 const int64_t* rp, const int32_t* lo, const int64_t* ustart,
+                                 uint32_t* pcol) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+    const int32_t v = ei[e];
+    pcol[rp[v] + lo[v] + (e - ustart[v])] = (uint32_t)ej[e];
+  }
+}
+
+__global__ void dl_lower_pos(int64_t m, const int32_t* sj, const int64_t* lstart,
+                             const int64_t* rp, const int32_t* si, uint32_t* pcol) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += stride) {
+    const int32_t v = sj[p];
+    pcol[rp[v] + (p - lstart[v])] = (uint32_t)si[p];
+  }
+}
+
+inline int gridm(int64_t n) {
+  int64_t g = (n + kST - 1) / kST;
+  int64_t cap = (int64_t)dev_info().sm_count * 32;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+}  // namespace
+
+extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
+                                       const int32_t* d_j, lg_csr** out) {
+  if (!out || n < 1 || m < 0 || (m > 0 && (!d_i || !d_j)))
+    return fail(LG_EINVAL, "lg_csr_laplacian_device: bad argument");
+  if (n >= ((int64_t)1 << 31)) return fail(LG_EINVAL, "lg_csr_laplacian_device: n too large");
+  int cbits = 1;
+  while (((int64_t)1 << cbits) < n) ++cbits;
+  if (cbits > 31) return fail(LG_EINVAL, "lg_csr_laplacian_device: n too large for packing");
+  lg_csr* a = new lg_csr();
+  a->n = n;
+  a->nnz = n + 2 * m;
+  a->packed = 1;
+  a->cbits = cbits;
+  a->nvals = 1;
+  a->noff = 2 * m;
+  int32_t *up = nullptr, *lo = nullptr, *sj = nullptr, *si = nullptr;
+  int64_t *len = nullptr, *up64 = nullptr, *lo64 = nullptr, *ustart = nullptr,
+          *lstart = nullptr;
+  void* tmp = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(up);
+    cudaFree(lo);
+    cudaFree(sj);
+    cudaFree(si);
+    cudaFree(len);
+    cudaFree(up64);
+    cudaFree(lo64);
+    cudaFree(ustart);
+    cudaFree(lstart);
+    cudaFree(tmp);
+  };
+  bool ok = cudaMalloc(&up, 4 * (size_t)n) == cudaSuccess &&
+            cudaMalloc(&lo, 4 * (size_t)n) == cudaSuccess &&
+            cudaMalloc(&len, 8 * (size_t)n) == cudaSuccess &&
+            cudaMalloc(&up64, 8 * (size_t)n) == cudaSuccess &&
+            cudaMalloc(&lo64, 8 * (size_t)n) == cudaSuccess &&
+            cudaMalloc(&ustart, 8 * (size_t)n) == cudaSuccess &&
+            cudaMalloc(&lstart, 8 * (size_t)n) == cudaSuccess &&
+            cudaMalloc(&a->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
+            cudaMalloc(&a->pdiag, 8 * (size_t)n) == cudaSuccess &&
+            cudaMalloc(&a->table, 8) == cudaSuccess &&
+            cudaMalloc(&a->pcol, 4 * (size_t)std::max<int64_t>(2 * m, 1)) == cudaSuccess &&
+            (m == 0 || (cudaMalloc(&sj, 4 * (size_t)m) == cudaSuccess &&
+                        cudaMalloc(&si, 4 * (size_t)m) == cudaSuccess));
+  if (!ok) {
+    cleanup();
+    lg_csr_destroy(a);
+    return fail(LG_ENOMEM, "lg_csr_laplacian_device: allocation failed");
+  }
+  const double minus_one = -1.0;
+  cudaMemcpy(a->table, &minus_one, 8, cudaMemcpyHostToDevice);
+  cudaMemset(up, 0, 4 * (size_t)n);
+  cudaMemset(lo, 0, 4 * (size_t)n);
+  if (m) dl_count<<<gridm(m), kST>>>(m, d_i, d_j, up, lo);
+  // lo64 = lo counts as int64 for the lower-run starts
+  dl_len<<<gridm(n), kST>>>(n, up, lo, len, up64, a->pdiag);
+  size_t tb = 0, t2 = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, len, a->prp + 1, (int64_t)n);
+  cub::DeviceScan::ExclusiveSum(nullptr, t2, up64, ustart, (int64_t)n);
+  tb = std::max(tb, t2);
+  if (m) {
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, d_j, sj, d_i, si, (int64_t)m, 0, cbits);
+    tb = std::max(tb, t2);
+  }
+  if (cudaMalloc(&tmp, tb) != cudaSuccess) {
+    cleanup();
+    lg_csr_destroy(a);
+    return fail(LG_ENOMEM, "lg_csr_laplacian_device: temp alloc");
+  }
+  cudaMemset(a->prp, 0, 8);
+  cub::DeviceScan::InclusiveSum(tmp, tb, len, a->prp + 1, (int64_t)n);
+  cub::DeviceScan::ExclusiveSum(tmp, tb, up64, ustart, (int64_t)n);
+  if (m) {
+    // stable radix sort by j keeps ascending i inside every key run
+    cub::DeviceRadixSort::SortPairs(tmp, tb, d_j, sj, d_i, si, (int64_t)m, 0, cbits);
+    // lower-run starts: exclusive scan of the lower counts
+    dl_len<<<gridm(n), kST>>>(n, lo, up, len, lo64, a->pdiag);  // lo64 = lo
+    cub::DeviceScan::ExclusiveSum(tmp, tb, lo64, lstart, (int64_t)n);
+    dl_lower_pos<<<gridm(m), kST>>>(m, sj, lstart, a->prp, si, a->pcol);
+    dl_scatter_upper<<<gridm(m), kST>>>(m, d_i, d_j, a->prp, lo, ustart, a->pcol);
+  }
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    cleanup();
+    lg_csr_destroy(a);
+    return fail(LG_ECUDA, std::string("lg_csr_laplacian_device: ") + cudaGetErrorString(err));
+  }
+  cleanup();
+  // row-block schedule from the off-diagonal row pointers (host, O(n))
+  std::vector<int64_t> prp((size_t)n + 1);
+  cudaMemcpy(prp.data(), a->prp, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost);
+  std::vector<SpmvBlock> blocks;
+  std::vector<int32_t> lnp;
+  std::vector<int64_t> lfirst;
+  build_schedule(n, prp.data(), blocks, lnp, lfirst);
+  a->nblocks = (int64_t)blocks.size();
+  a->nlong = (int64_t)lnp.size();
+  for (int32_t v : lnp) a->nparts += v;
+  if ((a->nblocks &&
+       cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess) ||
+      (a->nlong && (cudaMalloc(&a->long_nparts, 4 * (size_t)a->nlong) != cudaSuccess ||
+                    cudaMalloc(&a->long_first, 8 * (size_t)a->nlong) != cudaSuccess))) {
+    lg_csr_destroy(a);
+    return fail(LG_ENOMEM, "lg_csr_laplacian_device: schedule alloc");
+  }
+  if (a->nblocks)
+    cudaMemcpy(a->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
+  if (a->nlong) {
+    cudaMemcpy(a->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(a->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
+  }
+  // the plain arrays are not materialised (device-only matrix)
+  *out = a;
+  return LG_OK;
+}
+
+// Device diagonal (degrees) of a packed matrix, for Jacobi preconditioning
+// of device-only matrices.
+extern "C" int lg_csr_diagonal(const lg_csr* a, double* d_out) {
+  if (!a || !d_out) return fail(LG_EINVAL, "lg_csr_diagonal: bad argument");
+  if (!a->packed) return fail(LG_EINVAL, "lg_csr_diagonal: only for packed matrices");
+  LG_CUDA(cudaMemcpy(d_out, a->pdiag, 8 * (size_t)a->n, cudaMemcpyDeviceToDevice));
   return LG_OK;
 }
 
