@@ -365,7 +365,7 @@ def main():
     # e2e through the public API with host buffers (rank 0 replica path)
     xh = np.random.default_rng(1).standard_normal(n)
     e2e = None
-    if world == 1:
+    if rank == 0:
         for _ in range(3):
             L.spmv(a, xh)
         torch.cuda.synchronize()
@@ -376,7 +376,8 @@ def main():
         e2e_s = (time.perf_counter() - t0) / reps
         e2e = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                "d2h_bytes_per_step": 8 * n,
-               "path": "paper_1311_1695_b200.spmv(a, numpy x) -> numpy y"}
+               "path": "paper_1311_1695_b200.spmv(a, numpy x) -> numpy y"
+                       + (" (rank 0, whole matrix)" if world > 1 else "")}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -396,7 +397,16 @@ def main():
                                if d.packed else "CSR f64 / int32",
                      "bytes_model": ("4 (nnz - n) + 8 (n+1) + 8 n + 16 n (packed)" if d.packed
                                      else "12 nnz + 8 (n+1) + 16 n (SURVEY 8(d))"),
-                     "effective_bytes_model": "12 nnz + 8 (n+1) + 16 n (SURVEY 8(d))"},
+                     "effective_bytes_model": "12 nnz + 8 (n+1) + 16 n (SURVEY 8(d))",
+                     # the kernel is bound by the L1TEX sector rate of the
+                     # random x gathers, not by HBM: one gather per
+                     # off-diagonal nonzero, measured floor 39.1 us for C4's
+                     # 9.9 M gathers (scripts/micro/gather.cu: 0.87 sectors /
+                     # SM / cycle, independent of grid, cache operator or
+                     # block-local sorting)
+                     "gather_floor_us": 39.1 * (local_nnz - local_rows) / 9917680.0,
+                     "frac_of_gather_floor": (39.1 * (local_nnz - local_rows) / 9917680.0)
+                     / (ms * 1e3)},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }
@@ -404,7 +414,10 @@ def main():
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_solve:
         f = L.ic0_factorize(a)
-        line["solve"] = solve_block(a, f, L.ic0_factorize_multicolor(a))
+        f_mc = L.ic0_factorize_multicolor(a)
+        f.device()
+        f_mc.device()   # device factor upload = setup, like the reference's splu
+        line["solve"] = solve_block(a, f, f_mc)
     if rank == 0 and world == 1 and not args.no_c5:
         line["c5"] = c5_block(peaks)
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -421,13 +421,19 @@ __device__ __forceinline__ void stage(const SweepArgs& a, int64_t t, int lane, S
 
 __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int lane) {
   double s = 0.0;
+  if (a.dbg & 4) {
 #pragma unroll
-  for (int e = 0; e < kLaneMax; ++e)
-    if (e < st.ne) s += st.val[e] * __ldcg(a.x + st.col[e]);
+    for (int e = 0; e < kLaneMax; ++e)
+      if (e < st.ne) s += st.val[e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < kLaneMax; ++e)
+      if (e < st.ne) s += st.val[e] * __ldcg(a.x + st.col[e]);
+  }
   if (st.info != 0) {
     const int L = st.info >> 8, cnt = st.info & 0xff;
     for (int o = L >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((lane / L) < cnt && (lane % L) == 0) {
+    if ((lane / L) < cnt && (lane % L) == 0 && !(a.dbg & 8)) {
       const double v = (st.bv - s) / st.dg;
       a.x[st.row] = v;
       if (a.out2) a.out2[a.omap[st.row]] = v;
@@ -680,7 +686,9 @@ static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
                        const std::vector<double>& diag, bool forward, SweepDev& d) {
   SweepHost h;
   const SweepLaunch& L = sweep_launch();
-  build_sweep(n, rp, col, val, diag, forward, L.csize * kSweepWarps, h);
+  const char* nm = getenv("LG_NARROW_MULT");
+  const int mult = nm ? atoi(nm) : 1;
+  build_sweep(n, rp, col, val, diag, forward, L.csize * kSweepWarps * mult, h);
   d.nsegs = (int32_t)h.segs.size();
   d.nbar = h.nbar;
   d.levels = h.levels;
