@@ -174,6 +174,8 @@ int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
  * entries) receives the last apply's timestamps.  Returns the number of
  * segments (forward + backward). */
 int lg_ic0_trace(lg_ic0* f, int enable, unsigned long long* host_out, int cap);
+/* Debug: dataflow-sweep task timestamps {level, start, ready, done} (ns). */
+int lg_ic0_flow_trace(lg_ic0* f, int enable, unsigned long long* host_out, int cap);
 /* Debug: per-segment {tasks, narrow, barrier, 0} of one sweep. */
 int lg_ic0_schedule(const lg_ic0* f, int backward, int* host_out, int cap);
 /* Jacobi (diagonal) apply z = r / diag, a flagged non-reference variant. */

@@ -105,6 +105,7 @@ _SIGS = {
     "lg_ic0_info": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_ic0_apply": (c_int, [c_p, c_p, c_p, c_p, c_p]),
     "lg_ic0_trace": (c_int, [c_p, c_int, c_p, c_int]),
+    "lg_ic0_flow_trace": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_ic0_schedule": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_diag_apply": (c_int, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "lg_fused": (c_int, [c_p, c_p, c_p]),

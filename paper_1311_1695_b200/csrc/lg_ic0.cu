@@ -58,6 +58,12 @@ struct SweepSeg {
   int32_t pad;
 };
 
+struct RowInfo {   // per permuted row position (dataflow sweep)
+  double dg;       // diagonal
+  int32_t xrow;    // row of x written (factor numbering)
+  int32_t bidx;    // index of b read
+};
+
 // Device data of one sweep direction.  Rows are stored PERMUTED into
 // processing order (level, length class), so a level's nonzeros are one
 // contiguous stream and a task needs one row-pointer load.
@@ -76,6 +82,14 @@ struct SweepDev {
   unsigned* hub_ticket = nullptr;
   double* hub_part = nullptr;
   unsigned long long* bar = nullptr;
+  int32_t* tlevel = nullptr;      // level of every task
+  int32_t* lexpect = nullptr;     // [levels * 32] tasks per (level, shard)
+  unsigned* lcount = nullptr;     // [levels * 32] completion counters
+  unsigned long long* ttrace = nullptr;   // debug: dataflow per-task timestamps
+  RowInfo* rinfo = nullptr;       // dataflow row records, permuted order
+  int32_t* oidx = nullptr;        // permuted row -> second-output index (or NULL)
+  int32_t ntasks = 0;
+  int32_t nparts = 0;        // hub partial slots
   int32_t nsegs = 0;
   int32_t nbar = 0;          // grid barriers per sweep
   int levels = 0;
@@ -195,6 +209,7 @@ struct SweepHost {
   std::vector<uint16_t> lanetab;  // per task x lane: rel_start << 5 | count
   std::vector<SweepSeg> segs;
   std::vector<int32_t> hub_first, hub_nchunk;
+  std::vector<int32_t> tlevel, lexpect;
   int32_t nparts = 0;
   int32_t nbar = 0;
   int levels = 0;
@@ -296,7 +311,10 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
     }
     const int32_t t1 = (int32_t)h.tasks.size();
     h.segs.push_back({t0, t1, (t1 - t0) <= narrow_tasks ? 1 : 0, 0, 0, 0});
+    for (int32_t t = t0; t < t1; ++t) h.tlevel.push_back(l);
   }
+  h.lexpect.assign((size_t)nl * 32, 0);
+  for (size_t t = 0; t < h.tlevel.size(); ++t) h.lexpect[(size_t)h.tlevel[t] * 32 + (t & 31)]++;
   for (size_t sg = h.segs.size(); sg-- > 0;) {
     const bool same = sg + 1 < h.segs.size() && h.segs[sg + 1].narrow == h.segs[sg].narrow;
     h.segs[sg].run_t1 = same ? h.segs[sg + 1].run_t1 : h.segs[sg].t1;
@@ -621,6 +639,273 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
   }
 }
 
+// ---- dataflow sweep (default) ------------------------------------------------
+// The solution vector is its own dependency flag: before a sweep x is filled
+// with an all-ones NaN sentinel, every row is stored once with a relaxed
+// 8-byte store (never the sentinel: a computed all-ones NaN is canonicalised)
+// and a consumer re-polls exactly the entries it still sees as the sentinel.
+// A dependency hop then costs one L2 store + one L2 load (~0.33 us measured,
+// scripts/micro/chain.cu) instead of a fence + flag + acquire (~0.9 us), and
+// no warp ever waits for a whole level -- only for the rows it reads.
+//
+// Warp w (of W workers) walks tasks t = w, w+W, ... in level order, staging
+// task t+W while it completes task t.  Everything a task needs is at most
+// three dependent loads away: the task descriptor / lane table, then the
+// lane's columns + values + the row record {diag, x row, b index}, then the
+// x gathers and b.  To keep polling traffic off L2, a task of level L only
+// starts once levels <= L - gate are fully counted: one poller warp per CTA
+// watches relaxed per-(level, shard) completion counters and publishes the
+// highest complete level in shared memory (the counts only throttle;
+// correctness rests on the sentinels).  Deadlock freedom: every task depends
+// only on tasks of lower levels, which precede it in their own warps' lists,
+// and the cooperative launch keeps all warps resident.
+constexpr unsigned long long kSentinel = ~0ull;
+constexpr int kFlowThreads = 384;   // 1 poller + 11 worker warps, one CTA per SM
+
+struct FlowArgs {
+  const int64_t* prp;
+  const int32_t* pcol;
+  const double* pval;
+  const RowInfo* rinfo;
+  const int32_t* oidx;   // permuted row -> out2 index (NULL: no second output)
+  const SweepTask* tasks;
+  const int64_t* tbase;
+  const uint16_t* lanetab;
+  const int32_t* tlevel;
+  const int32_t* lexpect;
+  unsigned* lcount;
+  const int32_t* hub_first;
+  const int32_t* hub_nchunk;
+  double* hub_part;
+  const double* b;
+  double* x;
+  double* out2;
+  const int* skip;
+  unsigned long long* ttrace;   // debug: per task {start, inputs ready, done}
+  int32_t ntasks;
+  int32_t levels;
+  int32_t gate;
+};
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  if (__double_as_longlong(v) == (long long)kSentinel) v = __longlong_as_double(0x7ff8000000000000ll);
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void red_relaxed_add(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ bool is_sentinel(double v) {
+  return __double_as_longlong(v) == (long long)kSentinel;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void flow_init_kernel(double* x, int64_t n, unsigned* cnt, int ncnt, double* part,
+                                 int npart, const int* skip) {
+  if (skip && *skip) return;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i < ncnt; i += st) cnt[i] = 0u;
+  for (int64_t i = i0; i < npart; i += st) part[i] = __longlong_as_double((long long)kSentinel);
+  for (int64_t i = i0; i < n; i += st) x[i] = __longlong_as_double((long long)kSentinel);
+}
+
+// Task staging in two non-blocking phases (phase 2 one task later).
+struct FStage1 {
+  SweepTask tk;
+  int64_t base;
+  uint32_t lt;
+  int32_t lev;
+};
+struct FStaged {
+  int32_t info;   // task.b (0: hub chunk)
+  int32_t p;      // pack: permuted row of the lane's group (-1: idle) | chunk: permuted hub row
+  int32_t c, hid; // chunk: chunk index, hub id
+  int32_t ne, sh, lev;
+  int32_t col[kLaneMax];
+  double val[kLaneMax];
+  RowInfo ri;
+};
+
+__device__ __forceinline__ void fstage1(const FlowArgs& a, int64_t t, int lane, FStage1& s) {
+  s.tk = a.tasks[t];
+  s.base = a.tbase[t];
+  s.lt = a.lanetab[t * 32 + lane];
+  s.lev = a.tlevel[t];
+}
+
+__device__ __forceinline__ void fstage2(const FlowArgs& a, const FStage1& s, int lane,
+                                        FStaged& st) {
+  const SweepTask tk = s.tk;
+  st.info = tk.b;
+  st.lev = s.lev;
+  st.ne = s.lt & 31;
+  const int64_t lo = s.base + (s.lt >> 5);
+  if (tk.b != 0) {
+    const int L = tk.b >> 8, cnt = tk.b & 0xff;
+    st.sh = __ffs(L) - 1;
+    st.p = -1;
+    if ((lane >> st.sh) < cnt) {
+      st.p = tk.p + (lane >> st.sh);
+      st.ri = a.rinfo[st.p];
+    }
+  } else {
+    st.p = tk.p;
+    st.c = tk.c;
+    st.hid = tk.d;
+    st.sh = 5;
+    if (tk.c == 0) st.ri = a.rinfo[tk.p];
+  }
+#pragma unroll
+  for (int e = 0; e < kLaneMax; ++e) {
+    if (e < st.ne) {
+      const int64_t k = lo + ((int64_t)e << st.sh);
+      st.col[e] = a.pcol[k];
+      st.val[e] = a.pval[k];
+    }
+  }
+}
+
+__device__ __forceinline__ void publish(const FlowArgs& a, int32_t p, const RowInfo& ri, double v) {
+  st_relaxed_f64(a.x + ri.xrow, v);
+  if (a.out2) a.out2[a.oidx[p]] = v;
+}
+
+__device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& st, int lane,
+                                              unsigned long long* tr) {
+  const bool owner = st.info != 0 ? (st.p >= 0 && (lane & ((1 << st.sh) - 1)) == 0)
+                                  : (st.c == 0 && lane == 0);
+  double bv = 0.0;
+  if (owner) bv = a.b[st.ri.bidx];
+  double xv[kLaneMax];
+  unsigned miss = 0;
+#pragma unroll
+  for (int e = 0; e < kLaneMax; ++e) {
+    if (e < st.ne) {
+      xv[e] = ld_relaxed_f64(a.x + st.col[e]);
+      if (is_sentinel(xv[e])) miss |= 1u << e;
+    }
+  }
+  unsigned spins = 0;
+  while (__any_sync(0xffffffffu, miss != 0)) {
+    __nanosleep(20);
+    if (++spins > (1u << 24)) __trap();   // a row never produced: abort, do not hang
+#pragma unroll
+    for (int e = 0; e < kLaneMax; ++e) {
+      if (miss & (1u << e)) {
+        xv[e] = ld_relaxed_f64(a.x + st.col[e]);
+        if (!is_sentinel(xv[e])) miss &= ~(1u << e);
+      }
+    }
+  }
+  if (tr && lane == 0) tr[1] = gtimer();
+  double s = 0.0;
+#pragma unroll
+  for (int e = 0; e < kLaneMax; ++e)
+    if (e < st.ne) s += st.val[e] * xv[e];
+  if (st.info != 0) {
+    for (int o = 1 << (st.sh - 1); o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (owner) publish(a, st.p, st.ri, (bv - s) / st.ri.dg);
+    return;
+  }
+  // chunk of a hub row: every chunk but the first publishes its partial
+  // with a relaxed store (sentinel-initialised slots); chunk 0 sums them
+  // lane-strided + butterfly, a fixed order whoever finishes last
+  s = warp_sum(s);
+  const int32_t first = a.hub_first[st.hid], nch = a.hub_nchunk[st.hid];
+  if (st.c != 0) {
+    if (lane == 0) st_relaxed_f64(a.hub_part + first + st.c, s);
+    return;
+  }
+  double t = 0.0;
+  for (int32_t c = lane; c < nch; c += 32) {
+    double v = s;
+    if (c != 0) {
+      v = ld_relaxed_f64(a.hub_part + first + c);
+      for (unsigned k = 0; is_sentinel(v); ++k) {
+        if (k > (1u << 24)) __trap();
+        __nanosleep(20);
+        v = ld_relaxed_f64(a.hub_part + first + c);
+      }
+    }
+    t += v;
+  }
+  t = warp_sum(t);
+  if (lane == 0) publish(a, st.p, st.ri, (bv - t) / st.ri.dg);
+}
+
+__global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a) {
+  if (a.skip && *a.skip) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWorkers = kFlowThreads / 32 - 1;
+  __shared__ volatile int s_done;
+  __shared__ volatile int s_active;
+  if (threadIdx.x == 0) {
+    s_done = -1;
+    s_active = kWorkers;
+  }
+  __syncthreads();
+  const int gate = a.gate;
+  if (warp == 0) {   // level watcher
+    for (int L = 0; L < a.levels - gate; ++L) {
+      const int idx = L * 32 + lane;
+      const unsigned want = (unsigned)a.lexpect[idx];
+      while (true) {
+        const unsigned v = ld_relaxed_u32(a.lcount + idx);
+        if (__all_sync(0xffffffffu, v >= want)) break;
+        if (s_active == 0) return;
+        __nanosleep(32);
+      }
+      s_done = L;
+    }
+    return;
+  }
+  const int64_t W = (int64_t)gridDim.x * kWorkers;
+  const int64_t nt = a.ntasks;
+  int64_t t = (int64_t)blockIdx.x * kWorkers + warp - 1;
+  if (t < nt) {
+    FStaged st, stn;
+    FStage1 s1n;
+    {
+      FStage1 s1;
+      fstage1(a, t, lane, s1);
+      fstage2(a, s1, lane, st);
+    }
+    if (t + W < nt) fstage1(a, t + W, lane, s1n);
+    for (; t < nt; t += W) {
+      FStage1 s1nn;
+      if (t + 2 * W < nt) fstage1(a, t + 2 * W, lane, s1nn);
+      if (t + W < nt) fstage2(a, s1n, lane, stn);
+      for (unsigned spins = 0; s_done < st.lev - gate; ++spins) {
+        __nanosleep(32);
+        if (spins > (1u << 24)) __trap();
+      }
+      unsigned long long* tr = a.ttrace ? a.ttrace + 3 * t : nullptr;
+      if (tr && lane == 0) tr[0] = gtimer();
+      flow_complete(a, st, lane, tr);
+      if (tr && lane == 0) tr[2] = gtimer();
+      if (lane == 0) red_relaxed_add(a.lcount + st.lev * 32 + (t & 31), 1u);
+      st = stn;
+      s1n = s1nn;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) atomicSub((int*)&s_active, 1);
+}
+
 template <typename T>
 static bool upload(T** dst, const std::vector<T>& v) {
   if (v.empty()) return true;
@@ -681,9 +966,12 @@ static SweepLaunch& sweep_launch() {
   return L;
 }
 
+// omap (permuted factor, else NULL): factor row -> original row; the forward
+// sweep reads b there and the backward sweep writes its second output there.
 static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
                        const std::vector<int32_t>& col, const std::vector<double>& val,
-                       const std::vector<double>& diag, bool forward, SweepDev& d) {
+                       const std::vector<double>& diag, bool forward, const int32_t* omap,
+                       SweepDev& d) {
   SweepHost h;
   const SweepLaunch& L = sweep_launch();
   const char* nm = getenv("LG_NARROW_MULT");
@@ -696,7 +984,26 @@ static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
             upload(&d.perm, h.perm) && upload(&d.pdiag, h.pdiag) && upload(&d.tasks, h.tasks) &&
             upload(&d.tbase, h.tbase) && upload(&d.lanetab, h.lanetab) &&
             upload(&d.segs, h.segs) && upload(&d.hub_first, h.hub_first) &&
-            upload(&d.hub_nchunk, h.hub_nchunk);
+            upload(&d.hub_nchunk, h.hub_nchunk) && upload(&d.tlevel, h.tlevel) &&
+            upload(&d.lexpect, h.lexpect);
+  d.ntasks = (int32_t)h.tasks.size();
+  d.nparts = h.nparts;
+  {
+    std::vector<RowInfo> ri((size_t)n);
+    std::vector<int32_t> oi;
+    for (int64_t p = 0; p < n; ++p) {
+      const int32_t r = h.perm[(size_t)p];
+      ri[(size_t)p] = {h.pdiag[(size_t)p], r, (forward && omap) ? omap[r] : r};
+    }
+    if (!forward && omap) {
+      oi.resize((size_t)n);
+      for (int64_t p = 0; p < n; ++p) oi[(size_t)p] = omap[h.perm[(size_t)p]];
+    }
+    ok = ok && upload(&d.rinfo, ri) && upload(&d.oidx, oi);
+  }
+  if (ok && !h.lexpect.empty())
+    ok = cudaMalloc(&d.lcount, 4 * h.lexpect.size()) == cudaSuccess &&
+         cudaMemset(d.lcount, 0, 4 * h.lexpect.size()) == cudaSuccess;
   if (!ok) return false;
   if (!h.hub_first.empty()) {
     if (cudaMalloc(&d.hub_ticket, sizeof(unsigned) * h.hub_first.size()) != cudaSuccess ||
@@ -725,6 +1032,12 @@ static void free_sweep(SweepDev& d) {
   cudaFree(d.hub_ticket);
   cudaFree(d.hub_part);
   cudaFree(d.bar);
+  cudaFree(d.tlevel);
+  cudaFree(d.lexpect);
+  cudaFree(d.lcount);
+  cudaFree(d.ttrace);
+  cudaFree(d.rinfo);
+  cudaFree(d.oidx);
   d = SweepDev();
 }
 
@@ -757,6 +1070,76 @@ static SweepArgs sweep_args(const SweepDev& d, const double* b, double* x, const
   const char* dbg = getenv("LG_SWEEP_DBG");
   a.dbg = dbg ? atoi(dbg) : 0;
   return a;
+}
+
+// LG_SWEEP_MODE=0 selects the level-barrier sweep (kept for comparison and
+// for the per-level trace); the default is the dataflow sweep.
+static int sweep_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("LG_SWEEP_MODE");
+    mode = e ? atoi(e) : 1;
+  }
+  return mode;
+}
+
+static int sweep_gate() {
+  static int g = -1;
+  if (g < 0) {
+    const char* e = getenv("LG_SWEEP_GATE");
+    g = e ? std::max(1, atoi(e)) : 3;
+  }
+  return g;
+}
+
+static int launch_flow(const SweepDev& dv, int64_t n, const double* b, double* x, double* out2,
+                       const int* skip, cudaStream_t s) {
+  static int grid = 0;
+  if (!grid) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_flow_kernel, kFlowThreads, 0) !=
+            cudaSuccess ||
+        occ < 1)
+      occ = 1;
+    grid = occ * dev_info().sm_count;
+  }
+  flow_init_kernel<<<vec_grid(std::max<int64_t>(n, 1)), kThreads, 0, s>>>(
+      x, n, dv.lcount, dv.levels * 32, dv.hub_part, dv.nparts, skip);
+  LG_CUDA(cudaGetLastError());
+  FlowArgs a;
+  a.prp = dv.prp;
+  a.pcol = dv.pcol;
+  a.pval = dv.pval;
+  a.rinfo = dv.rinfo;
+  a.oidx = dv.oidx;
+  a.tasks = dv.tasks;
+  a.tbase = dv.tbase;
+  a.lanetab = dv.lanetab;
+  a.tlevel = dv.tlevel;
+  a.lexpect = dv.lexpect;
+  a.lcount = dv.lcount;
+  a.hub_first = dv.hub_first;
+  a.hub_nchunk = dv.hub_nchunk;
+  a.hub_part = dv.hub_part;
+  a.b = b;
+  a.x = x;
+  a.out2 = out2;
+  a.skip = skip;
+  a.ttrace = dv.ttrace;
+  a.ntasks = dv.ntasks;
+  a.levels = dv.levels;
+  a.gate = sweep_gate();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kFlowThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;   // all warps co-resident
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_flow_kernel, a));
+  return LG_OK;
 }
 
 static int launch_sweep(SweepArgs& args, cudaStream_t s) {
@@ -891,25 +1274,26 @@ int lg_ic0_create_perm(int64_t n, const int64_t* l_rp, const int64_t* l_col,
         fill[(size_t)j]++;
       }
   }
-  lg_ic0* f = new lg_ic0();
-  f->n = n;
-  f->nnz_l = nnz;
-  bool ok = make_sweep(n, frp, fcol, fval, dg, true, f->fwd) &&
-            make_sweep(n, brp, bcol, bval, dg, false, f->bwd) && upload(&f->diag, dg) &&
-            (n == 0 || cudaMalloc(&f->tmp, 8 * (size_t)n) == cudaSuccess);
-  if (ok && perm_h) {
-    std::vector<int32_t> om((size_t)n);
+  std::vector<int32_t> om;
+  if (perm_h) {
+    om.resize((size_t)n);
     std::vector<char> seen((size_t)n, 0);
     for (int64_t i = 0; i < n; ++i) {
-      if (perm_h[i] < 0 || perm_h[i] >= n || seen[(size_t)perm_h[i]]) {
-        lg_ic0_destroy(f);
+      if (perm_h[i] < 0 || perm_h[i] >= n || seen[(size_t)perm_h[i]])
         return fail(LG_EINVAL, "lg_ic0_create_perm: perm is not a permutation");
-      }
       seen[(size_t)perm_h[i]] = 1;
       om[(size_t)i] = (int32_t)perm_h[i];
     }
-    ok = upload(&f->omap, om) && cudaMalloc(&f->zp, 8 * (size_t)n) == cudaSuccess;
   }
+  const int32_t* omp = perm_h ? om.data() : nullptr;
+  lg_ic0* f = new lg_ic0();
+  f->n = n;
+  f->nnz_l = nnz;
+  bool ok = make_sweep(n, frp, fcol, fval, dg, true, omp, f->fwd) &&
+            make_sweep(n, brp, bcol, bval, dg, false, omp, f->bwd) && upload(&f->diag, dg) &&
+            (n == 0 || cudaMalloc(&f->tmp, 8 * (size_t)n) == cudaSuccess);
+  if (ok && perm_h)
+    ok = upload(&f->omap, om) && cudaMalloc(&f->zp, 8 * (size_t)n) == cudaSuccess;
   if (!ok) {
     lg_ic0_destroy(f);
     return fail(LG_ENOMEM, "lg_ic0_create: device allocation / upload failed");
@@ -943,6 +1327,44 @@ int lg_ic0_trace(lg_ic0* f, int enable, unsigned long long* host_out, int cap) {
   if (!enable && f->trace) {
     cudaFree(f->trace);
     f->trace = nullptr;
+  }
+  return total;
+}
+
+// Debug: dataflow sweep task timestamps.  enable=1 allocates the buffers
+// (the following applies record); host_out receives, per sweep direction,
+// ntasks records {level, start, inputs ready, done} (ns, globaltimer).
+// Returns the total number of records (fwd + bwd).
+int lg_ic0_flow_trace(lg_ic0* f, int enable, unsigned long long* host_out, int cap) {
+  if (!f) return fail(LG_EINVAL, "lg_ic0_flow_trace: NULL handle");
+  const int total = f->fwd.ntasks + f->bwd.ntasks;
+  SweepDev* dirs[2] = {&f->fwd, &f->bwd};
+  if (enable) {
+    for (SweepDev* d : dirs)
+      if (!d->ttrace && d->ntasks &&
+          cudaMalloc(&d->ttrace, 24 * (size_t)d->ntasks) != cudaSuccess)
+        return fail(LG_ENOMEM, "lg_ic0_flow_trace: alloc");
+  }
+  if (host_out) {
+    LG_CUDA(cudaDeviceSynchronize());
+    int k = 0;
+    for (SweepDev* d : dirs) {
+      if (!d->ttrace) continue;
+      std::vector<unsigned long long> tr(3 * (size_t)d->ntasks);
+      std::vector<int32_t> lv((size_t)d->ntasks);
+      LG_CUDA(cudaMemcpy(tr.data(), d->ttrace, 24 * (size_t)d->ntasks, cudaMemcpyDeviceToHost));
+      LG_CUDA(cudaMemcpy(lv.data(), d->tlevel, 4 * (size_t)d->ntasks, cudaMemcpyDeviceToHost));
+      for (int t = 0; t < d->ntasks && 4 * (k + 1) <= cap; ++t, ++k) {
+        host_out[4 * k] = (unsigned long long)lv[(size_t)t];
+        for (int j = 0; j < 3; ++j) host_out[4 * k + 1 + j] = tr[3 * (size_t)t + j];
+      }
+    }
+  }
+  if (!enable) {
+    for (SweepDev* d : dirs) {
+      cudaFree(d->ttrace);
+      d->ttrace = nullptr;
+    }
   }
   return total;
 }
@@ -1072,6 +1494,11 @@ int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
     // layout: fwd segs, fwd inline-stage counter, bwd segs, bwd counter
     fa.trace = f->trace;
     ba.trace = f->trace + f->fwd.nsegs + 1;
+  }
+  if (sweep_mode() != 0 && !f->trace) {
+    int rc = launch_flow(f->fwd, f->n, r, f->tmp, nullptr, skip, s);
+    if (rc) return rc;
+    return launch_flow(f->bwd, f->n, f->tmp, f->omap ? f->zp : z, f->omap ? z : nullptr, skip, s);
   }
   int rc = launch_sweep(fa, s);
   if (rc) return rc;
