@@ -106,6 +106,11 @@ struct lg_ic0 {
   int32_t* omap = nullptr;   // permuted factor: factor row -> original row
   double* zp = nullptr;      // permuted factor: backward result (factor numbering)
   int grid = 0;
+  // dataflow sweeps hand their scratch state to each other: the forward
+  // sweep re-arms the backward one (x sentinels, counters, hub slots) and
+  // vice versa, so an apply is exactly two launches; false after a
+  // level-barrier apply (the state then needs one explicit re-arm)
+  mutable bool flow_armed = false;
 };
 
 namespace lg {
@@ -192,7 +197,18 @@ static int dag_levels(int64_t n, const std::vector<int64_t>& rp,
   return n ? maxl + 1 : 0;
 }
 
-static int lanes_for(int64_t len) {
+// Lanes per row.  On wide levels (many more rows than warps) tasks are
+// packed densely, one lane per row up to kLaneMax entries, to minimise the
+// number of tasks a warp walks; on narrow levels (latency-bound) rows are
+// spread over more lanes so each lane's share of the chain is short.
+static int lanes_for(int64_t len, bool wide) {
+  if (wide) {
+    if (len <= 8) return 1;
+    if (len <= 16) return 2;
+    if (len <= 32) return 4;
+    if (len <= 64) return 8;
+    return 32;
+  }
   if (len <= 4) return 2;
   if (len <= 16) return 4;
   if (len <= 64) return 8;
@@ -230,9 +246,15 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
   std::vector<int64_t> lcount((size_t)nl + 1, 0);
   for (int64_t i = 0; i < n; ++i) lcount[(size_t)level[(size_t)i] + 1]++;
   for (int l = 0; l < nl; ++l) lcount[(size_t)l + 1] += lcount[(size_t)l];
+  static const int64_t wide_rows = [] {
+    const char* e = getenv("LG_WIDE_ROWS");
+    return e ? (int64_t)atoll(e) : (int64_t)16384;
+  }();
+  std::vector<char> lwide((size_t)nl);
+  for (int l = 0; l < nl; ++l) lwide[(size_t)l] = lcount[(size_t)l + 1] - lcount[(size_t)l] > wide_rows;
   auto cls = [&](int32_t r) {
     const int64_t len = rp[(size_t)r + 1] - rp[(size_t)r];
-    return len > kHubChunk ? 64 : lanes_for(len);
+    return len > kHubChunk ? 64 : lanes_for(len, lwide[(size_t)level[(size_t)r]]);
   };
   h.perm.resize((size_t)n);
   {
@@ -312,6 +334,32 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
     const int32_t t1 = (int32_t)h.tasks.size();
     h.segs.push_back({t0, t1, (t1 - t0) <= narrow_tasks ? 1 : 0, 0, 0, 0});
     for (int32_t t = t0; t < t1; ++t) h.tlevel.push_back(l);
+  }
+  // re-lay the entries task by task, every task starting on a multiple of 4
+  // entries (16-byte aligned columns, 32-byte aligned values); lane tables
+  // are relative to the task base
+  {
+    const size_t nt = h.tasks.size();
+    std::vector<int32_t> qcol;
+    std::vector<double> qval;
+    qcol.reserve(h.pcol.size() + 4 * nt);
+    qval.reserve(h.pval.size() + 4 * nt);
+    for (size_t t = 0; t < nt; ++t) {
+      const SweepTask& tk = h.tasks[t];
+      const int64_t lo = h.tbase[t];
+      const int64_t hi = tk.b != 0 ? h.prp[(size_t)tk.p + (size_t)(tk.b & 0xff)]
+                                   : std::min<int64_t>(h.prp[(size_t)tk.p + 1], lo + kHubChunk);
+      const int64_t nb = (int64_t)qcol.size();
+      qcol.insert(qcol.end(), h.pcol.begin() + lo, h.pcol.begin() + hi);
+      qval.insert(qval.end(), h.pval.begin() + lo, h.pval.begin() + hi);
+      while (qcol.size() & 3) {
+        qcol.push_back(0);
+        qval.push_back(0.0);
+      }
+      h.tbase[t] = nb;
+    }
+    h.pcol.swap(qcol);
+    h.pval.swap(qval);
   }
   h.lexpect.assign((size_t)nl * 32, 0);
   for (size_t t = 0; t < h.tlevel.size(); ++t) h.lexpect[(size_t)h.tlevel[t] * 32 + (t & 31)]++;
@@ -663,7 +711,6 @@ constexpr unsigned long long kSentinel = ~0ull;
 constexpr int kFlowThreads = 384;   // 1 poller + 11 worker warps, one CTA per SM
 
 struct FlowArgs {
-  const int64_t* prp;
   const int32_t* pcol;
   const double* pval;
   const RowInfo* rinfo;
@@ -682,9 +729,14 @@ struct FlowArgs {
   double* out2;
   const int* skip;
   unsigned long long* ttrace;   // debug: per task {start, inputs ready, done}
+  double* next_x;               // x of the other sweep: row re-armed after its b is read
+  unsigned* next_cnt;           // the other sweep's counters / hub slots, re-armed here
+  double* next_part;
+  int32_t next_ncnt, next_npart;
   int32_t ntasks;
   int32_t levels;
   int32_t gate;
+  uint32_t backoff;   // max poll back-off (ns)
 };
 
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
@@ -782,6 +834,9 @@ __device__ __forceinline__ void fstage2(const FlowArgs& a, const FStage1& s, int
 __device__ __forceinline__ void publish(const FlowArgs& a, int32_t p, const RowInfo& ri, double v) {
   st_relaxed_f64(a.x + ri.xrow, v);
   if (a.out2) a.out2[a.oidx[p]] = v;
+  // this row's b has been consumed (by this thread, once): re-arm the row in
+  // the other sweep's x.  Safe when that buffer aliases b (z == r).
+  a.next_x[ri.xrow] = __longlong_as_double((long long)kSentinel);
 }
 
 __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& st, int lane,
@@ -799,9 +854,10 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
       if (is_sentinel(xv[e])) miss |= 1u << e;
     }
   }
-  unsigned spins = 0;
+  unsigned spins = 0, nap = 16;
   while (__any_sync(0xffffffffu, miss != 0)) {
-    __nanosleep(20);
+    __nanosleep(nap);
+    nap = min(nap * 2, a.backoff);
     if (++spins > (1u << 24)) __trap();   // a row never produced: abort, do not hang
 #pragma unroll
     for (int e = 0; e < kLaneMax; ++e) {
@@ -817,7 +873,7 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
   for (int e = 0; e < kLaneMax; ++e)
     if (e < st.ne) s += st.val[e] * xv[e];
   if (st.info != 0) {
-    for (int o = 1 << (st.sh - 1); o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    for (int o = (1 << st.sh) >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (owner) publish(a, st.p, st.ri, (bv - s) / st.ri.dg);
     return;
   }
@@ -875,6 +931,13 @@ __global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a)
   }
   const int64_t W = (int64_t)gridDim.x * kWorkers;
   const int64_t nt = a.ntasks;
+  {
+    const int64_t i0 = (int64_t)blockIdx.x * (kFlowThreads - 32) + threadIdx.x - 32;
+    const int64_t stride = (int64_t)gridDim.x * (kFlowThreads - 32);
+    for (int64_t i = i0; i < a.next_ncnt; i += stride) a.next_cnt[i] = 0u;
+    for (int64_t i = i0; i < a.next_npart; i += stride)
+      a.next_part[i] = __longlong_as_double((long long)kSentinel);
+  }
   int64_t t = (int64_t)blockIdx.x * kWorkers + warp - 1;
   if (t < nt) {
     FStaged st, stn;
@@ -980,7 +1043,7 @@ static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
   d.nsegs = (int32_t)h.segs.size();
   d.nbar = h.nbar;
   d.levels = h.levels;
-  bool ok = upload(&d.prp, h.prp) && upload(&d.pcol, h.pcol) && upload(&d.pval, h.pval) &&
+  bool ok = upload(&d.pcol, h.pcol) && upload(&d.pval, h.pval) &&
             upload(&d.perm, h.perm) && upload(&d.pdiag, h.pdiag) && upload(&d.tasks, h.tasks) &&
             upload(&d.tbase, h.tbase) && upload(&d.lanetab, h.lanetab) &&
             upload(&d.segs, h.segs) && upload(&d.hub_first, h.hub_first) &&
@@ -1092,8 +1155,8 @@ static int sweep_gate() {
   return g;
 }
 
-static int launch_flow(const SweepDev& dv, int64_t n, const double* b, double* x, double* out2,
-                       const int* skip, cudaStream_t s) {
+static int launch_flow(const SweepDev& dv, const SweepDev& other, const double* b, double* x,
+                       double* out2, double* next_x, const int* skip, cudaStream_t s) {
   static int grid = 0;
   if (!grid) {
     int occ = 0;
@@ -1103,11 +1166,7 @@ static int launch_flow(const SweepDev& dv, int64_t n, const double* b, double* x
       occ = 1;
     grid = occ * dev_info().sm_count;
   }
-  flow_init_kernel<<<vec_grid(std::max<int64_t>(n, 1)), kThreads, 0, s>>>(
-      x, n, dv.lcount, dv.levels * 32, dv.hub_part, dv.nparts, skip);
-  LG_CUDA(cudaGetLastError());
   FlowArgs a;
-  a.prp = dv.prp;
   a.pcol = dv.pcol;
   a.pval = dv.pval;
   a.rinfo = dv.rinfo;
@@ -1126,9 +1185,18 @@ static int launch_flow(const SweepDev& dv, int64_t n, const double* b, double* x
   a.out2 = out2;
   a.skip = skip;
   a.ttrace = dv.ttrace;
+  a.next_x = next_x;
+  a.next_cnt = other.lcount;
+  a.next_ncnt = other.levels * 32;
+  a.next_part = other.hub_part;
+  a.next_npart = other.nparts;
   a.ntasks = dv.ntasks;
   a.levels = dv.levels;
   a.gate = sweep_gate();
+  {
+    const char* e = getenv("LG_SWEEP_BACKOFF");
+    a.backoff = e ? (uint32_t)std::max(16, atoi(e)) : 16u;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kFlowThreads);
@@ -1294,6 +1362,13 @@ int lg_ic0_create_perm(int64_t n, const int64_t* l_rp, const int64_t* l_col,
             (n == 0 || cudaMalloc(&f->tmp, 8 * (size_t)n) == cudaSuccess);
   if (ok && perm_h)
     ok = upload(&f->omap, om) && cudaMalloc(&f->zp, 8 * (size_t)n) == cudaSuccess;
+  if (ok && n) {   // arm the dataflow forward sweep (all-ones = the x sentinel)
+    ok = cudaMemset(f->tmp, 0xff, 8 * (size_t)n) == cudaSuccess;
+    for (SweepDev* d : {&f->fwd, &f->bwd})
+      if (ok && d->nparts)
+        ok = cudaMemset(d->hub_part, 0xff, 8 * (size_t)d->nparts) == cudaSuccess;
+    f->flow_armed = ok;
+  }
   if (!ok) {
     lg_ic0_destroy(f);
     return fail(LG_ENOMEM, "lg_ic0_create: device allocation / upload failed");
@@ -1496,10 +1571,18 @@ int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
     ba.trace = f->trace + f->fwd.nsegs + 1;
   }
   if (sweep_mode() != 0 && !f->trace) {
-    int rc = launch_flow(f->fwd, f->n, r, f->tmp, nullptr, skip, s);
+    double* zx = f->omap ? f->zp : z;
+    if (!f->flow_armed) {   // arm the forward sweep (creation, or after a barrier apply)
+      flow_init_kernel<<<vec_grid(f->n), kThreads, 0, s>>>(
+          f->tmp, f->n, f->fwd.lcount, f->fwd.levels * 32, f->fwd.hub_part, f->fwd.nparts, nullptr);
+      LG_CUDA(cudaGetLastError());
+      f->flow_armed = true;
+    }
+    int rc = launch_flow(f->fwd, f->bwd, r, f->tmp, nullptr, zx, skip, s);
     if (rc) return rc;
-    return launch_flow(f->bwd, f->n, f->tmp, f->omap ? f->zp : z, f->omap ? z : nullptr, skip, s);
+    return launch_flow(f->bwd, f->fwd, f->tmp, zx, f->omap ? z : nullptr, f->tmp, skip, s);
   }
+  f->flow_armed = false;
   int rc = launch_sweep(fa, s);
   if (rc) return rc;
   return launch_sweep(ba, s);

@@ -45,6 +45,13 @@ for name in [x for x in sys.argv[1:] if not x.startswith("--")] or ["C3"]:
         print(f"   all tasks: ready->done median {np.median(c)/1e3:.2f} p90 {np.percentile(c,90)/1e3:.2f} us")
         big = np.argsort(-step)[:6]
         print("   slowest level steps (L, us):", [(int(i + 1), round(float(step[i]) / 1e3, 2)) for i in big])
+        if "--gaps" in sys.argv:
+            W = int(sys.argv[sys.argv.index("--gaps") + 1])
+            gap = st[W:] - dn[:-W]   # start of a warp's next task - done of this one
+            for l in range(min(nl, 8)):
+                m = (lvl[:-W] == l)
+                print(f"     L{l}: done-start med {np.median(dn[:-W][m]-st[:-W][m])/1e3:.2f} us, "
+                      f"gap to warp's next task med {np.median(gap[m])/1e3:.2f} p90 {np.percentile(gap[m],90)/1e3:.2f} us")
         if "--levels" in sys.argv:
             for l in range(nl):
                 m = lvl == l

@@ -267,6 +267,40 @@ def test_ic0_configs(L, cfg):
     del Lm
 
 
+@pytest.mark.parametrize("mc", [False, True])
+def test_ic0_dataflow_state_handoff(L, mc):
+    """The dataflow sweeps re-arm each other's scratch state (x sentinels,
+    counters, hub slots): repeated applies, skipped applies, in-place applies
+    and an interleaved level-barrier apply (the trace path) must all give the
+    same bits."""
+    import ctypes
+    import torch
+    from paper_1311_1695_b200 import _device as dev, _native as nat
+    a = L.build_laplacian(L.config_graph("C2"))
+    f = L.ic0_factorize_multicolor(a) if mc else L.ic0_factorize(a)
+    d = f.device()
+    rng = np.random.default_rng(3)
+    xs = [torch.from_numpy(rng.standard_normal(a.n)).cuda() for _ in range(3)]
+    want = [f.apply(x.cpu().numpy()) for x in xs]
+    ref = [d.apply(x, dev.empty(a.n)).clone() for x in xs]
+    for w, r in zip(want, ref):
+        assert np.max(np.abs(r.cpu().numpy() - w)) <= 1e-12 * np.max(np.abs(w))
+    skip = torch.ones(1, dtype=torch.int32, device="cuda")
+    z = torch.full((a.n,), 7.0, dtype=torch.float64, device="cuda")
+    d.apply_raw(xs[0].data_ptr(), z.data_ptr(), skip.data_ptr(), dev.stream_ptr())
+    assert torch.all(z == 7.0)                      # skipped: untouched
+    assert torch.equal(d.apply(xs[1], dev.empty(a.n)), ref[1])
+    lib = nat.load()
+    lib.lg_ic0_trace(d.handle, 1, None, 0)          # level-barrier path
+    assert torch.equal(d.apply(xs[2], dev.empty(a.n)), ref[2])
+    lib.lg_ic0_trace(d.handle, 0, None, 0)          # back to the dataflow path
+    assert torch.equal(d.apply(xs[0], dev.empty(a.n)), ref[0])
+    y = xs[1].clone()
+    d.apply(y, y)                                   # z aliases r
+    assert torch.equal(y, ref[1])
+    assert torch.equal(d.apply(xs[2], dev.empty(a.n)), ref[2])
+
+
 def test_jacobi_variant(L):
     a = L.build_laplacian(L.config_graph("C1"))
     jf = L.JacobiFactor(a)
