@@ -108,6 +108,25 @@ def to_host(x):
     return np.asarray(x, dtype=np.float64)
 
 
+def columns_to_host(rows, n):
+    """Device rows (a list of 1-D tensors or a 2-D (m, n) tensor) as the
+    host matrix np.column_stack(rows) -- transposed on the device, one copy."""
+    t = torch()
+    if isinstance(rows, (list, tuple)):
+        if not rows:
+            return np.zeros((n, 0))
+        rows = t.stack(list(rows))
+    if rows.shape[0] == 0:
+        return np.zeros((n, 0))
+    m = rows.t().contiguous()
+    # a pinned (already mapped, cached by torch's host allocator) result
+    # buffer: the copy runs at PCIe speed instead of page-faulting a fresh
+    # pageable array; the numpy array keeps the buffer alive
+    out = t.empty(m.shape, dtype=m.dtype, pin_memory=True)
+    out.copy_(m)
+    return out.numpy()
+
+
 def ptr(x):
     return x.data_ptr() if x is not None else None
 

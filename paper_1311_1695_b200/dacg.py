@@ -39,6 +39,7 @@ import numpy as np
 
 from . import _device as dev
 from ._plan import Fused, Graph, PrecApply, Prog, Slots, Spmv
+from ._rng import NormalStream
 from .ic0 import ic0_factorize
 from .pcg import kernel_basis, project_device
 from .precond import device_preconditioner
@@ -157,7 +158,7 @@ _SCALARS = ("q", "res", "gg", "num", "gz", "denom", "beta", "since", "period", "
             "qn", "qold", "zero", "one", "half", "two", "tol", "sqtol", "eps14", "t0", "t1",
             "t2", "t3", "t4", "t5", "t6", "sx", "sp", "cp", "spt", "a11", "a22", "a12",
             "r1a", "r1b", "r2a", "r2b", "h1", "h2", "cb", "cpp", "nr", "xapb", "paxb",
-            "iters", "xnorm2", "th", "rf2")
+            "iters", "xnorm2", "th", "rf2", "ran", "delta", "conv")
 
 
 class _DacgPlan:
@@ -170,7 +171,7 @@ class _DacgPlan:
         S = self.S = Slots(capacity=256 + 4 * (kcap + 2))
         for nm in _SCALARS:
             S.add(nm)
-        for nm in ("stop", "par", "degen", "rqinc"):
+        for nm in ("stop", "par", "degen", "rqinc", "halt"):
             S.add_flag(nm)
         S.add("cz", kcap + 1)
         S.add("cpv", kcap + 1)
@@ -189,7 +190,7 @@ class _DacgPlan:
     def _progs(self):
         S = self.S
         # PR beta with reset and clamp (dacg.py:188-195); denom <- g.z
-        p = Prog(S)
+        p = Prog(S, skip="halt")
         p.ge("reset", "since", "period")
         p.divz("beta", "num", "denom")
         p.const("zero", 0.0)
@@ -197,9 +198,10 @@ class _DacgPlan:
         p.sel("beta", "reset", "zero")
         p.sel("since", "reset", "zero")
         p.mov("denom", "gz")
+        p.inc("ran")
         self.p_beta = p.build()
         # parallel test (dacg.py:48-52) -> par, stop
-        p = Prog(S)
+        p = Prog(S, skip="halt")
         p.const("zero", 0.0)
         p.const("tol", _PARALLEL_TOL)
         p.eq("t0", "pp", "zero")
@@ -211,9 +213,10 @@ class _DacgPlan:
         p.emit("OR", p._s("t6"), p._s("t0"), p._s("t5"))
         p.flag("par", "t6")
         p.flag("stop", "t6")
+        p.flagor("halt", "t6")
         self.p_par = p.build()
         # plane pencil from Gram dots (mirror of _plane_from_gram)
-        p = Prog(S, skip="stop")
+        p = Prog(S, skip="halt")
         p.const("zero", 0.0)
         p.const("half", 0.5)
         p.const("one", 1.0)
@@ -233,6 +236,7 @@ class _DacgPlan:
         p.emit("OR", p._s("t0"), p._s("t0"), p._s("t3"))
         p.flag("degen", "t0")
         p.flagor("stop", "t0")
+        p.flagor("halt", "t0")
         p.haltif("t0")
         p.div("a11", "xax", "xx")
         p.div("t1", "xap", "sx")
@@ -290,7 +294,7 @@ class _DacgPlan:
         p.div("be", "be", "t1")
         self.p_plane = p.build()
         # q' = x'.ax' / x'.x' and the RQ-increase guard (dacg.py:221-225)
-        p = Prog(S, skip="stop")
+        p = Prog(S, skip="halt")
         p.const("one", 1.0)
         p.const("eps14", 1e-14)
         p.div("qn", "na", "nn")
@@ -301,18 +305,32 @@ class _DacgPlan:
         p.gt("t2", "qn", "t1")
         p.flag("rqinc", "t2")
         p.flagor("stop", "t2")
+        p.flagor("halt", "t2")
         p.haltif("t2")
         p.mov("qold", "q")
         p.mov("q", "qn")
         self.p_norm = p.build()
-        # residual + counters
-        p = Prog(S, skip="stop")
+        # residual + counters; a convergence candidate (the host's test
+        # res / q <= delta, same operations) halts the rest of the batch
+        p = Prog(S, skip="halt")
         p.const("half", 0.5)
+        p.const("zero", 0.0)
         p.sqrt("t1", "gg")
         p.mul("res", "half", "t1")
         p.inc("since")
         p.inc("iters")
+        p.div("t2", "res", "q")
+        p.le("t3", "t2", "delta")
+        p.gt("t4", "q", "zero")
+        p.emit("AND", p._s("conv"), p._s("t3"), p._s("t4"))
+        p.flagor("halt", "conv")
         self.p_end = p.build()
+        # batch start: clear the halt flag and the executed-iteration count
+        p = Prog(S)
+        p.const("zero", 0.0)
+        p.flag("halt", "zero")
+        p.mov("ran", "zero")
+        self.p_clear = p.build()
 
     def plan(self, b):
         """Launch list of one iteration for parity b (x in X[b])."""
@@ -324,25 +342,25 @@ class _DacgPlan:
         X, AX, G = self.X, self.AX, self.G
         Z0, Z, P, T, AP, XN, AXN, D = (self.Z0, self.Z, self.P, self.T, self.AP, self.XN,
                                        self.AXN, self.D)
-        stop = S.fp("stop")
+        stop = S.fp("halt")   # every launch of an iteration skips once a batch halted
         res = lambda nm: S.s[S.idx[nm]:]  # noqa: E731
         L = []
-        L.append(PrecApply(self.prec, G[c], Z0))
-        L.append(Fused(n, blocks=[(C, k, Z0)], result=res("cz")))
+        L.append(PrecApply(self.prec, G[c], Z0, skip=stop))
+        L.append(Fused(n, blocks=[(C, k, Z0)], result=res("cz"), skip=stop))
         # z = z0 - C cz; num = (g - g_prev).z; gz = g.z   (g_prev lives in G[o])
         L.append(Fused(n, outs=[dict(out=Z, terms=[(Z0, 1.0)], upd=(C, k, S.p("cz")))],
-                       dots=[(G[c], 1, G[o]), (G[c], 1)], result=res("num")))
+                       dots=[(G[c], 1, G[o]), (G[c], 1)], result=res("num"), skip=stop))
         L.append(self.p_beta)
         # p1 = -z + beta p; C^T p1
         L.append(Fused(n, outs=[dict(out=T, terms=[(Z, -1.0), (P, 1.0, S.p("beta"))])],
-                       blocks=[(C, k, 1)], result=res("cpv")))
+                       blocks=[(C, k, 1)], result=res("cpv"), skip=stop))
         # p2 = p1 - C cpv; xp = x.p2
         L.append(Fused(n, outs=[dict(out=D, terms=[(T, 1.0)], upd=(C, k, S.p("cpv")))],
-                       dots=[(X[c], 1)], result=res("xp")))
+                       dots=[(X[c], 1)], result=res("xp"), skip=stop))
         # p = p2 - xp x; Gram dots
         L.append(Fused(n, outs=[dict(out=P, terms=[(D, 1.0), (X[c], -1.0, S.p("xp"))])],
                        dots=[(X[c], None), (1, None), (X[c], 1), (X[c], AX[c]), (1, AX[c])],
-                       result=res("xx")))
+                       result=res("xx"), skip=stop))
         L.append(self.p_par)
         L.append(Spmv(self.csr, P, AP, dots=[P, X[c]], result=res("pap"), skip=stop))
         L.append(self.p_plane)
@@ -384,6 +402,9 @@ def dacg_smallest(a, neig, delta=1e-6, f=None, null_basis=None,
         return _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0)
 
 
+_BATCH = 8   # iterations launched per host synchronisation
+
+
 def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
     t0 = time.perf_counter()
     if counter is None:
@@ -399,6 +420,7 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
         raise ValueError(f"asked for {neig} pairs but only {usable} exist "
                          "outside the kernel")
     rng = np.random.default_rng(seed)
+    draws = NormalStream(rng, a.n)
     reset_period = max(1, a.n // 10)
     n = a.n
     kcap = null_basis.k + neig
@@ -406,6 +428,7 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
         raise ValueError("more than 64 deflation columns")
     pl = _device_plan(a, f, n, kcap)
     S, C = pl.S, pl.C
+    S.set(delta=delta)
     k = null_basis.k
     if k:
         C[:k] = null_basis.device()
@@ -422,7 +445,7 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
         if pair_idx == 0 and x0 is not None:
             start = np.asarray(dev.to_host(x0), dtype=np.float64).copy()
         else:
-            start = rng.standard_normal(n)
+            start = draws.draw()
         xs = dev.to_device(start)
         # x = guard.project_out(x); x /= |x|; ax = A x; q = x.ax; g = 2(ax - q x)
         project_device(C, k, xs, out=pl.D, slots=S) if k else pl.D.copy_(xs)
@@ -468,16 +491,29 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
                 theta = float(s[ix["th"]])
                 res_fresh = float(np.sqrt(s[ix["rf2"]]))
                 if theta > 0 and res_fresh / theta <= delta:
-                    accepted = (theta, dev.to_host(xc), res_fresh / theta, xc)
+                    accepted = (theta, None, res_fresh / theta, xc)
                     break
                 # continue from the refreshed iterate (dacg.py:184-186)
                 X[b].copy_(xc)
                 AX[b].copy_(w)
                 S.set(q=theta)
                 Fused(n, outs=[dict(out=G[b], terms=[(w, 2.0), (xc, -2.0, S.p("th"))])])()
-            L = pl.plan(b)
-            pl.graph(b)()
+            # a batch of iterations back to back on the device: every launch
+            # of an iteration skips once an earlier one halted (convergence
+            # candidate, collapsed direction, degenerate plane, RQ increase),
+            # so the host synchronises once per batch instead of per iteration
+            nb = min(_BATCH, maxit_per_pair - iterations)
+            pl.p_clear()
+            for j in range(nb):
+                pl.graph(b ^ (j & 1))()
             s, fl = S.fetch()
+            ran = int(s[ix["ran"]])
+            if ran < 1:
+                raise SolverError(f"pair {pair_idx}: device batch did not run")
+            counter.increment(ran - 1)
+            iterations += ran - 1
+            b ^= (ran - 1) & 1          # parity of the last iteration that ran
+            L = pl.plan(b)
             if fl[S.fidx["par"]]:
                 # collapsed direction: steepest descent, then random (dacg.py:199-212)
                 retries = 0
@@ -486,7 +522,7 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
                     if retries == 1:
                         src, sign = pl.Z, -1.0
                     elif retries <= 3:
-                        src, sign = dev.to_device(rng.standard_normal(n)), 1.0
+                        src, sign = dev.to_device(draws.draw()), 1.0
                     else:
                         raise SolverError(
                             f"pair {pair_idx}: no usable search direction at "
@@ -497,6 +533,7 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
                     else:
                         pl.D.copy_(pl.T)
                     Fused(n, dots=[(X[b], pl.D)], result=res("xp"))()
+                    pl.p_clear()
                     L[6]()   # p = p2 - (x.p2) x and the Gram dots
                     L[7]()   # parallel test (rewrites par / stop)
                     s, fl = S.fetch()
@@ -515,8 +552,7 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
             iterations += 1
             b = 1 - b
         if accepted is None:
-            partial = EigenPairSet(np.asarray(vals),
-                                   np.column_stack(vecs) if vecs else np.zeros((n, 0)),
+            partial = EigenPairSet(np.asarray(vals), dev.columns_to_host(vecs, n),
                                    np.asarray(resids))
             err = SolverError(
                 f"pair {pair_idx}: iteration cap {maxit_per_pair} reached "
@@ -524,16 +560,16 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
             err.partial = partial
             err.stalled_pair = pair_idx
             raise err
-        theta, u, rres, xc = accepted
+        theta, _, rres, xc = accepted
         vals.append(theta)
-        vecs.append(u)
         resids.append(rres)
         per_pair.append(iterations)
         C[k].copy_(xc)
+        vecs.append(C[k])   # accepted vectors stay on the device until the end
         k += 1
 
     order = np.argsort(vals, kind="stable")
-    pairs = EigenPairSet(np.asarray(vals)[order], np.column_stack(vecs)[:, order],
+    pairs = EigenPairSet(np.asarray(vals)[order], dev.columns_to_host([vecs[i] for i in order], n),
                          np.asarray(resids)[order])
     report = SolverReport(
         solver="dacg", neig=neig, delta=delta, mvp=counter.count, outer_its=0,

@@ -22,6 +22,7 @@ import numpy as np
 
 from . import _device as dev
 from ._plan import Fused, Slots, Spmv
+from ._rng import NormalStream
 from .ic0 import ic0_factorize
 from .kernels import DeviceGS, GramSchmidtBreakdown, dense_sym_eig
 from .pcg import DevicePcg, kernel_basis
@@ -209,6 +210,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
         raise ValueError("need 0 < m_min < m_max")
     rng = np.random.default_rng(seed)
     n = a.n
+    draws = NormalStream(rng, n)
     csr = device_csr(a)
     prec = device_preconditioner(f, n)
     kg = null_basis.k
@@ -231,7 +233,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
     wfix = dev.empty(n)
     tmpv = dev.empty((m_max + 1, n))
     tmpw = dev.empty((m_max + 1, n))
-    cand = dev.to_device(v0 if v0 is not None else rng.standard_normal(n))
+    cand = dev.to_device(v0 if v0 is not None else draws.draw())
 
     class _Space:  # view of B[kg:kg+m] / W as a workspace for _ritz
         pass
@@ -262,7 +264,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
             try:
                 gs.run(cand, [(B, kg + m)], B[kg + m])
             except GramSchmidtBreakdown:
-                cand = dev.to_device(rng.standard_normal(n))
+                cand = dev.to_device(draws.draw())
                 try:
                     gs.run(cand, [(B, kg + m)], B[kg + m])
                 except GramSchmidtBreakdown as exc:
@@ -305,7 +307,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
             res_fix = float(np.sqrt(S.fetch()[0][S.idx["vf"] + 1]))
             if res_fix < delta * theta_fix:
                 locked_vals.append(theta_fix)
-                locked_vecs.append(dev.to_host(ufix))
+                locked_vecs.append(kg)   # row of B holding the locked vector
                 locked_res.append(res_fix / theta_fix)
                 # carry the other Ritz directions (jd.py:197-205)
                 if m > 1:
@@ -319,7 +321,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
                     W[:m] = tmpw[:m]
                 H = np.diag(hvals[1:])
                 best_res, since_best, outer_here = np.inf, 0, 0
-                cand = dev.to_device(rng.standard_normal(n))
+                cand = dev.to_device(draws.draw())
                 continue
         if saturated:
             raise SolverError(
@@ -362,7 +364,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
 
     order = np.argsort(locked_vals, kind="stable")
     vals = np.asarray(locked_vals)[order]
-    vecs = np.column_stack(locked_vecs)[:, order]
+    vecs = dev.columns_to_host(B[[locked_vecs[i] for i in order]], n)
     resids = np.asarray(locked_res)[order]
     pairs = EigenPairSet(vals, vecs, resids)
     report = SolverReport(

@@ -213,6 +213,7 @@ def pcg_solve(op, precond, b, tol, maxit, deflation=None, counter=None, callback
 
 
 # ------------------------------------------------------------ DevicePcg --
+_PCG_BATCH = 8
 class DevicePcg:
     """Deflated PCG with every step on the device.
 
@@ -247,6 +248,7 @@ class DevicePcg:
         self.Y, self.AP, self.T, self.Z1 = e(n), e(n), e(n), e(n)
         self._progs()
         self._sig = None
+        self._hint = 4
 
     def _progs(self):
         S = self.S
@@ -411,12 +413,19 @@ class DevicePcg:
         s, flags = S.fetch()
         if not flags[S.fidx["stop"]]:
             while its < maxit:
-                self.body_graph()
+                # several iterations per host synchronisation: every body
+                # launch skips once "stop" is set, and "its" counts only the
+                # iterations that ran; the batch follows the previous solve's
+                # iteration count (consecutive correction solves are alike)
+                nb = max(1, min(_PCG_BATCH, maxit - its, max(2, self._hint - its)))
+                for _ in range(nb):
+                    self.body_graph()
                 s, flags = S.fetch()
                 its = int(s[S.idx["its"]])
                 relres = float(s[S.idx["relres"]])
                 if flags[S.fidx["stop"]]:
                     break
+            self._hint = its
         if flags[S.fidx["zero"]]:
             X.zero_()
             return X, 0, 0.0, True, False
