@@ -182,7 +182,7 @@ __device__ __forceinline__ double finish_row(const SpmvArgs& a, int64_t r, doubl
 }
 
 template <int NA, bool PACKED>
-__global__ void __launch_bounds__(kST, (NA == 0 ? LG_SPMV_MINB : 1))
+__global__ void __launch_bounds__(kST, (NA <= 4 ? LG_SPMV_MINB : (NA <= 16 ? 8 : 2)))
 spmv_kernel(SpmvArgs a, lg_ws ws) {
   if (a.skip && *a.skip) return;
   __shared__ double sm[kChunk];
@@ -730,6 +730,35 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
   int na = ndots + nq;
   const bool pk = a->packed != 0;
   if (na == 0) return launch<0>(args, ws, s, pk);
+  static const bool fused_epilogue = [] {
+    const char* e = getenv("LG_SPMV_EPILOGUE");
+    return e && atoi(e) == 1;
+  }();
+  if (!fused_epilogue) {
+    // The gather loop is latency-bound and wants every register for
+    // occupancy: the dot / Q^T y epilogue costs less as one streaming pass
+    // over y right behind the SpMV (measured on C4: +4-9 us instead of
+    // +18-60 us inside the kernel).  Same result layout: dots, then Q^T y.
+    int rc = launch<0>(args, ws, s, pk);
+    if (rc) return rc;
+    lg_fused_args f{};
+    f.n = a->n;
+    f.ndots = ndots;
+    for (int d = 0; d < ndots; ++d) {
+      f.da[d] = y;
+      f.db[d] = (dvec && dvec[d]) ? dvec[d] : nullptr;
+    }
+    if (nq) {
+      f.nblocks = 1;
+      f.b[0].q = q;
+      f.b[0].ld = ldq;
+      f.b[0].k = nq;
+      f.b[0].v = y;
+    }
+    f.result = out;
+    f.skip = skip;
+    return lg_fused(&f, ws, stream);
+  }
   if (na <= 4) return launch<4>(args, ws, s, pk);
   if (na <= 16) return launch<16>(args, ws, s, pk);
   return launch<LG_MAXD + LG_MAXQ>(args, ws, s, pk);

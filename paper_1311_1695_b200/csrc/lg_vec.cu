@@ -35,69 +35,127 @@ struct FusedDev {
   const int* skip;
 };
 
-__device__ __forceinline__ double pick(const double* p, int64_t i,
-                                       const double (&o)[LG_MAXO]) {
-  const uintptr_t u = (uintptr_t)p;
-  if (u == 1) return o[0];
-  if (u == 2) return o[1];
-  if (u == 3) return o[2];
-  // Non-coherent load: an element is read and then written only by its own
-  // thread, and never re-read after the write, so in-place passes stay
-  // correct while the compiler may hoist loads of later grid-stride steps
-  // above earlier stores (several elements in flight per thread).
-  return __ldg(p + i);
+// Elements per thread per tile.  A warp owns a tile of 32*kU consecutive
+// elements and lane l handles tile elements l, l+32, ...: every load
+// instruction is one coalesced 256-byte warp access, and each thread keeps
+// kU independent loads per operand in flight (memory-level parallelism is
+// what a streaming pass over HBM needs; one element per thread leaves the
+// pass latency-bound at ~1-3 TB/s).
+constexpr int kU = 4;
+
+template <int U>
+__device__ __forceinline__ void load_u(const double* p, int64_t i0, int64_t n, double (&v)[U]) {
+  // Non-coherent loads: an element is read and then written only by its
+  // own thread and never re-read after the write, so in-place passes stay
+  // correct.
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = i0 + 32 * u;
+    v[u] = i < n ? __ldg(p + i) : 0.0;
+  }
 }
 
-__device__ __forceinline__ double output_value(const lg_output& o,
-                                               const double* coef,
-                                               const double* uc, const double* uc2, int64_t i,
-                                               const double (&ov)[LG_MAXO],
-                                               double post, int pmode) {
-  double v = 0.0;
+// operand u-values: an input vector or an output of this pass
+template <int U>
+__device__ __forceinline__ void operand(const double* p, int64_t i0, int64_t n,
+                                        const double (&ov)[LG_MAXO][U], double (&v)[U]) {
+  const uintptr_t k = (uintptr_t)p;
+  // constant indices only: a runtime index would move ov to local memory
+  if (k == 1) {
 #pragma unroll
-  for (int t = 0; t < LG_MAXT; ++t)
-    if (t < o.nterms) v += coef[t] * pick(o.t[t].v, i, ov);
-  if (o.uk > 0 || o.uk2 > 0) {
-    double s = 0.0;
-    const double* q = o.uq + i;
-    for (int j = 0; j < o.uk; ++j) s += uc[j] * __ldg(q + (int64_t)j * o.uld);
-    const double* q2 = o.uq2 + i;
-    for (int j = 0; j < o.uk2; ++j) s += uc2[j] * __ldg(q2 + (int64_t)j * o.uld2);
-    v -= s;
+    for (int u = 0; u < U; ++u) v[u] = ov[0][u];
+  } else if (k == 2) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ov[1][u];
+  } else if (k == 3) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ov[2][u];
+  } else {
+    load_u<U>(p, i0, n, v);
   }
-  if (pmode == 1) v *= post;
-  else if (pmode == 2) v /= post;
-  return v;
+}
+
+template <int U>
+__device__ __forceinline__ void output_u(const lg_output& o, const double* coef,
+                                         const double* uc, const double* uc2, int64_t i0,
+                                         int64_t n, const double (&ov)[LG_MAXO][U], double post,
+                                         int pmode, double (&v)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = 0.0;
+#pragma unroll
+  for (int t = 0; t < LG_MAXT; ++t) {
+    if (t < o.nterms) {
+      double x[U];
+      operand<U>(o.t[t].v, i0, n, ov, x);
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] += coef[t] * x[u];
+    }
+  }
+  if (o.uk > 0 || o.uk2 > 0) {
+    double sq[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) sq[u] = 0.0;
+    for (int j = 0; j < o.uk; ++j) {
+      double x[U];
+      load_u<U>(o.uq + (int64_t)j * o.uld, i0, n, x);
+#pragma unroll
+      for (int u = 0; u < U; ++u) sq[u] += uc[j] * x[u];
+    }
+    for (int j = 0; j < o.uk2; ++j) {
+      double x[U];
+      load_u<U>(o.uq2 + (int64_t)j * o.uld2, i0, n, x);
+#pragma unroll
+      for (int u = 0; u < U; ++u) sq[u] += uc2[j] * x[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] -= sq[u];
+  }
+  if (pmode == 1) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] *= post;
+  } else if (pmode == 2) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] /= post;
+  }
 }
 
 template <int NA>
-__global__ void __launch_bounds__(kThreads, (NA <= 16 ? 4 : 1))
+__global__ void __launch_bounds__(kThreads, (NA <= 8 ? 3 : (NA <= 16 ? 2 : 1)))
 fused_kernel(FusedDev a, lg_ws ws) {
   if (a.skip && *a.skip) return;
   constexpr int M = NA > 0 ? NA : 1;
   __shared__ double uc_sm[LG_MAXO][LG_MAXQ];
   __shared__ double uc2_sm[LG_MAXO][LG_MAXQ];
   __shared__ double red_sm[kWarps * M];
-  double coef[LG_MAXO][LG_MAXT];
-  double post[LG_MAXO] = {1.0, 1.0, 1.0};
-  int pmode[LG_MAXO] = {0, 0, 0};
+  // per-pass coefficients in shared memory (uniform broadcast reads keep
+  // the registers for the kU-element tiles)
+  __shared__ double coef[LG_MAXO][LG_MAXT];
+  __shared__ double post[LG_MAXO];
+  __shared__ int pmode[LG_MAXO];
+  if (threadIdx.x < LG_MAXO * LG_MAXT) {
+    const int k = threadIdx.x / LG_MAXT, t = threadIdx.x % LG_MAXT;
+    const lg_output& o = a.o[k];
+    double c = 0.0;
+    if (t < o.nterms) {
+      c = o.t[t].h;
+      if (o.t[t].d) c *= *o.t[t].d;
+    }
+    coef[k][t] = c;
+    if (t == 0) {
+      double p = 1.0;
+      int m = 0;
+      if (o.post_mode) {
+        p = *o.d_post;
+        if (o.post_mode == 3) p = sqrt(p);
+        m = (o.post_mode == 1) ? 1 : 2;
+      }
+      post[k] = p;
+      pmode[k] = m;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < LG_MAXO; ++k) {
     const lg_output& o = a.o[k];
-#pragma unroll
-    for (int t = 0; t < LG_MAXT; ++t) {
-      double c = 0.0;
-      if (t < o.nterms) {
-        c = o.t[t].h;
-        if (o.t[t].d) c *= *o.t[t].d;
-      }
-      coef[k][t] = c;
-    }
-    if (o.post_mode) {
-      double p = *o.d_post;
-      post[k] = (o.post_mode == 3) ? sqrt(p) : p;
-      pmode[k] = (o.post_mode == 1) ? 1 : 2;
-    }
     for (int j = threadIdx.x; j < o.uk; j += blockDim.x)
       uc_sm[k][j] = o.cscale * o.uc[j];
     for (int j = threadIdx.x; j < o.uk2; j += blockDim.x)
@@ -111,34 +169,57 @@ fused_kernel(FusedDev a, lg_ws ws) {
   const int nd = a.ndots;
   const int k0 = a.nblocks > 0 ? a.b[0].k : 0;
   const int k1 = a.nblocks > 1 ? a.b[1].k : 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = a.n;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t tile = 32 * kU;
+  const int64_t wstride = (((int64_t)gridDim.x * blockDim.x) >> 5) * tile;
 
-#pragma unroll 2
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
-       i += stride) {
-    double ov[LG_MAXO] = {0.0, 0.0, 0.0};
+  for (int64_t i0 = gw * tile + lane; i0 - lane < n; i0 += wstride) {
+    double ov[LG_MAXO][kU];
 #pragma unroll
     for (int k = 0; k < LG_MAXO; ++k) {
       if (a.o[k].out) {
-        ov[k] = output_value(a.o[k], coef[k], uc_sm[k], uc2_sm[k], i, ov, post[k], pmode[k]);
-        a.o[k].out[i] = ov[k];
+        output_u<kU>(a.o[k], coef[k], uc_sm[k], uc2_sm[k], i0, n, ov, post[k], pmode[k], ov[k]);
+        double* out = a.o[k].out;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (i0 + 32 * u < n) out[i0 + 32 * u] = ov[k][u];
       }
     }
     if constexpr (NA > 0) {
-      double bv0 = 0.0, bv1 = 0.0;
-      if (k0) bv0 = pick(a.b[0].v, i, ov);
-      if (k1) bv1 = pick(a.b[1].v, i, ov);
+      double bv0[kU], bv1[kU];
+      if (k0) operand<kU>(a.b[0].v, i0, n, ov, bv0);
+      if (k1) operand<kU>(a.b[1].v, i0, n, ov, bv1);
 #pragma unroll
       for (int s = 0; s < NA; ++s) {
         if (s < nd) {
-          double x = pick(a.da[s], i, ov);
-          if (a.dc[s]) x -= pick(a.dc[s], i, ov);
-          double y = a.db[s] ? pick(a.db[s], i, ov) : x;
-          acc[s] += x * y;
+          double x[kU], y[kU];
+          operand<kU>(a.da[s], i0, n, ov, x);
+          if (a.dc[s]) {
+            double c[kU];
+            operand<kU>(a.dc[s], i0, n, ov, c);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) x[u] -= c[u];
+          }
+          if (a.db[s]) {
+            operand<kU>(a.db[s], i0, n, ov, y);
+          } else {
+#pragma unroll
+            for (int u = 0; u < kU; ++u) y[u] = x[u];
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) acc[s] += x[u] * y[u];
         } else if (s < nd + k0) {
-          acc[s] += bv0 * __ldg(a.b[0].q + i + (int64_t)(s - nd) * a.b[0].ld);
+          double q[kU];
+          load_u<kU>(a.b[0].q + (int64_t)(s - nd) * a.b[0].ld, i0, n, q);
+#pragma unroll
+          for (int u = 0; u < kU; ++u) acc[s] += bv0[u] * q[u];
         } else if (s < nd + k0 + k1) {
-          acc[s] += bv1 * __ldg(a.b[1].q + i + (int64_t)(s - nd - k0) * a.b[1].ld);
+          double q[kU];
+          load_u<kU>(a.b[1].q + (int64_t)(s - nd - k0) * a.b[1].ld, i0, n, q);
+#pragma unroll
+          for (int u = 0; u < kU; ++u) acc[s] += bv1[u] * q[u];
         }
       }
     }
@@ -148,7 +229,18 @@ fused_kernel(FusedDev a, lg_ws ws) {
 
 template <int NA>
 static int launch_fused(const FusedDev& a, lg_ws* ws, cudaStream_t s) {
-  int g = vec_grid(a.n);
+  // one resident wave at most (the grid-stride tiles cover the rest)
+  static int cap = 0;
+  if (!cap) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<NA>, kThreads, 0) !=
+            cudaSuccess ||
+        occ < 1)
+      occ = 1;
+    cap = std::min(occ * dev_info().sm_count, kMaxRedBlocks);
+  }
+  const int64_t want = (a.n + (int64_t)kThreads * kU - 1) / ((int64_t)kThreads * kU);
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
   fused_kernel<NA><<<g, kThreads, 0, s>>>(a, *ws);
   LG_LAUNCH_CHECK("fused_kernel");
   return LG_OK;

@@ -16,28 +16,32 @@ for lab, f in (("ic0", L.ic0_factorize(a)), ("mc", L.ic0_factorize_multicolor(a)
         pl.X[0].copy_(x / x.norm()); pl.X[1].copy_(pl.X[0])
         Spmv(pl.csr, pl.X[0], pl.AX[0])(); pl.AX[1].copy_(pl.AX[0])
         pl.G[0].copy_(pl.AX[0]); pl.G[1].copy_(pl.AX[0]); pl.P.zero_()
-        pl.S.set(since=10, period=100, q=1.0)
+        pl.S.set(since=10, period=100, q=1.0, delta=-1.0)   # never a convergence halt
         g = pl.graph(0)
-        for _ in range(3): g()
+        for _ in range(3):
+            pl.p_clear(); g()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(st)
-        for _ in range(200): g()
+        for _ in range(200):
+            pl.p_clear(); g()
         e1.record(st); torch.cuda.synchronize()
         gpu = e0.elapsed_time(e1) / 200 * 1e3
         t0 = time.perf_counter()
         for _ in range(200):
-            g(); pl.S.fetch()
+            pl.p_clear(); g(); pl.S.fetch()
         host = (time.perf_counter() - t0) / 200 * 1e6
         # eager (no graph) for comparison
         L_ = pl.plan(0)
         t0 = time.perf_counter()
         for _ in range(200):
+            pl.p_clear()
             for fn in L_: fn()
             pl.S.fetch()
         eager = (time.perf_counter() - t0) / 200 * 1e6
         # per-launch GPU time
         parts = []
+        pl.p_clear()
         for i, fn in enumerate(L_):
             e0.record(st)
             for _ in range(50): fn()

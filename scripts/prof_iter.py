@@ -17,10 +17,14 @@ with dev.solver_stream() as st:
     pl.X[0].copy_(x / x.norm()); pl.X[1].copy_(pl.X[0])
     Spmv(pl.csr, pl.X[0], pl.AX[0])(); pl.AX[1].copy_(pl.AX[0])
     pl.G[0].copy_(pl.AX[0]); pl.G[1].copy_(pl.AX[0]); pl.P.zero_()
-    pl.S.set(since=10, period=100, q=1.0)
+    pl.S.set(since=10, period=100, q=1.0, delta=-1.0)
+    pl.p_clear()
     steps = pl.plan(0)
     for _ in range(3):
+        pl.p_clear()
         for fn in steps: fn()
+    torch.cuda.synchronize()
+    pl.p_clear()
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
     for fn in steps: fn()
