@@ -247,6 +247,12 @@ typedef struct {
  * block combination Q c, optionally rescaled by a device scalar, plus
  * deterministic dot products / Q^T v block dots of inputs and outputs. */
 int lg_fused(const lg_fused_args* args, lg_ws* ws, void* stream);
+/* lg_fused followed, in the pass's finishing CTA, by a device scalar program
+ * (lg_scalar_prog semantics) over slots / flags: the program sees this
+ * pass's dot products and costs no launch of its own.  The pass must
+ * compute at least one dot product; the pass's skip flag covers both. */
+int lg_fused_prog(const lg_fused_args* args, double* slots, int* flags, const uint8_t* prog,
+                  int nops, const double* imm, int nimm, lg_ws* ws, void* stream);
 
 /* Out[:, 0:p] = In[:, 0:m] * Y  (Y is m x p column-major, host, copied by
  * value into the launch; m <= 64, p <= 32; In/Out column-major ld = n). */

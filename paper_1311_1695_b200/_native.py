@@ -13,6 +13,7 @@ device is visible, every hot-path call raises.
 """
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -109,6 +110,7 @@ _SIGS = {
     "lg_ic0_schedule": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_diag_apply": (c_int, [c_i64, c_p, c_p, c_p, c_p, c_p]),
     "lg_fused": (c_int, [c_p, c_p, c_p]),
+    "lg_fused_prog": (c_int, [c_p, c_p, c_p, c_p, c_int, c_p, c_int, c_p, c_p]),
     "lg_gemm_small": (c_int, [c_i64, c_p, c_i64, c_int, c_p, c_int, c_p, c_i64, c_p]),
     "lg_scalar_prog": (c_int, [c_p, c_p, c_p, c_int, c_p, c_int, c_p, c_p]),
 }
@@ -130,8 +132,13 @@ def load():
                 raise RuntimeError(
                     f"{LIB_PATH} is missing: build it with "
                     "`python -m paper_1311_1695_b200.build` (there is no CPU fallback)")
-            lib = ctypes.CDLL(str(LIB_PATH))
+            # LG_LIB_OVERRIDE: an alternative build of the same library
+            # (A/B timing of kernel variants in one process tree; dev only)
+            path = os.environ.get("LG_LIB_OVERRIDE") or str(LIB_PATH)
+            lib = ctypes.CDLL(path)
             for name, (res, args) in _SIGS.items():
+                if os.environ.get("LG_LIB_OVERRIDE") and not hasattr(lib, name):
+                    continue
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -192,7 +192,7 @@ class Fused:
     Q is a (kcap, n) tensor (column-major n x kcap) or (address, ld) tuple.
     """
 
-    def __init__(self, n, outs=(), dots=(), blocks=(), result=None, skip=None):
+    def __init__(self, n, outs=(), dots=(), blocks=(), result=None, skip=None, prog=None):
         a = nat.FusedArgs()
         a.n = n
         self._keep = []
@@ -246,6 +246,16 @@ class Fused:
         self.args = a
         self.argp = ctypes.byref(a)
         self.nres = len(dots) + sum(int(b[1]) for b in blocks)
+        # a scalar program run by the pass's finishing CTA (its own skip flag
+        # must be the pass's: one predicate covers both)
+        self.prog = None
+        if prog is not None:
+            if not dots and not blocks:
+                raise ValueError("a folded program needs a pass with dot products")
+            pskip = prog.S.fp(prog.skip) if prog.skip else None
+            if pskip != skip:
+                raise ValueError("folded program and pass must share the skip flag")
+            self.prog = prog.build()
 
     @staticmethod
     def _qaddr(q):
@@ -269,9 +279,13 @@ class Fused:
 
     def __call__(self, ws=None, stream=None):
         ws = ws or dev.workspace()
-        nat.check(nat.load().lg_fused(self.argp, ws.handle,
-                                      stream if stream is not None else dev.stream_ptr()),
-                  "lg_fused")
+        st = stream if stream is not None else dev.stream_ptr()
+        if self.prog is None:
+            nat.check(nat.load().lg_fused(self.argp, ws.handle, st), "lg_fused")
+            return
+        b = self.prog._built
+        nat.check(nat.load().lg_fused_prog(self.argp, b[0], b[1], b[2], b[3], b[4], b[5],
+                                           ws.handle, st), "lg_fused_prog")
 
 
 class Spmv:

@@ -102,7 +102,7 @@ inline int vec_grid(int64_t n) {
 // adds extra[e * stride_extra + d] for e < nextra (per-long-row slots of the
 // SpMV) -- also in fixed order.  Returns true in the finishing CTA.
 template <int NA>
-__device__ __forceinline__ void grid_reduce(double (&acc)[NA], int na,
+__device__ __forceinline__ bool grid_reduce(double (&acc)[NA], int na,
                                             lg_ws ws, double* result,
                                             double* smem,
                                             const double* extra = nullptr,
@@ -125,7 +125,7 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NA], int na,
       // a one-element partial list summed lane-strided + butterfly equals s
       result[threadIdx.x] = s + 0.0;
     }
-    return;
+    return true;
   }
   if ((int)threadIdx.x < na) {
     double s = 0.0;
@@ -133,20 +133,34 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NA], int na,
     ws.partial[(int64_t)blockIdx.x * kMaxRedVals + threadIdx.x] = s;
   }
   __shared__ int am_last;
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned t = atomicAdd(ws.ticket, 1u);
+    // one acq_rel ticket instead of fence + atomic + fence: the release
+    // publishes this CTA's partials (ordered before it by the barrier), the
+    // acquire in the last CTA makes every partial visible to it
+    unsigned t;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(ws.ticket) : "memory");
     am_last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!am_last) return;
-  __threadfence();
+  if (!am_last) return false;
   const int nb = gridDim.x;
   for (int d = warp; d < na; d += nw) {
+    // lane-strided partials, summed in increasing CTA order; the loads of
+    // a batch are issued together (a dependent load-add chain would cost
+    // one L2 round trip per 32 CTAs)
     double s = 0.0;
-    for (int b = lane; b < nb; b += 32)
-      s += ld_cg(ws.partial + (int64_t)b * kMaxRedVals + d);
+    for (int b0 = lane; b0 < nb; b0 += 32 * 16) {
+      double v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int b = b0 + 32 * j;
+        v[j] = b < nb ? ld_cg(ws.partial + (int64_t)b * kMaxRedVals + d) : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (b0 + 32 * j < nb) s += v[j];
+    }
     s = warp_sum(s);
     if (extra) {
       // long-row contributions, fixed order, lanes strided then tree
@@ -158,6 +172,7 @@ __device__ __forceinline__ void grid_reduce(double (&acc)[NA], int na,
     if (lane == 0) result[d] = s;
   }
   if (threadIdx.x == 0) *ws.ticket = 0u;
+  return true;
 }
 
 }  // namespace lg

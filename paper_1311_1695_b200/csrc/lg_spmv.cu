@@ -317,7 +317,15 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
         const int64_t first = a.long_first[lr];
         const int np = a.long_nparts[lr];
         double t = 0.0;
-        for (int p = tid; p < np; p += 32) t += ld_cg(a.long_part + first + p);
+        for (int p0 = tid; p0 < np; p0 += 32 * 8) {
+          double v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            v[j] = p0 + 32 * j < np ? ld_cg(a.long_part + first + p0 + 32 * j) : 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (p0 + 32 * j < np) t += v[j];
+        }
         t = warp_sum(t);
         if (tid == 0) {
           const int64_t r = blk.row0;

@@ -18,7 +18,7 @@
 #include <algorithm>
 #include <cstring>
 
-#include "lg_common.cuh"
+#include "lg_scalar.cuh"
 
 namespace lg {
 
@@ -119,9 +119,16 @@ __device__ __forceinline__ void output_u(const lg_output& o, const double* coef,
   }
 }
 
-template <int NA>
+// optional scalar program run by the pass's finishing CTA
+struct ProgDev {
+  ScalarProg p;
+  double* sg;
+  int* fg;
+};
+
+template <int NA, bool PROG>
 __global__ void __launch_bounds__(kThreads, (NA <= 8 ? 3 : (NA <= 16 ? 2 : 1)))
-fused_kernel(FusedDev a, lg_ws ws) {
+fused_kernel(FusedDev a, lg_ws ws, const __grid_constant__ ProgDev pd) {
   if (a.skip && *a.skip) return;
   constexpr int M = NA > 0 ? NA : 1;
   __shared__ double uc_sm[LG_MAXO][LG_MAXQ];
@@ -224,24 +231,30 @@ fused_kernel(FusedDev a, lg_ws ws) {
       }
     }
   }
-  if constexpr (NA > 0) grid_reduce<NA>(acc, nd + k0 + k1, ws, a.result, red_sm);
+  if constexpr (NA > 0) {
+    const bool fin = grid_reduce<NA>(acc, nd + k0 + k1, ws, a.result, red_sm);
+    if constexpr (PROG) {
+      if (fin) cta_run_program(pd.p, pd.sg, pd.fg);
+    }
+  }
 }
 
-template <int NA>
-static int launch_fused(const FusedDev& a, lg_ws* ws, cudaStream_t s) {
+template <int NA, bool PROG>
+static int launch_fused(const FusedDev& a, lg_ws* ws, cudaStream_t s, const ProgDev* pd) {
   // one resident wave at most (the grid-stride tiles cover the rest)
   static int cap = 0;
   if (!cap) {
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<NA>, kThreads, 0) !=
-            cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fused_kernel<NA, PROG>, kThreads,
+                                                      0) != cudaSuccess ||
         occ < 1)
       occ = 1;
     cap = std::min(occ * dev_info().sm_count, kMaxRedBlocks);
   }
   const int64_t want = (a.n + (int64_t)kThreads * kU - 1) / ((int64_t)kThreads * kU);
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
-  fused_kernel<NA><<<g, kThreads, 0, s>>>(a, *ws);
+  static thread_local ProgDev none{};
+  fused_kernel<NA, PROG><<<g, kThreads, 0, s>>>(a, *ws, pd ? *pd : none);
   LG_LAUNCH_CHECK("fused_kernel");
   return LG_OK;
 }
@@ -296,7 +309,8 @@ using namespace lg;
 
 extern "C" {
 
-int lg_fused(const lg_fused_args* args, lg_ws* ws, void* stream) {
+static int fused_dispatch(const lg_fused_args* args, lg_ws* ws, void* stream,
+                          const ProgDev* pd) {
   if (!args) return fail(LG_EINVAL, "lg_fused: NULL args");
   const lg_fused_args& a = *args;
   if (a.n < 0) return fail(LG_EINVAL, "lg_fused: negative n");
@@ -332,7 +346,7 @@ int lg_fused(const lg_fused_args* args, lg_ws* ws, void* stream) {
     if (!a.da[d]) return fail(LG_EINVAL, "lg_fused: NULL dot operand");
   int na = a.ndots + nq;
   if (na > 0 && (!a.result || !ws)) return fail(LG_EINVAL, "lg_fused: dots need result and ws");
-  if (a.n == 0) {
+  if (a.n == 0 && !pd) {
     if (na > 0) LG_CUDA(cudaMemsetAsync(a.result, 0, sizeof(double) * na, (cudaStream_t)stream));
     return LG_OK;
   }
@@ -354,12 +368,37 @@ int lg_fused(const lg_fused_args* args, lg_ws* ws, void* stream) {
   lg_ws dummy{};
   lg_ws* w = ws ? ws : &dummy;
   cudaStream_t s = (cudaStream_t)stream;
-  if (na == 0) return launch_fused<0>(d, w, s);
-  if (na <= 4) return launch_fused<4>(d, w, s);
-  if (na <= 8) return launch_fused<8>(d, w, s);
-  if (na <= 16) return launch_fused<16>(d, w, s);
-  if (na <= 32) return launch_fused<32>(d, w, s);
-  return launch_fused<LG_MAXD + LG_MAXQ>(d, w, s);
+  if (pd) {
+    if (na == 0) return fail(LG_EINVAL, "lg_fused_prog: the pass needs dot products");
+    if (na <= 4) return launch_fused<4, true>(d, w, s, pd);
+    if (na <= 8) return launch_fused<8, true>(d, w, s, pd);
+    if (na <= 16) return launch_fused<16, true>(d, w, s, pd);
+    return launch_fused<LG_MAXD + LG_MAXQ, true>(d, w, s, pd);
+  }
+  if (na == 0) return launch_fused<0, false>(d, w, s, nullptr);
+  if (na <= 4) return launch_fused<4, false>(d, w, s, nullptr);
+  if (na <= 8) return launch_fused<8, false>(d, w, s, nullptr);
+  if (na <= 16) return launch_fused<16, false>(d, w, s, nullptr);
+  if (na <= 32) return launch_fused<32, false>(d, w, s, nullptr);
+  return launch_fused<LG_MAXD + LG_MAXQ, false>(d, w, s, nullptr);
+}
+
+int lg_fused(const lg_fused_args* args, lg_ws* ws, void* stream) {
+  return fused_dispatch(args, ws, stream, nullptr);
+}
+
+int lg_fused_prog(const lg_fused_args* args, double* slots, int* flags, const uint8_t* prog_h,
+                  int nops, const double* imm_h, int nimm, lg_ws* ws, void* stream) {
+  if (!slots || !flags || nops < 0 || nops > LG_MAXOPS || nimm < 0 || nimm > LG_MAXIMM ||
+      (nops > 0 && !prog_h) || (nimm > 0 && !imm_h))
+    return fail(LG_EINVAL, "lg_fused_prog: bad program");
+  static thread_local ProgDev pd;
+  pd.p.nops = nops;
+  std::memcpy(pd.p.ops, prog_h, 4 * (size_t)nops);
+  if (nimm) std::memcpy(pd.p.imm, imm_h, sizeof(double) * (size_t)nimm);
+  pd.sg = slots;
+  pd.fg = flags;
+  return fused_dispatch(args, ws, stream, &pd);
 }
 
 int lg_gemm_small(int64_t n, const double* in, int64_t ldi, int m,

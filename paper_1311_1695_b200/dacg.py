@@ -345,36 +345,37 @@ class _DacgPlan:
         stop = S.fp("halt")   # every launch of an iteration skips once a batch halted
         res = lambda nm: S.s[S.idx[nm]:]  # noqa: E731
         L = []
+        # scalar programs run in the finishing CTA of the pass whose dots
+        # they consume (lg_fused_prog): no launch of their own
         L.append(PrecApply(self.prec, G[c], Z0, skip=stop))
         L.append(Fused(n, blocks=[(C, k, Z0)], result=res("cz"), skip=stop))
         # z = z0 - C cz; num = (g - g_prev).z; gz = g.z   (g_prev lives in G[o])
         L.append(Fused(n, outs=[dict(out=Z, terms=[(Z0, 1.0)], upd=(C, k, S.p("cz")))],
-                       dots=[(G[c], 1, G[o]), (G[c], 1)], result=res("num"), skip=stop))
-        L.append(self.p_beta)
+                       dots=[(G[c], 1, G[o]), (G[c], 1)], result=res("num"), skip=stop,
+                       prog=self.p_beta))
         # p1 = -z + beta p; C^T p1
         L.append(Fused(n, outs=[dict(out=T, terms=[(Z, -1.0), (P, 1.0, S.p("beta"))])],
                        blocks=[(C, k, 1)], result=res("cpv"), skip=stop))
         # p2 = p1 - C cpv; xp = x.p2
         L.append(Fused(n, outs=[dict(out=D, terms=[(T, 1.0)], upd=(C, k, S.p("cpv")))],
                        dots=[(X[c], 1)], result=res("xp"), skip=stop))
-        # p = p2 - xp x; Gram dots
+        # p = p2 - xp x; Gram dots; parallel test
         L.append(Fused(n, outs=[dict(out=P, terms=[(D, 1.0), (X[c], -1.0, S.p("xp"))])],
                        dots=[(X[c], None), (1, None), (X[c], 1), (X[c], AX[c]), (1, AX[c])],
-                       result=res("xx"), skip=stop))
-        L.append(self.p_par)
-        L.append(Spmv(self.csr, P, AP, dots=[P, X[c]], result=res("pap"), skip=stop))
-        L.append(self.p_plane)
+                       result=res("xx"), skip=stop, prog=self.p_par))
+        L.append(Spmv(self.csr, P, AP, skip=stop))
+        # pap = ap.p, xap = ap.x; plane pencil
+        L.append(Fused(n, dots=[(AP, P), (AP, X[c])], result=res("pap"), skip=stop,
+                       prog=self.p_plane))
         L.append(Fused(n, outs=[dict(out=XN, terms=[(X[c], 1.0, S.p("al")), (P, 1.0, S.p("be"))]),
                                 dict(out=AXN, terms=[(AX[c], 1.0, S.p("al")),
                                                      (AP, 1.0, S.p("be"))])],
-                       dots=[(1, None), (1, 2)], result=res("nn"), skip=stop))
-        L.append(self.p_norm)
+                       dots=[(1, None), (1, 2)], result=res("nn"), skip=stop, prog=self.p_norm))
         nn = S.p("nn")
         L.append(Fused(n, outs=[dict(out=X[o], terms=[(XN, 1.0)], post=(nn, 3)),
                                 dict(out=AX[o], terms=[(AXN, 1.0)], post=(nn, 3)),
                                 dict(out=G[o], terms=[(2, 2.0), (1, -2.0, S.p("q"))])],
-                       dots=[(3, None)], result=res("gg"), skip=stop))
-        L.append(self.p_end)
+                       dots=[(3, None)], result=res("gg"), skip=stop, prog=self.p_end))
         self.plans[key] = L
         return L
 
@@ -403,6 +404,7 @@ def dacg_smallest(a, neig, delta=1e-6, f=None, null_basis=None,
 
 
 _BATCH = 8   # iterations launched per host synchronisation
+_GRAM = 5    # plan index of the Gram-dot pass (with the parallel test)
 
 
 def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
@@ -534,12 +536,11 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
                         pl.D.copy_(pl.T)
                     Fused(n, dots=[(X[b], pl.D)], result=res("xp"))()
                     pl.p_clear()
-                    L[6]()   # p = p2 - (x.p2) x and the Gram dots
-                    L[7]()   # parallel test (rewrites par / stop)
+                    L[_GRAM]()   # p = p2 - (x.p2) x, Gram dots, parallel test
                     s, fl = S.fetch()
                     if not fl[S.fidx["par"]]:
                         break
-                for fn in L[8:]:
+                for fn in L[_GRAM + 1:]:
                     fn()
                 s, fl = S.fetch()
             if fl[S.fidx["degen"]]:

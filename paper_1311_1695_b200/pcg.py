@@ -348,10 +348,11 @@ class DevicePcg:
                 body.append(Fused(n, outs=[self._upd(dict(out=T, terms=[(Y, 1.0)]), "cy1")],
                                   blocks=self._qdots(1), result=self._res("cy2"), skip=stop))
                 body.append(Fused(n, outs=[self._upd(dict(out=AP, terms=[(T, 1.0)]), "cy2")],
-                                  dots=[(P, 1)], result=self._res("pap"), skip=stop))
+                                  dots=[(P, 1)], result=self._res("pap"), skip=stop,
+                                  prog=self.p_gamma))
             else:
                 body.append(Fused(n, outs=[dict(out=AP, terms=[(Y, 1.0)])], dots=[(P, 1)],
-                                  result=self._res("pap"), skip=stop))
+                                  result=self._res("pap"), skip=stop, prog=self.p_gamma))
         else:
             if len(qb) == 1:
                 body.append(Spmv(self.csr, P, Y, q=qb[0][0], nq=qb[0][1],
@@ -364,8 +365,8 @@ class DevicePcg:
             o = dict(out=AP, terms=[(Y, 1.0)])
             if has_q:
                 self._upd(o, "cy1")
-            body.append(Fused(n, outs=[o], dots=[(P, 1)], result=self._res("pap"), skip=stop))
-        body.append(self.p_gamma)
+            body.append(Fused(n, outs=[o], dots=[(P, 1)], result=self._res("pap"), skip=stop,
+                              prog=self.p_gamma))
         gam = S.p("gamma")
         if has_q:
             body.append(Fused(n, outs=[dict(out=X, terms=[(X, 1.0), (P, 1.0, gam)]),
@@ -374,15 +375,15 @@ class DevicePcg:
             # R = T - Q cr1, rr = R.R and Q^T R -> cr (rr is followed by cr)
             body.append(Fused(n, outs=[self._upd(dict(out=R, terms=[(T, 1.0)]), "cr1")],
                               dots=[(1, None)], blocks=self._qdots(1), result=self._res("rr"),
-                              skip=stop))
+                              skip=stop, prog=self.p_relres))
         else:
             body.append(Fused(n, outs=[dict(out=X, terms=[(X, 1.0), (P, 1.0, gam)]),
                                        dict(out=R, terms=[(R, 1.0), (AP, -1.0, gam)])],
-                              dots=[(2, None)], result=self._res("rr"), skip=stop))
-        body.append(self.p_relres)
+                              dots=[(2, None)], result=self._res("rr"), skip=stop,
+                              prog=self.p_relres))
         body += ps
-        body.append(Fused(n, outs=[zlast()], dots=[(R, 1)], result=self._res("rzn"), skip=stop))
-        body.append(self.p_beta)
+        body.append(Fused(n, outs=[zlast()], dots=[(R, 1)], result=self._res("rzn"), skip=stop,
+                          prog=self.p_beta))
         body.append(Fused(n, outs=[dict(out=P, terms=[(Z, 1.0), (P, 1.0, S.p("beta"))])],
                           skip=stop))
         self.body = body
