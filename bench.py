@@ -106,7 +106,8 @@ def build_graph(config):
     return config_graph(config)
 
 
-from paper_1311_1695_b200.dist import SliceGather, partition_rows  # noqa: E402
+from paper_1311_1695_b200.dist import (PaddedAllGather, RowPartition,  # noqa: E402
+                                      local_operator, partition_rows)
 
 
 def cpu_spmv_threads(rp, col, val, x, nthreads, chunks):
@@ -313,27 +314,27 @@ def main():
 
     import paper_1311_1695_b200 as L
     from paper_1311_1695_b200 import _device as dev
-    from paper_1311_1695_b200.sparse import DeviceCsr
 
     g = build_graph(args.config)
     a = L.build_laplacian(g)
     n, nnz = a.n, a.nnz
-    cuts = partition_rows(a.row_ptr, world)
+    part = RowPartition(a.row_ptr, world)
+    cuts = part.cuts
     r0, r1 = cuts[rank], cuts[rank + 1]
+    xh0 = np.random.default_rng(0).standard_normal(n)
     if world == 1:
         d = a.device()
+        x = dev.to_device(xh0)
+        y = dev.empty(n)
+        gather = None
     else:
-        lo, hi = int(a.row_ptr[r0]), int(a.row_ptr[r1])
-        # local row block as a rectangular operator: rows r0..r1, all columns
-        # (square n x n CSR with empty rows outside the block)
-        rp = np.zeros(n + 1, dtype=np.int64)
-        rp[r0 + 1:r1 + 1] = a.row_ptr[r0 + 1:r1 + 1] - lo
-        rp[r1 + 1:] = hi - lo
-        d = DeviceCsr(n, rp, a.col_idx[lo:hi], a.values[lo:hi])
-    x = dev.to_device(np.random.default_rng(0).standard_normal(n))
-    y = dev.empty(n)
-    counts = [cuts[i + 1] - cuts[i] for i in range(world)]
-    gather = SliceGather(dist, counts, rank, x) if world > 1 else None
+        # this rank's rows, columns in the padded layout where every rank's
+        # slice of an n-vector sits at rank * maxc: the exchange is one
+        # in-place NCCL all-gather into the SpMV operand (no copies)
+        d = local_operator(a, part, rank)
+        x = dev.to_device(part.pad(xh0))
+        y = dev.empty(part.npad)
+        gather = PaddedAllGather(dist, part, rank)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 

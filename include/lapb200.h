@@ -74,7 +74,11 @@ typedef struct lg_csr lg_csr;
  * reference CsrMatrix, sparse.py:39-41).  Columns are stored as int32 when
  * n < 2^31.  Builds the nnz-balanced row-block schedule and, when the
  * off-diagonal values take few distinct values, the packed value table.
- * flags: bit0 = disable packed-value format. */
+ * flags: LG_CSR_PLAIN disables the packed-value format; LG_CSR_SKIP_EMPTY
+ * leaves rows without stored entries out of the schedule (lg_spmv does not
+ * write y there): one rank's row block embedded in the global index space. */
+#define LG_CSR_PLAIN 1
+#define LG_CSR_SKIP_EMPTY 2
 int lg_csr_create(int64_t n, int64_t nnz, const int64_t* row_ptr_h,
                   const int64_t* col_h, const double* val_h, int flags,
                   lg_csr** out);

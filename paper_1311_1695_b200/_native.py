@@ -25,6 +25,8 @@ LG_ECUDA = -2
 LG_ENOMEM = -3
 LG_EBREAKDOWN = -4
 
+LG_CSR_PLAIN = 1
+LG_CSR_SKIP_EMPTY = 2
 LG_MAXT = 4
 LG_MAXD = 8
 LG_MAXB = 2

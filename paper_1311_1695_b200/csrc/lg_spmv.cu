@@ -356,12 +356,20 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
 }
 
 // Build the row-block schedule on the host (O(n)).
+// absent (optional): rows with no stored entry that are left out of the
+// schedule altogether (y is not written there) -- the row block of one rank
+// in the row-partitioned multi-GPU SpMV, embedded in the global index space.
 static void build_schedule(int64_t n, const int64_t* rp,
                            std::vector<SpmvBlock>& blocks,
                            std::vector<int32_t>& long_nparts,
-                           std::vector<int64_t>& long_first) {
+                           std::vector<int64_t>& long_first,
+                           const std::vector<char>* absent = nullptr) {
   int64_t r = 0, part_total = 0;
   while (r < n) {
+    if (absent && (*absent)[(size_t)r]) {
+      ++r;
+      continue;
+    }
     int64_t len = rp[r + 1] - rp[r];
     if (len > kChunk) {
       int32_t np = (int32_t)((len + kChunk - 1) / kChunk);
@@ -385,6 +393,7 @@ static void build_schedule(int64_t n, const int64_t* rp,
     }
     int64_t r0 = r, nz = 0;
     while (r < n && r - r0 < kRowCap) {
+      if (absent && (*absent)[(size_t)r]) break;
       int64_t l = rp[r + 1] - rp[r];
       if (l > kChunk || nz + l > kChunk) break;
       nz += l;
@@ -477,6 +486,7 @@ static bool make_packed(int64_t n, const int64_t* rp, const int64_t* col, const 
   const int vbits = 32 - cbits;
   const int64_t maxvals = std::min<int64_t>((int64_t)1 << vbits, kMaxTable);
   std::vector<uint64_t> uniq;
+  int64_t ndiag = 0;
   {
     std::vector<uint64_t> bitsv;
     bitsv.reserve(1024);
@@ -487,6 +497,7 @@ static bool make_packed(int64_t n, const int64_t* rp, const int64_t* col, const 
       for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
         if (col[k] == r) {
           has_diag = true;
+          ++ndiag;
           continue;
         }
         uint64_t bv;
@@ -501,7 +512,7 @@ static bool make_packed(int64_t n, const int64_t* rp, const int64_t* col, const 
           if ((int64_t)uniq.size() > maxvals) return false;
         }
       }
-      if (!has_diag) return false;
+      if (!has_diag && rp[r + 1] > rp[r]) return false;   // an empty row packs as 0
     }
     tmp.insert(tmp.end(), uniq.begin(), uniq.end());
     std::sort(tmp.begin(), tmp.end());
@@ -513,7 +524,7 @@ static bool make_packed(int64_t n, const int64_t* rp, const int64_t* col, const 
   for (size_t i = 0; i < uniq.size(); ++i) std::memcpy(&table[i], &uniq[i], 8);
   prp.assign((size_t)n + 1, 0);
   diag.assign((size_t)n, 0.0);
-  const int64_t noff = rp[n] - n;
+  const int64_t noff = rp[n] - ndiag;
   pcol.resize((size_t)std::max<int64_t>(noff, 0));
   int64_t o = 0;
   for (int64_t r = 0; r < n; ++r) {
@@ -541,7 +552,6 @@ extern "C" {
 
 int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
                   const double* val, int flags, lg_csr** out) {
-  (void)flags;
   if (!out) return fail(LG_EINVAL, "lg_csr_create: out is NULL");
   if (n < 0 || nnz < 0) return fail(LG_EINVAL, "lg_csr_create: negative size");
   if (n >= ((int64_t)1 << 31))
@@ -567,7 +577,13 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
   std::vector<SpmvBlock> blocks;
   std::vector<int32_t> lnp;
   std::vector<int64_t> lfirst;
-  build_schedule(n, packed ? prp.data() : rp, blocks, lnp, lfirst);
+  std::vector<char> absent;
+  if (flags & LG_CSR_SKIP_EMPTY) {
+    absent.resize((size_t)n);
+    for (int64_t r = 0; r < n; ++r) absent[(size_t)r] = rp[r + 1] == rp[r];
+  }
+  build_schedule(n, packed ? prp.data() : rp, blocks, lnp, lfirst,
+                 (flags & LG_CSR_SKIP_EMPTY) ? &absent : nullptr);
 
   lg_csr* a = new lg_csr();
   a->n = n;
