@@ -106,8 +106,9 @@ def build_graph(config):
     return config_graph(config)
 
 
-from paper_1311_1695_b200.dist import (PaddedAllGather, RowPartition,  # noqa: E402
-                                      local_operator, partition_rows)
+from paper_1311_1695_b200.dist import (RowPartition, SliceExchange,  # noqa: E402
+                                      device_row_ptr, local_operator,
+                                      local_operator_device, partition_rows)
 
 
 def cpu_spmv_threads(rp, col, val, x, nthreads, chunks):
@@ -247,11 +248,14 @@ def solve_block(a, f, f_mc=None):
     return out
 
 
-def c5_block(peaks, steps=10):
+def c5_block(peaks, steps=10, dist=None, world=1, rank=0):
     """BASELINE configs[4] (R-MAT scale 26, edge factor 16, ~2.1e9 nonzeros):
     device-side ingest (sampling, dedupe, largest component, packed
-    Laplacian) and the SpMV on it.  Not buildable by the reference (SURVEY
-    0.8); reported next to the headline, not as it."""
+    Laplacian) and the SpMV on it -- at N > 1 row-partitioned by nonzeros
+    (each rank builds the same graph, keeps its row block in the padded
+    block, every rank's slice of x exchanged in place per product with one
+    NCCL point-to-point group; time = max over ranks).  Not buildable by the reference; reported next to
+    the headline, not as it."""
     import torch
     from paper_1311_1695_b200 import _device as dev
     from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
@@ -260,27 +264,51 @@ def c5_block(peaks, steps=10):
     A = rmat_laplacian_device(26, 16, seed=0)
     torch.cuda.synchronize()
     build = time.perf_counter() - t0
-    d = A.device()
-    x = dev.to_device(np.random.default_rng(0).standard_normal(A.n))
-    y = dev.empty(A.n)
-    for _ in range(3):
+    n = A.n
+    xh = np.random.default_rng(0).standard_normal(n)
+    gather = None
+    x = dev.to_device(xh)
+    y = dev.empty(n)
+    if world > 1:
+        part = RowPartition(device_row_ptr(A.device()), world)
+        d = local_operator_device(A.device(), part, rank)
+        A._dev = None          # the full matrix is no longer needed on this rank
+        torch.cuda.empty_cache()
+        gather = SliceExchange(dist, part, rank)
+    else:
+        d = A.device()
+
+    def step():
+        if gather is not None:
+            gather(x)
         d.matvec(x, y)
+
+    for _ in range(3):
+        step()
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     e1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     for i in range(steps):
         e0[i].record()
-        d.matvec(x, y)
+        step()
         e1[i].record()
     torch.cuda.synchronize()
     ms = float(np.mean([p.elapsed_time(q) for p, q in zip(e0, e1)]))
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     out = {"workload": "C5: R-MAT scale 26 ef 16 (a,b,c)=(.57,.19,.19), LCC, unit weights, "
                        "device-built (counter-based RNG)",
-           "n": A.n, "m": A.m, "nnz": A.nnz, "build_s": build, "spmv_ms": ms,
-           "matvecs_per_s": 1e3 / ms,
-           "stream_gbs": d.stream_bytes / (ms * 1e-3) / 1e9,
-           "effective_gbs": d.algo_bytes / (ms * 1e-3) / 1e9,
-           "frac_stream_of_hbm": d.stream_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+           "n": n, "m": A.m, "nnz": A.nnz, "n_gpus": world,
+           "parallelism": f"rows{world} (nnz-balanced row blocks, in-place P2P exchange "
+                          "of x per product)" if world > 1 else "single",
+           "build_s": build, "spmv_ms": ms, "matvecs_per_s": 1e3 / ms,
+           "stream_gbs_rank0": d.stream_bytes / (ms * 1e-3) / 1e9,
+           "effective_gbs": (12 * A.nnz + 8 * (n + 1) + 16 * n) / (ms * 1e-3) / 1e9,
+           "frac_stream_of_hbm_rank0": d.stream_bytes / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
            "l2": "x (262 MB) exceeds L2; not flushed"}
     del A, d, x, y
     torch.cuda.empty_cache()
@@ -322,19 +350,16 @@ def main():
     cuts = part.cuts
     r0, r1 = cuts[rank], cuts[rank + 1]
     xh0 = np.random.default_rng(0).standard_normal(n)
+    x = dev.to_device(xh0)
+    y = dev.empty(n)
+    gather = None
     if world == 1:
         d = a.device()
-        x = dev.to_device(xh0)
-        y = dev.empty(n)
-        gather = None
     else:
-        # this rank's rows, columns in the padded layout where every rank's
-        # slice of an n-vector sits at rank * maxc: the exchange is one
-        # in-place NCCL all-gather into the SpMV operand (no copies)
+        # this rank's rows (global columns); the exchange moves every rank's
+        # slice of x to every peer in place (one NCCL P2P group per product)
         d = local_operator(a, part, rank)
-        x = dev.to_device(part.pad(xh0))
-        y = dev.empty(part.npad)
-        gather = PaddedAllGather(dist, part, rank)
+        gather = SliceExchange(dist, part, rank)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
 
@@ -437,8 +462,10 @@ def main():
         f.device()
         f_mc.device()   # device factor upload = setup, like the reference's splu
         line["solve"] = solve_block(a, f, f_mc)
-    if rank == 0 and world == 1 and not args.no_c5:
-        line["c5"] = c5_block(peaks)
+    if not args.no_c5:
+        c5 = c5_block(peaks, dist=dist, world=world, rank=rank)
+        if rank == 0:
+            line["c5"] = c5
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(g)
     if rank == 0:

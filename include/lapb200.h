@@ -76,7 +76,7 @@ typedef struct lg_csr lg_csr;
  * off-diagonal values take few distinct values, the packed value table.
  * flags: LG_CSR_PLAIN disables the packed-value format; LG_CSR_SKIP_EMPTY
  * leaves rows without stored entries out of the schedule (lg_spmv does not
- * write y there): one rank's row block embedded in the global index space. */
+ * write y there): one rank's row block of the row-partitioned SpMV. */
 #define LG_CSR_PLAIN 1
 #define LG_CSR_SKIP_EMPTY 2
 int lg_csr_create(int64_t n, int64_t nnz, const int64_t* row_ptr_h,
@@ -130,6 +130,13 @@ int lg_rmat_device(int scale, int edge_factor, double a, double b, double c,
  * renumbered in increasing order, edges compacted in place of the input). */
 int lg_lcc_device(int64_t n, int64_t m, int32_t** d_i, int32_t** d_j,
                   int64_t* n_out, int64_t* m_out);
+/* Multi-GPU row block: rows [r0, r1) of a packed matrix as a packed n x n
+ * matrix whose other rows are absent from the schedule (lg_spmv does not
+ * write y there); columns keep the global numbering, so each rank's slice of
+ * an n-vector is exchanged in place. */
+int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** out);
+/* Stream row pointers (packed: off-diagonal; plain: row_ptr), n + 1 int64. */
+int lg_csr_row_ptr(const lg_csr* a, int64_t* host_out);
 /* Unit-weight Laplacian of a canonical device edge list, built directly in
  * the packed SpMV format on the device (no host copy of the matrix). */
 int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,

@@ -979,6 +979,82 @@ extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
   return LG_OK;
 }
 
+// ---- one rank's row block (multi-GPU) --------------------------------------
+// Rows [r0, r1) of a packed matrix as a packed n x n matrix whose other rows
+// are absent from the schedule (lg_spmv leaves y there untouched): the
+// operator one rank applies to the fully exchanged x in the row-partitioned
+// SpMV.  Columns keep the global numbering, so every rank's slice of an
+// n-vector is exchanged in place (no packing, no padding).
+extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** out) {
+  if (!a || !out || r0 < 0 || r1 < r0 || r1 > a->n)
+    return fail(LG_EINVAL, "lg_csr_row_block: bad argument");
+  if (!a->packed) return fail(LG_EINVAL, "lg_csr_row_block: only for packed matrices");
+  const int64_t n = a->n, nloc = r1 - r0;
+  std::vector<int64_t> lrp((size_t)nloc + 1);
+  LG_CUDA(cudaMemcpy(lrp.data(), a->prp + r0, 8 * (size_t)(nloc + 1), cudaMemcpyDeviceToHost));
+  const int64_t off0 = lrp[0], m = lrp[(size_t)nloc] - off0;
+  std::vector<int64_t> prp((size_t)n + 1, 0);
+  for (int64_t i = 0; i < nloc; ++i) prp[(size_t)(r0 + i + 1)] = lrp[(size_t)i + 1] - off0;
+  for (int64_t r = r1 + 1; r <= n; ++r) prp[(size_t)r] = m;
+  std::vector<char> absent((size_t)n, 1);
+  for (int64_t r = r0; r < r1; ++r) absent[(size_t)r] = 0;
+  std::vector<SpmvBlock> blocks;
+  std::vector<int32_t> lnp;
+  std::vector<int64_t> lfirst;
+  build_schedule(n, prp.data(), blocks, lnp, lfirst, &absent);
+
+  lg_csr* b = new lg_csr();
+  b->n = n;
+  b->nnz = m + nloc;
+  b->packed = 1;
+  b->cbits = a->cbits;
+  b->nvals = a->nvals;
+  b->noff = m;
+  b->nblocks = (int64_t)blocks.size();
+  b->nlong = (int64_t)lnp.size();
+  for (int32_t v : lnp) b->nparts += v;
+  bool ok = cudaMalloc(&b->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
+            (m == 0 || cudaMalloc(&b->pcol, 4 * (size_t)m) == cudaSuccess) &&
+            cudaMalloc(&b->pdiag, 8 * (size_t)n) == cudaSuccess &&
+            (b->nvals == 0 || cudaMalloc(&b->table, 8 * (size_t)b->nvals) == cudaSuccess) &&
+            (b->nblocks == 0 ||
+             cudaMalloc(&b->blocks, sizeof(SpmvBlock) * (size_t)b->nblocks) == cudaSuccess) &&
+            (b->nlong == 0 || (cudaMalloc(&b->long_nparts, 4 * (size_t)b->nlong) == cudaSuccess &&
+                               cudaMalloc(&b->long_first, 8 * (size_t)b->nlong) == cudaSuccess));
+  if (!ok) {
+    lg_csr_destroy(b);
+    return fail(LG_ENOMEM, "lg_csr_row_block: allocation failed");
+  }
+  cudaMemcpy(b->prp, prp.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice);
+  cudaMemset(b->pdiag, 0, 8 * (size_t)n);
+  cudaMemcpy(b->pdiag + r0, a->pdiag + r0, 8 * (size_t)nloc, cudaMemcpyDeviceToDevice);
+  if (b->nvals) cudaMemcpy(b->table, a->table, 8 * (size_t)b->nvals, cudaMemcpyDeviceToDevice);
+  if (m) cudaMemcpy(b->pcol, a->pcol + off0, 4 * (size_t)m, cudaMemcpyDeviceToDevice);
+  if (b->nblocks)
+    cudaMemcpy(b->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
+  if (b->nlong) {
+    cudaMemcpy(b->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(b->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
+  }
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    lg_csr_destroy(b);
+    return fail(LG_ECUDA, std::string("lg_csr_row_block: ") + cudaGetErrorString(err));
+  }
+  *out = b;
+  return LG_OK;
+}
+
+// Stream row pointers of a matrix (packed: off-diagonal row pointers; plain:
+// row_ptr) to the host, n + 1 entries -- what the nnz-balanced row
+// partition of a device-only matrix is computed from.
+extern "C" int lg_csr_row_ptr(const lg_csr* a, int64_t* host_out) {
+  if (!a || !host_out) return fail(LG_EINVAL, "lg_csr_row_ptr: bad argument");
+  LG_CUDA(cudaMemcpy(host_out, a->packed ? a->prp : a->row_ptr, 8 * (size_t)(a->n + 1),
+                     cudaMemcpyDeviceToHost));
+  return LG_OK;
+}
+
 // Device diagonal (degrees) of a packed matrix, for Jacobi preconditioning
 // of device-only matrices.
 extern "C" int lg_csr_diagonal(const lg_csr* a, double* d_out) {

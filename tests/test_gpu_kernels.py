@@ -394,11 +394,11 @@ def test_device_rmat_lcc_laplacian_pipeline(L):
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_row_partitioned_spmv_padded_layout(L, world):
-    """The multi-GPU SpMV's per-rank operators (rows of one rank, columns in
-    the padded index space, other rows absent from the schedule), run one
-    after another on one device on a fully gathered padded x, reproduce the
-    single-device product bit for bit and write only their own rows."""
+def test_row_partitioned_spmv_row_blocks(L, world):
+    """The multi-GPU SpMV's per-rank operators (the rank's rows, global
+    columns, other rows absent from the schedule), run one after another on
+    one device on the exchanged x, reproduce the single-device product bit
+    for bit and write only their own rows."""
     import torch
     from paper_1311_1695_b200 import _device as dev
     from paper_1311_1695_b200.dist import RowPartition, local_operator
@@ -408,16 +408,39 @@ def test_row_partitioned_spmv_padded_layout(L, world):
     want = a.device()
     y_ref = dev.empty(a.n)
     want.matvec(x, y_ref)
-    xp = part.pad(x)
-    yp = torch.full((part.npad,), 12345.0, dtype=torch.float64, device="cuda")
+    y = torch.zeros(a.n, dtype=torch.float64, device="cuda")
     for r in range(world):
         op = local_operator(a, part, r)
         assert op.packed == want.packed
-        ys = torch.full((part.npad,), 12345.0, dtype=torch.float64, device="cuda")
-        op.matvec(xp, ys)
-        a0, a1 = part.local_rows(r)
-        untouched = torch.ones(part.npad, dtype=torch.bool, device="cuda")
-        untouched[a0:a1] = False
-        assert torch.all(ys[untouched] == 12345.0)
-        yp[a0:a1] = ys[a0:a1]
-    assert torch.equal(part.unpad(yp), y_ref)
+        ys = torch.full((a.n,), 12345.0, dtype=torch.float64, device="cuda")
+        op.matvec(x, ys)
+        r0, r1 = part.rows(r)
+        assert torch.all(ys[:r0] == 12345.0) and torch.all(ys[r1:] == 12345.0)
+        y[r0:r1] = ys[r0:r1]
+    assert torch.equal(y, y_ref)
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_row_partitioned_spmv_device_sliced(L, world):
+    """Device-side row blocks of a device-only packed Laplacian (the C5 path:
+    R-MAT sampled, LCC and assembled on the device) reproduce the full
+    product bit for bit."""
+    import torch
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.dist import RowPartition, device_row_ptr, local_operator_device
+    A = rmat_laplacian_device(13, 8, seed=3)
+    full = A.device()
+    part = RowPartition(device_row_ptr(full), world)
+    x = torch.from_numpy(np.random.default_rng(5).standard_normal(A.n)).cuda()
+    y_ref = dev.empty(A.n)
+    full.matvec(x, y_ref)
+    y = torch.zeros(A.n, dtype=torch.float64, device="cuda")
+    for r in range(world):
+        op = local_operator_device(full, part, r)
+        ys = torch.full((A.n,), -7.0, dtype=torch.float64, device="cuda")
+        op.matvec(x, ys)
+        r0, r1 = part.rows(r)
+        assert torch.all(ys[:r0] == -7.0) and torch.all(ys[r1:] == -7.0)
+        y[r0:r1] = ys[r0:r1]
+    assert torch.equal(y, y_ref)
