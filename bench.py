@@ -248,6 +248,40 @@ def solve_block(a, f, f_mc=None):
     return out
 
 
+def solve_configs_block():
+    """Wall time to k eigenpairs on the smaller BASELINE configs with the
+    reference's own solver settings (golden: neig, delta, reference IC(0)),
+    next to the reference's MVPs / eigenvalues / wall time (build container):
+    C1 DACG / JD / IRLM, C2 DACG / JD, C3 JD."""
+    import torch
+    import paper_1311_1695_b200 as L
+    runs = {"C1": ("dacg", "jd", "irlm"), "C2": ("dacg", "jd"), "C3": ("jd",)}
+    fns = {"dacg": L.dacg_smallest, "jd": L.jd_smallest, "irlm": L.irlm_smallest}
+    out = {}
+    for cfg, solvers in runs.items():
+        gold = json.loads((ROOT / "tests" / "golden" / f"config_{cfg}.json").read_text())
+        a = L.build_laplacian(L.config_graph(cfg))
+        f = L.ic0_factorize(a)
+        f.device()
+        for name in solvers:
+            walls = []
+            for _ in range(2):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                pairs, rep = fns[name](a, gold["neig"], delta=gold["delta"], f=f)
+                torch.cuda.synchronize()
+                walls.append(time.perf_counter() - t0)
+            r = gold["solvers"][name]
+            ref_vals = np.asarray(r["eigenvalues"])
+            out[f"{cfg}_{name}"] = {
+                "neig": gold["neig"], "delta": gold["delta"], "wall_s": walls[1],
+                "wall_s_first_call": walls[0], "mvp": rep.mvp, "reference_mvp": r["mvp"],
+                "eig_relerr_vs_reference": float(np.max(np.abs(pairs.values - ref_vals)
+                                                        / np.abs(ref_vals))),
+                "reference_wall_s_build_container": r["wall_seconds"]}
+    return out
+
+
 def c5_block(peaks, steps=10, dist=None, world=1, rank=0):
     """BASELINE configs[4] (R-MAT scale 26, edge factor 16, ~2.1e9 nonzeros):
     device-side ingest (sampling, dedupe, largest component, packed
@@ -462,6 +496,7 @@ def main():
         f.device()
         f_mc.device()   # device factor upload = setup, like the reference's splu
         line["solve"] = solve_block(a, f, f_mc)
+        line["solve_configs"] = solve_configs_block()
     if not args.no_c5:
         c5 = c5_block(peaks, dist=dist, world=world, rank=rank)
         if rank == 0:
