@@ -159,9 +159,10 @@ def solver_stream():
     stream of the current device, ordered after the caller's stream."""
     t = torch()
     d = t.cuda.current_device()
-    s = _solver_streams.get(d)
+    key = (d, threading.get_ident())     # one per thread (simulated ranks)
+    s = _solver_streams.get(key)
     if s is None:
-        s = _solver_streams[d] = t.cuda.Stream(device=d)
+        s = _solver_streams[key] = t.cuda.Stream(device=d)
     s.wait_stream(t.cuda.current_stream())
     return _StreamCtx(t, s)
 

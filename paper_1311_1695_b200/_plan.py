@@ -403,3 +403,142 @@ class Graph:
             self.release()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# Execution context: the whole vector on one GPU, or one rank's row slice.
+
+
+class AllReduce:
+    """Sum a slot range over the ranks (dot-product partials of a pass)."""
+
+    def __init__(self, comm, result, count):
+        self.comm = comm
+        self.result = result
+        self.count = count      # int or a callable (live count after set_k)
+
+    def __call__(self, ws=None, stream=None):
+        c = self.count() if callable(self.count) else self.count
+        if c:
+            self.comm.allreduce_(self.result[:c])
+
+
+class Exchange:
+    """Complete a full-length vector from every rank's slice, in place."""
+
+    def __init__(self, comm, x):
+        self.comm, self.x = comm, x
+
+    def __call__(self, ws=None, stream=None):
+        self.comm.exchange_(self.x)
+
+
+class Seq:
+    """Launches run in order (one plan entry of a row-partitioned solver)."""
+
+    def __init__(self, steps):
+        self.steps = [s for s in steps if s is not None]
+        self.fused = next((s for s in self.steps if isinstance(s, Fused)), None)
+
+    def set_k(self, **kw):
+        self.fused.set_k(**kw)
+
+    @property
+    def nres(self):
+        return self.fused.nres
+
+    def __call__(self, ws=None, stream=None):
+        for s in self.steps:
+            s(stream=stream)
+
+
+class Ctx:
+    """Where a solver's n-vector work runs.
+
+    comm None: every pass covers the whole vector (one GPU) and a scalar
+    program folds into the finishing CTA of the pass it reads.
+    comm given (dist.RowComm): passes cover this rank's rows [r0, r1) of the
+    same full-length buffers, their dot partials are all-reduced before the
+    program (then a launch of its own), and an SpMV first completes its input
+    from the other ranks' slices and multiplies the rank's row block.
+    """
+
+    def __init__(self, n, comm=None):
+        self.n = n
+        self.comm = comm if (comm is not None and comm.world > 1) else None
+        self.lo = self.comm.r0 if self.comm else 0
+        self.nl = self.comm.nl if self.comm else n
+
+    @property
+    def dist(self):
+        return self.comm is not None
+
+    def v(self, t):
+        """A vector operand restricted to this rank's rows."""
+        if self.comm is None or t is None or isinstance(t, int):
+            return t
+        return t[self.lo:self.lo + self.nl]
+
+    def q(self, c):
+        """A column block (k, n) restricted to this rank's rows."""
+        if self.comm is None or c is None:
+            return c
+        if isinstance(c, tuple):
+            return (c[0] + 8 * self.lo, c[1])
+        return (c.data_ptr() + 8 * self.lo, c.shape[-1])
+
+    def fused(self, outs=(), dots=(), blocks=(), result=None, skip=None, prog=None):
+        if self.comm is None:
+            return Fused(self.n, outs=outs, dots=dots, blocks=blocks, result=result,
+                         skip=skip, prog=prog)
+        o2 = []
+        for o in outs:
+            if o is None:
+                o2.append(None)
+                continue
+            d = dict(o)
+            d["out"] = self.v(o["out"])
+            d["terms"] = [(self.v(t[0]),) + tuple(t[1:]) for t in o.get("terms", ())]
+            for key in ("upd", "upd2"):
+                if o.get(key) is not None:
+                    u = o[key]
+                    d[key] = (self.q(u[0]),) + tuple(u[1:])
+            o2.append(d)
+        d2 = [tuple(self.v(x) for x in dt) for dt in dots]
+        b2 = [(self.q(b[0]), b[1], self.v(b[2])) for b in blocks]
+        f = Fused(self.nl, outs=o2, dots=d2, blocks=b2, result=result, skip=skip)
+        steps = [f]
+        if result is not None and (dots or blocks):
+            steps.append(AllReduce(self.comm, result, lambda: f.nres))
+        if prog is not None:
+            steps.append(prog.build() if prog._built is None else prog)
+        return Seq(steps)
+
+    def spmv(self, csr, x, y, theta=0.0, theta_d=None, theta_neg=False, dots=(), q=None,
+             nq=0, result=None, skip=None):
+        if self.comm is None:
+            return Spmv(csr, x, y, theta=theta, theta_d=theta_d, theta_neg=theta_neg,
+                        dots=dots, q=q, nq=nq, result=result, skip=skip)
+        steps = [Exchange(self.comm, x),
+                 Spmv(csr, x, y, theta=theta, theta_d=theta_d, theta_neg=theta_neg, skip=skip)]
+        if dots or nq:
+            steps.append(self.fused(dots=[(y, d) for d in dots],
+                                    blocks=[(q, nq, y)] if nq else (), result=result,
+                                    skip=skip))
+        return Seq(steps)
+
+    def project(self, c, k, v, out, slots, name=None):
+        """out = v - C (C^T v) over this rank's rows (two passes)."""
+        name = name or f"_pc{k}"
+        if name not in slots.idx:
+            slots.add(name, max(k, 1))
+        res = slots.s[slots.idx[name]:]
+        self.fused(blocks=[(c, k, v)], result=res)()
+        self.fused(outs=[dict(out=out, terms=[(v, 1.0)], upd=(c, k, slots.p(name)))])()
+        return out
+
+    def gather(self, x):
+        """Complete a full-length vector from the ranks' slices."""
+        if self.comm is not None:
+            self.comm.exchange_(x)
+        return x

@@ -38,7 +38,7 @@ import time
 import numpy as np
 
 from . import _device as dev
-from ._plan import Fused, Graph, PrecApply, Prog, Slots, Spmv
+from ._plan import Ctx, Fused, Graph, PrecApply, Prog, Slots, Spmv
 from ._rng import NormalStream
 from .ic0 import ic0_factorize
 from .pcg import kernel_basis, project_device
@@ -164,10 +164,15 @@ _SCALARS = ("q", "res", "gg", "num", "gz", "denom", "beta", "since", "period", "
 class _DacgPlan:
     """Prebuilt launches of one DACG iteration (two buffer parities)."""
 
-    def __init__(self, a, f, n, kcap):
+    def __init__(self, a, f, n, kcap, comm=None):
         self.n = n
-        self.csr = device_csr(a)
-        self.prec = device_preconditioner(f, n)
+        self.cx = Ctx(n, comm)
+        if self.cx.dist:
+            self.csr = self.cx.comm.local_operator(a)
+            self.prec = self.cx.comm.local_preconditioner(a, f)
+        else:
+            self.csr = device_csr(a)
+            self.prec = device_preconditioner(f, n)
         S = self.S = Slots(capacity=256 + 4 * (kcap + 2))
         for nm in _SCALARS:
             S.add(nm)
@@ -347,32 +352,33 @@ class _DacgPlan:
         L = []
         # scalar programs run in the finishing CTA of the pass whose dots
         # they consume (lg_fused_prog): no launch of their own
-        L.append(PrecApply(self.prec, G[c], Z0, skip=stop))
-        L.append(Fused(n, blocks=[(C, k, Z0)], result=res("cz"), skip=stop))
+        cx = self.cx
+        L.append(PrecApply(self.prec, cx.v(G[c]), cx.v(Z0), skip=stop))
+        L.append(cx.fused(blocks=[(C, k, Z0)], result=res("cz"), skip=stop))
         # z = z0 - C cz; num = (g - g_prev).z; gz = g.z   (g_prev lives in G[o])
-        L.append(Fused(n, outs=[dict(out=Z, terms=[(Z0, 1.0)], upd=(C, k, S.p("cz")))],
+        L.append(cx.fused(outs=[dict(out=Z, terms=[(Z0, 1.0)], upd=(C, k, S.p("cz")))],
                        dots=[(G[c], 1, G[o]), (G[c], 1)], result=res("num"), skip=stop,
                        prog=self.p_beta))
         # p1 = -z + beta p; C^T p1
-        L.append(Fused(n, outs=[dict(out=T, terms=[(Z, -1.0), (P, 1.0, S.p("beta"))])],
+        L.append(cx.fused(outs=[dict(out=T, terms=[(Z, -1.0), (P, 1.0, S.p("beta"))])],
                        blocks=[(C, k, 1)], result=res("cpv"), skip=stop))
         # p2 = p1 - C cpv; xp = x.p2
-        L.append(Fused(n, outs=[dict(out=D, terms=[(T, 1.0)], upd=(C, k, S.p("cpv")))],
+        L.append(cx.fused(outs=[dict(out=D, terms=[(T, 1.0)], upd=(C, k, S.p("cpv")))],
                        dots=[(X[c], 1)], result=res("xp"), skip=stop))
         # p = p2 - xp x; Gram dots; parallel test
-        L.append(Fused(n, outs=[dict(out=P, terms=[(D, 1.0), (X[c], -1.0, S.p("xp"))])],
+        L.append(cx.fused(outs=[dict(out=P, terms=[(D, 1.0), (X[c], -1.0, S.p("xp"))])],
                        dots=[(X[c], None), (1, None), (X[c], 1), (X[c], AX[c]), (1, AX[c])],
                        result=res("xx"), skip=stop, prog=self.p_par))
-        L.append(Spmv(self.csr, P, AP, skip=stop))
+        L.append(cx.spmv(self.csr, P, AP, skip=stop))
         # pap = ap.p, xap = ap.x; plane pencil
-        L.append(Fused(n, dots=[(AP, P), (AP, X[c])], result=res("pap"), skip=stop,
+        L.append(cx.fused(dots=[(AP, P), (AP, X[c])], result=res("pap"), skip=stop,
                        prog=self.p_plane))
-        L.append(Fused(n, outs=[dict(out=XN, terms=[(X[c], 1.0, S.p("al")), (P, 1.0, S.p("be"))]),
+        L.append(cx.fused(outs=[dict(out=XN, terms=[(X[c], 1.0, S.p("al")), (P, 1.0, S.p("be"))]),
                                 dict(out=AXN, terms=[(AX[c], 1.0, S.p("al")),
                                                      (AP, 1.0, S.p("be"))])],
                        dots=[(1, None), (1, 2)], result=res("nn"), skip=stop, prog=self.p_norm))
         nn = S.p("nn")
-        L.append(Fused(n, outs=[dict(out=X[o], terms=[(XN, 1.0)], post=(nn, 3)),
+        L.append(cx.fused(outs=[dict(out=X[o], terms=[(XN, 1.0)], post=(nn, 3)),
                                 dict(out=AX[o], terms=[(AXN, 1.0)], post=(nn, 3)),
                                 dict(out=G[o], terms=[(2, 2.0), (1, -2.0, S.p("q"))])],
                        dots=[(3, None)], result=res("gg"), skip=stop, prog=self.p_end))
@@ -384,36 +390,44 @@ class _DacgPlan:
         key = ("g", b, self.k)
         g = self.plans.get(key)
         if g is None:
-            g = self.plans[key] = Graph(self.plan(b))
+            g = Graph(self.plan(b))
+            if self.cx.dist:
+                g.eager = True   # host-issued collectives inside the iteration
+            self.plans[key] = g
         return g
 
 
-def _device_plan(a, f, n, kcap):
-    return _DacgPlan(a, f, n, kcap)
+def _device_plan(a, f, n, kcap, comm=None):
+    return _DacgPlan(a, f, n, kcap, comm)
 
 
 def dacg_smallest(a, neig, delta=1e-6, f=None, null_basis=None,
-                  maxit_per_pair=20000, *, seed=0, counter=None, x0=None):
+                  maxit_per_pair=20000, *, seed=0, counter=None, x0=None, comm=None):
     """neig smallest strictly positive eigenpairs by Rayleigh quotient
     descent (dacg.py:122-276).  Each accepted iterate is verified with a
     fresh product against ||A x - q x|| / q <= delta and joined to the
     deflation set; raises with partial results attached when a pair exceeds
-    maxit_per_pair."""
+    maxit_per_pair.
+
+    comm (extension, not in the reference): a dist.RowComm -- this process is
+    one rank of a row-partitioned solve; f is then a
+    JacobiFactor, 'jacobi' or 'block_ic0' (default: block-Jacobi IC(0)), and
+    every rank returns the same pairs."""
     with dev.solver_stream():
-        return _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0)
+        return _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0, comm)
 
 
 _BATCH = 8   # iterations launched per host synchronisation
 _GRAM = 5    # plan index of the Gram-dot pass (with the parallel test)
 
 
-def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
+def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0, comm=None):
     t0 = time.perf_counter()
     if counter is None:
         counter = MvpCounter()
     if null_basis is None:
         null_basis = kernel_basis(a.n)
-    if f is None:
+    if f is None and (comm is None or comm.world == 1):
         f = ic0_factorize(a)
     if neig < 1:
         raise ValueError("neig must be at least 1")
@@ -428,8 +442,8 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
     kcap = null_basis.k + neig
     if kcap > 64:
         raise ValueError("more than 64 deflation columns")
-    pl = _device_plan(a, f, n, kcap)
-    S, C = pl.S, pl.C
+    pl = _device_plan(a, f, n, kcap, comm)
+    S, C, cx = pl.S, pl.C, pl.cx
     S.set(delta=delta)
     k = null_basis.k
     if k:
@@ -450,15 +464,15 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
             start = draws.draw()
         xs = dev.to_device(start)
         # x = guard.project_out(x); x /= |x|; ax = A x; q = x.ax; g = 2(ax - q x)
-        project_device(C, k, xs, out=pl.D, slots=S) if k else pl.D.copy_(xs)
-        Fused(n, dots=[(pl.D, None)], result=res("xnorm2"))()
+        cx.project(C, k, xs, pl.D, S) if k else pl.D.copy_(xs)
+        cx.fused(dots=[(pl.D, None)], result=res("xnorm2"))()
         if float(S.fetch()[0][ix["xnorm2"]]) == 0.0:
             raise SolverError(f"pair {pair_idx}: start vector lies in the deflated subspace")
-        Fused(n, outs=[dict(out=X[0], terms=[(pl.D, 1.0)], post=(S.p("xnorm2"), 3))])()
-        Spmv(pl.csr, X[0], AX[0], dots=[X[0]], result=res("q"))()
+        cx.fused(outs=[dict(out=X[0], terms=[(pl.D, 1.0)], post=(S.p("xnorm2"), 3))])()
+        cx.spmv(pl.csr, X[0], AX[0], dots=[X[0]], result=res("q"))()
         counter.increment()
         setup_mvps += 1
-        Fused(n, outs=[dict(out=G[0], terms=[(AX[0], 2.0), (X[0], -2.0, S.p("q"))]),
+        cx.fused(outs=[dict(out=G[0], terms=[(AX[0], 2.0), (X[0], -2.0, S.p("q"))]),
                        dict(out=G[1], terms=[]), dict(out=pl.P, terms=[])],
               dots=[(1, None)], result=res("gg"))()
         S.set(since=reset_period, period=reset_period, iters=0, denom=0.0)
@@ -478,16 +492,16 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
                 # candidate passes on cached data; confirm with a fresh product
                 xc = pl.D
                 if k:
-                    project_device(C, k, X[b], out=xc, slots=S)
+                    cx.project(C, k, X[b], xc, S)
                 else:
                     xc.copy_(X[b])
-                Fused(n, dots=[(xc, None)], result=res("xnorm2"))()
-                Fused(n, outs=[dict(out=xc, terms=[(xc, 1.0)], post=(S.p("xnorm2"), 3))])()
+                cx.fused(dots=[(xc, None)], result=res("xnorm2"))()
+                cx.fused(outs=[dict(out=xc, terms=[(xc, 1.0)], post=(S.p("xnorm2"), 3))])()
                 w = pl.T
-                Spmv(pl.csr, xc, w, dots=[xc], result=res("th"))()
+                cx.spmv(pl.csr, xc, w, dots=[xc], result=res("th"))()
                 counter.increment()
                 verify_mvps += 1
-                Fused(n, outs=[dict(out=pl.AP, terms=[(w, 1.0), (xc, -1.0, S.p("th"))])],
+                cx.fused(outs=[dict(out=pl.AP, terms=[(w, 1.0), (xc, -1.0, S.p("th"))])],
                       dots=[(1, None)], result=res("rf2"))()
                 s, _ = S.fetch()
                 theta = float(s[ix["th"]])
@@ -499,7 +513,7 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
                 X[b].copy_(xc)
                 AX[b].copy_(w)
                 S.set(q=theta)
-                Fused(n, outs=[dict(out=G[b], terms=[(w, 2.0), (xc, -2.0, S.p("th"))])])()
+                cx.fused(outs=[dict(out=G[b], terms=[(w, 2.0), (xc, -2.0, S.p("th"))])])()
             # a batch of iterations back to back on the device: every launch
             # of an iteration skips once an earlier one halted (convergence
             # candidate, collapsed direction, degenerate plane, RQ increase),
@@ -529,12 +543,12 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
                         raise SolverError(
                             f"pair {pair_idx}: no usable search direction at "
                             f"iteration {iterations}")
-                    Fused(n, outs=[dict(out=pl.T, terms=[(src, sign)])])()
+                    cx.fused(outs=[dict(out=pl.T, terms=[(src, sign)])])()
                     if k:
-                        project_device(C, k, pl.T, out=pl.D, slots=S)
+                        cx.project(C, k, pl.T, pl.D, S)
                     else:
                         pl.D.copy_(pl.T)
-                    Fused(n, dots=[(X[b], pl.D)], result=res("xp"))()
+                    cx.fused(dots=[(X[b], pl.D)], result=res("xp"))()
                     pl.p_clear()
                     L[_GRAM]()   # p = p2 - (x.p2) x, Gram dots, parallel test
                     s, fl = S.fetch()
@@ -553,6 +567,8 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
             iterations += 1
             b = 1 - b
         if accepted is None:
+            for v in vecs:
+                cx.gather(v)
             partial = EigenPairSet(np.asarray(vals), dev.columns_to_host(vecs, n),
                                    np.asarray(resids))
             err = SolverError(
@@ -569,6 +585,8 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0):
         vecs.append(C[k])   # accepted vectors stay on the device until the end
         k += 1
 
+    for v in vecs:
+        cx.gather(v)     # row-partitioned: every rank returns whole vectors
     order = np.argsort(vals, kind="stable")
     pairs = EigenPairSet(np.asarray(vals)[order], dev.columns_to_host([vecs[i] for i in order], n),
                          np.asarray(resids)[order])

@@ -102,3 +102,199 @@ class SliceExchange:
             for req in d.batch_isend_irecv(ops):
                 req.wait()
         return x
+
+
+# ---------------------------------------------------------------------------
+# Row-partitioned solvers: the execution context of one rank.
+#
+# Every solver vector stays n long on every rank, but each rank only computes
+# its own row slice [r0, r1): fused vector passes run over the slice, their
+# dot-product partials are summed over ranks (one all-reduce per pass, before
+# the scalar program that reads them), the SpMV exchanges the slices of its
+# input in place and multiplies the rank's row block (global column
+# numbering), and the preconditioner is local (Jacobi, or block-Jacobi IC(0)
+# of the rank's diagonal block: the natural-order IC(0) sweeps do not shard).
+# Scalar programs run redundantly on every rank on identical inputs, so every
+# rank takes the same branches and launches the same collectives.
+
+
+class TorchBackend:
+    """Collectives of one rank over torch.distributed (NCCL over NVLink /
+    NVSwitch on the GPU box, gloo in CPU tests)."""
+
+    def __init__(self, dist):
+        self.dist = dist
+
+    def allreduce_(self, t, comm):
+        self.dist.all_reduce(t)
+
+    def exchange_(self, x, comm):
+        SliceExchange(self.dist, comm.part, comm.rank)(x)
+
+    def barrier(self, comm):
+        self.dist.barrier()
+
+
+class ThreadWorld:
+    """Ranks simulated by threads of one process on one GPU (tests only):
+    each rank runs on its own stream; all-reduce sums the ranks' tensors in
+    rank order (deterministic, identical on every rank) and the exchange
+    copies peer slices in place.  Kernels never wait on each other across
+    ranks -- ranks meet only at host barriers."""
+
+    def __init__(self, world):
+        import threading
+        self.world = int(world)
+        self.bar = threading.Barrier(self.world)
+        self.buf = [None] * self.world
+
+    def _sync(self):
+        import torch
+        torch.cuda.current_stream().synchronize()
+
+    def allreduce_(self, t, comm):
+        self._sync()
+        self.buf[comm.rank] = t
+        self.bar.wait()
+        acc = self.buf[0].clone()
+        for p in range(1, self.world):
+            acc += self.buf[p]
+        self._sync()
+        self.bar.wait()
+        t.copy_(acc)
+
+    def exchange_(self, x, comm):
+        self._sync()
+        self.buf[comm.rank] = x
+        self.bar.wait()
+        for p in range(self.world):
+            if p != comm.rank:
+                q0, q1 = comm.part.rows(p)
+                x[q0:q1].copy_(self.buf[p][q0:q1])
+        self._sync()
+        self.bar.wait()
+
+    def barrier(self, comm):
+        self._sync()
+        self.bar.wait()
+
+
+class RowComm:
+    """One rank of a row-partitioned solve: its partition, rank and
+    collective backend.  Pass it to dacg_smallest(..., comm=...).
+
+        comm = RowComm.from_torch(a, torch.distributed)        # NCCL / gloo
+    """
+
+    def __init__(self, part, rank, backend):
+        self.part = part
+        self.rank = int(rank)
+        self.world = part.world
+        self.r0, self.r1 = part.rows(self.rank)
+        self.backend = backend
+
+    @classmethod
+    def from_torch(cls, a, dist):
+        return cls(RowPartition(matrix_row_ptr(a), dist.get_world_size()), dist.get_rank(),
+                   TorchBackend(dist))
+
+    @property
+    def nl(self):
+        return self.r1 - self.r0
+
+    def allreduce_(self, t):
+        if self.world > 1:
+            self.backend.allreduce_(t, self)
+
+    def exchange_(self, x):
+        if self.world > 1:
+            self.backend.exchange_(x, self)
+
+    def barrier(self):
+        if self.world > 1:
+            self.backend.barrier(self)
+
+    def local_operator(self, a):
+        """This rank's row block of `a` (host CsrMatrix or device-only)."""
+        if hasattr(a, "row_ptr") and getattr(a, "col_idx", None) is not None:
+            return local_operator(a, self.part, self.rank)
+        return local_operator_device(a.device(), self.part, self.rank)
+
+    def local_preconditioner(self, a, f):
+        """The rank-local preconditioner for the solver seam `f`:
+        JacobiFactor -> its slice; None / 'block_ic0' -> block-Jacobi IC(0)
+        of the diagonal block (Jacobi for device-only matrices); 'jacobi'."""
+        from .precond import JacobiFactor
+        host = hasattr(a, "row_ptr") and getattr(a, "col_idx", None) is not None
+        if f is None:
+            f = "block_ic0" if host else "jacobi"
+        if isinstance(f, str):
+            if f == "jacobi":
+                f = JacobiFactor(a)
+            elif f == "block_ic0":
+                if not host:
+                    raise ValueError("block-Jacobi IC(0) needs the matrix on the host")
+                return BlockJacobiIc0(a, self)
+            else:
+                raise ValueError(f"unknown distributed preconditioner {f!r}")
+        if isinstance(f, JacobiFactor):
+            return LocalJacobi(f, self.r0, self.r1)
+        if isinstance(f, BlockJacobiIc0):
+            return f
+        raise ValueError("row-partitioned solves take a JacobiFactor, 'jacobi' or "
+                         "'block_ic0' as preconditioner (the natural-order IC(0) sweeps "
+                         "do not shard, SURVEY 8(e))")
+
+
+def matrix_row_ptr(a):
+    """Row pointers to balance on: host CSR arrays, or the device matrix's."""
+    if hasattr(a, "row_ptr") and getattr(a, "col_idx", None) is not None:
+        return np.asarray(a.row_ptr)
+    return device_row_ptr(a.device())
+
+
+class LocalJacobi:
+    """A rank's slice of a JacobiFactor: z = r / diag on rows [r0, r1),
+    applied to slice pointers."""
+
+    def __init__(self, f, r0, r1):
+        self.f = f
+        self.n = r1 - r0
+        self._dinv = f._dinv[r0:r1]
+
+    def apply_raw(self, r, z, skip, stream):
+        from . import _native as nat
+        nat.check(nat.load().lg_diag_apply(self.n, self._dinv.data_ptr(), r, z, skip, stream),
+                  "lg_diag_apply")
+
+
+class BlockJacobiIc0:
+    """Block-Jacobi IC(0) (flagged, non-reference): the
+    reference's IC(0) (same shift ladder, bit-exact host factorization) of
+    the rank's diagonal block A[r0:r1, r0:r1], applied by the device sweeps
+    to the rank's slice -- no communication in the apply."""
+
+    def __init__(self, a, comm):
+        from .ic0 import ic0_factorize
+        from .sparse import CsrMatrix
+        r0, r1 = comm.r0, comm.r1
+        rp = np.asarray(a.row_ptr)
+        ci = np.asarray(a.col_idx)
+        va = np.asarray(a.values)
+        lo, hi = int(rp[r0]), int(rp[r1])
+        rows = np.repeat(np.arange(r1 - r0), np.diff(rp[r0:r1 + 1]))
+        keep = (ci[lo:hi] >= r0) & (ci[lo:hi] < r1)
+        cols = ci[lo:hi][keep] - r0
+        vals = va[lo:hi][keep]
+        rr = rows[keep]
+        brp = np.zeros(r1 - r0 + 1, dtype=np.int64)
+        np.add.at(brp, rr + 1, 1)
+        brp = np.cumsum(brp)
+        self.block = CsrMatrix(r1 - r0, brp, cols, vals, symmetric=True)
+        self.factor = ic0_factorize(self.block)
+        self.n = r1 - r0
+        self.shift = self.factor.shift
+        self.attempts = self.factor.attempts
+
+    def apply_raw(self, r, z, skip, stream):
+        self.factor.device().apply_raw(r, z, skip, stream)

@@ -1,5 +1,7 @@
 """C4 SpMV / IC(0) launches for ncu (development aid)."""
+import os
 import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from paper_1311_1695_b200 import _device as dev

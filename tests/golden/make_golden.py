@@ -150,12 +150,15 @@ CONFIG_RUNS = {
     "C2": dict(neig=10, delta=1e-10, solvers=("dacg", "jd")),
     "C3": dict(neig=5, delta=1e-10, solvers=("jd",)),
     "C4": dict(neig=5, delta=1e-8, solvers=("jd", "dacg")),
+    # the full BASELINE neig for C3 (20, JD) and C4 (10, DACG + JD)
+    "C3n20": dict(neig=20, delta=1e-10, solvers=("jd",)),
+    "C4n10": dict(neig=10, delta=1e-8, solvers=("dacg", "jd")),
 }
 
 
 def make_config(name):
     from paper_1311_1695_b200.generators import config_graph  # new generators
-    g = config_graph(name)
+    g = config_graph(name[:2])
     # feed the reference the very same canonical edge list
     rg = EdgeList(g.n_nodes, g.i, g.j, g.w)
     t0 = time.perf_counter()

@@ -117,3 +117,87 @@ def test_row_partition_uneven_world3():
     assert all(p.exitcode == 0 for p in procs)
     for rank, ok_y, ok_bal, ok_dot in res:
         assert ok_y and ok_bal and ok_dot, (rank, ok_y, ok_bal, ok_dot)
+
+
+def _comm_worker(rank, world, port, q):
+    """RowComm over gloo: the collectives a row-partitioned solver issues
+    (slot all-reduce, in-place slice exchange) and the plan context's slice
+    views, on CPU tensors."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200.dist import RowComm
+    from paper_1311_1695_b200.generators import chung_lu_graph
+    from paper_1311_1695_b200.sparse import CsrMatrix
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = chung_lu_graph(3000, 2.1, 5.0, max_degree=300, seed=7)
+        rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+        a = CsrMatrix(g.n_nodes, rp, col, val)
+        comm = RowComm.from_torch(a, dist)
+        n = a.n
+        x_full = np.random.default_rng(1).standard_normal(n)
+        # slot all-reduce of per-rank dot partials = the global dot
+        part = torch.tensor([x_full[comm.r0:comm.r1] @ x_full[comm.r0:comm.r1], 1.0])
+        comm.allreduce_(part)
+        ok_red = (abs(float(part[0]) - x_full @ x_full) <= 1e-12 * (x_full @ x_full)
+                  and float(part[1]) == world)
+        # exchange completes a vector whose other slices hold garbage
+        x = torch.full((n,), np.nan, dtype=torch.float64)
+        x[comm.r0:comm.r1] = torch.from_numpy(x_full[comm.r0:comm.r1])
+        comm.exchange_(x)
+        ok_x = np.array_equal(x.numpy(), x_full)
+        q.put((rank, ok_red, ok_x, comm.r0, comm.r1))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_comm_collectives_gloo(world):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    res = sorted(q.get(timeout=5) for _ in procs)
+    assert all(p.exitcode == 0 for p in procs)
+    assert [r[3] for r in res][0] == 0 and all(res[i][4] == res[i + 1][3] for i in range(world - 1))
+    for rank, ok_red, ok_x, _, _ in res:
+        assert ok_red and ok_x, (rank, ok_red, ok_x)
+
+
+def test_block_jacobi_ic0_block_and_factor():
+    """The block-Jacobi IC(0) of a rank is the reference IC(0) of the dense
+    diagonal block A[r0:r1, r0:r1] (host factorization, no GPU needed)."""
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200.dist import BlockJacobiIc0, RowComm, RowPartition
+    from paper_1311_1695_b200.generators import chung_lu_graph
+    from paper_1311_1695_b200.graphs import largest_component
+    from paper_1311_1695_b200.sparse import CsrMatrix
+    g, _ = largest_component(chung_lu_graph(800, 2.1, 5.0, max_degree=100, seed=3))
+    rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+    a = CsrMatrix(g.n_nodes, rp, col, val)
+    dense = np.zeros((a.n, a.n))
+    for r in range(a.n):
+        dense[r, col[rp[r]:rp[r + 1]]] = val[rp[r]:rp[r + 1]]
+    part = RowPartition(rp, 3)
+    for rank in range(3):
+        comm = RowComm(part, rank, backend=None)
+        bj = BlockJacobiIc0(a, comm)
+        r0, r1 = comm.r0, comm.r1
+        blk = np.zeros((r1 - r0, r1 - r0))
+        b = bj.block
+        for r in range(b.n):
+            blk[r, b.col_idx[b.row_ptr[r]:b.row_ptr[r + 1]]] = b.values[b.row_ptr[r]:b.row_ptr[r + 1]]
+        assert np.array_equal(blk, dense[r0:r1, r0:r1])
+        lrp, lcol, lval, shift, att = O.ic0_factorize(O.Csr(b.n, b.row_ptr, b.col_idx, b.values),
+                                                     use_c=False)
+        assert np.array_equal(bj.factor.l.values.view(np.int64), lval.view(np.int64))
