@@ -294,6 +294,53 @@ def solve_configs_block(prebuilt=None):
     return out
 
 
+def solve_dist_block(a, dist=None, world=1, rank=0, neig=10, delta=1e-8):
+    """Row-partitioned DACG on C4 at the BASELINE's neig 10, delta 1e-8
+    (SURVEY 8(e)): every rank owns a row block and its slice of every solver
+    vector; one all-reduce per dot pass, one in-place slice exchange per
+    SpMV.  Preconditioner: block-Jacobi IC(0) of each rank's diagonal block
+    (the reference IC(0) itself at N = 1; the natural-order sweeps do not
+    shard).  Time to solution = max over ranks (factorization excluded, as in
+    the reference harness bench.py:123-125)."""
+    import torch
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200.dist import BlockJacobiIc0, RowComm, RowPartition, TorchBackend
+    part = RowPartition(a.row_ptr, world)
+    comm = RowComm(part, rank, TorchBackend(dist) if dist else None)
+    f = BlockJacobiIc0(a, comm) if world > 1 else L.ic0_factorize(a)
+    if world > 1:
+        f.factor.device()
+    else:
+        f.device()
+    walls = []
+    for _ in range(2):   # first call and steady state
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        pairs, rep = L.dacg_smallest(a, neig, delta=delta, f=f, comm=comm)
+        torch.cuda.synchronize()
+        w = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([w], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            w = float(t.item())
+        walls.append(w)
+    out = {"solver": "dacg", "neig": neig, "delta": delta, "n_gpus": world,
+           "wall_s": walls[1], "wall_s_first_call": walls[0], "mvp": rep.mvp,
+           "preconditioner": "block-Jacobi ic0 (flagged)" if world > 1 else "ic0 (reference)",
+           "parallelism": f"rows{world}" if world > 1 else "single"}
+    try:
+        gold = json.loads((ROOT / "tests/golden/config_C4n10.json").read_text())["solvers"]["dacg"]
+        ref = np.asarray(gold["eigenvalues"])
+        out["eig_relerr_vs_reference"] = float(np.max(np.abs(pairs.values - ref) / ref))
+        out["reference_mvp"] = gold["mvp"]
+        out["reference_wall_s_build_container"] = gold["wall_seconds"]
+    except Exception:
+        pass
+    return out
+
+
 def c5_block(peaks, steps=10, dist=None, world=1, rank=0):
     """BASELINE configs[4] (R-MAT scale 26, edge factor 16, ~2.1e9 nonzeros):
     device-side ingest (sampling, dedupe, largest component, packed
@@ -509,6 +556,10 @@ def main():
         f_mc.device()   # device factor upload = setup, like the reference's splu
         line["solve"] = solve_block(a, f, f_mc)
         line["solve_configs"] = solve_configs_block({"C4": (a, f)})
+    if not args.no_solve and args.config == "C4":
+        sd = solve_dist_block(a, dist=dist, world=world, rank=rank)
+        if rank == 0:
+            line["solve_dist"] = sd
     if not args.no_c5:
         c5 = c5_block(peaks, dist=dist, world=world, rank=rank)
         if rank == 0:

@@ -427,6 +427,10 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0, comm
         counter = MvpCounter()
     if null_basis is None:
         null_basis = kernel_basis(a.n)
+    if comm is not None and comm.world == 1 and isinstance(f, str):
+        # one rank: block-Jacobi IC(0) with one block is the reference IC(0)
+        from .precond import JacobiFactor
+        f = JacobiFactor(a) if f == "jacobi" else None
     if f is None and (comm is None or comm.world == 1):
         f = ic0_factorize(a)
     if neig < 1:

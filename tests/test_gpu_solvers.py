@@ -128,10 +128,12 @@ def test_baseline_small_configs(L, cfg):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("cfg", ["C3", "C4"])
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C3n20", "C4n10"])
 def test_baseline_large_configs(L, cfg):
+    # C3n20 / C4n10: the BASELINE's own neig (20 JD pairs on C3, 10 DACG + JD
+    # pairs on C4), reference runs recorded by tests/golden/make_golden.py
     ref = golden_config(cfg)
-    a = L.build_laplacian(L.config_graph(cfg))
+    a = L.build_laplacian(L.config_graph(cfg[:2]))
     f = L.ic0_factorize(a)
     for sv, rr in ref["solvers"].items():
         pairs, rep = solver(L, sv)(a, ref["neig"], delta=ref["delta"], f=f)
