@@ -295,13 +295,13 @@ def solve_configs_block(prebuilt=None):
 
 
 def solve_dist_block(a, dist=None, world=1, rank=0, neig=10, delta=1e-8):
-    """Row-partitioned DACG on C4 at the BASELINE's neig 10, delta 1e-8
-    (SURVEY 8(e)): every rank owns a row block and its slice of every solver
-    vector; one all-reduce per dot pass, one in-place slice exchange per
-    SpMV.  Preconditioner: block-Jacobi IC(0) of each rank's diagonal block
-    (the reference IC(0) itself at N = 1; the natural-order sweeps do not
-    shard).  Time to solution = max over ranks (factorization excluded, as in
-    the reference harness bench.py:123-125)."""
+    """Row-partitioned DACG and JD on C4 at the BASELINE's neig 10, delta
+    1e-8: every rank owns a row block and its slice of every
+    solver vector; one all-reduce per dot pass, one in-place slice exchange
+    per SpMV.  Preconditioner: block-Jacobi IC(0) of each rank's diagonal
+    block (the reference IC(0) itself at N = 1; the natural-order sweeps do
+    not shard).  Time to solution = max over ranks (factorization excluded,
+    as in the reference harness bench.py:123-125)."""
     import torch
     import paper_1311_1695_b200 as L
     from paper_1311_1695_b200.dist import BlockJacobiIc0, RowComm, RowPartition, TorchBackend
@@ -312,32 +312,37 @@ def solve_dist_block(a, dist=None, world=1, rank=0, neig=10, delta=1e-8):
         f.factor.device()
     else:
         f.device()
-    walls = []
-    for _ in range(2):   # first call and steady state
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        pairs, rep = L.dacg_smallest(a, neig, delta=delta, f=f, comm=comm)
-        torch.cuda.synchronize()
-        w = time.perf_counter() - t0
-        if dist:
-            t = torch.tensor([w], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            w = float(t.item())
-        walls.append(w)
-    out = {"solver": "dacg", "neig": neig, "delta": delta, "n_gpus": world,
-           "wall_s": walls[1], "wall_s_first_call": walls[0], "mvp": rep.mvp,
-           "preconditioner": "block-Jacobi ic0 (flagged)" if world > 1 else "ic0 (reference)",
-           "parallelism": f"rows{world}" if world > 1 else "single"}
     try:
-        gold = json.loads((ROOT / "tests/golden/config_C4n10.json").read_text())["solvers"]["dacg"]
-        ref = np.asarray(gold["eigenvalues"])
-        out["eig_relerr_vs_reference"] = float(np.max(np.abs(pairs.values - ref) / ref))
-        out["reference_mvp"] = gold["mvp"]
-        out["reference_wall_s_build_container"] = gold["wall_seconds"]
+        gold = json.loads((ROOT / "tests/golden/config_C4n10.json").read_text())["solvers"]
     except Exception:
-        pass
+        gold = {}
+    out = {}
+    for name, fn in (("dacg", L.dacg_smallest), ("jd", L.jd_smallest)):
+        walls = []
+        for _ in range(2):   # first call and steady state
+            torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
+            t0 = time.perf_counter()
+            pairs, rep = fn(a, neig, delta=delta, f=f, comm=comm)
+            torch.cuda.synchronize()
+            w = time.perf_counter() - t0
+            if dist:
+                t = torch.tensor([w], device="cuda", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                w = float(t.item())
+            walls.append(w)
+        r = {"neig": neig, "delta": delta, "n_gpus": world, "wall_s": walls[1],
+             "wall_s_first_call": walls[0], "mvp": rep.mvp,
+             "preconditioner": "block-Jacobi ic0 (flagged)" if world > 1 else "ic0 (reference)",
+             "parallelism": f"rows{world}" if world > 1 else "single"}
+        g = gold.get(name)
+        if g:
+            ref = np.asarray(g["eigenvalues"])
+            r["eig_relerr_vs_reference"] = float(np.max(np.abs(pairs.values - ref) / ref))
+            r["reference_mvp"] = g["mvp"]
+            r["reference_wall_s_build_container"] = g["wall_seconds"]
+        out[name] = r
     return out
 
 

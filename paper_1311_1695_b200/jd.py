@@ -21,7 +21,7 @@ import time
 import numpy as np
 
 from . import _device as dev
-from ._plan import Fused, Slots, Spmv
+from ._plan import Ctx, Fused, PrecApply, Slots, Spmv
 from ._rng import NormalStream
 from .ic0 import ic0_factorize
 from .kernels import DeviceGS, GramSchmidtBreakdown, dense_sym_eig
@@ -104,9 +104,10 @@ class JdWorkspace:
         self._m = m + 1
 
 
-def _ritz(ws, S, u_out, r_out):
+def _ritz(ws, S, u_out, r_out, cx=None):
     """theta, and on the device u = Vy/|Vy|, r = (Wy - theta Vy)/|Vy|;
     returns (theta, |r|^2)."""
+    cx = cx or Ctx(ws.n)
     vals, vecs = dense_sym_eig(ws.h)
     y = vecs[:, 0]
     theta = float(vals[0])
@@ -115,10 +116,10 @@ def _ritz(ws, S, u_out, r_out):
     S.set(theta=theta)
     n = ws.n
     # u_raw = V y, wy = W y (block updates with cscale -1), |u_raw|^2
-    Fused(n, outs=[dict(out=ws._ur, terms=[], upd=(ws.V, m, S.p("y"), -1.0)),
+    cx.fused(outs=[dict(out=ws._ur, terms=[], upd=(ws.V, m, S.p("y"), -1.0)),
                    dict(out=ws._wy, terms=[], upd=(ws.W, m, S.p("y"), -1.0))],
           dots=[(1, None)], result=S.s[S.idx["nu2"]:])()
-    Fused(n, outs=[dict(out=u_out, terms=[(ws._ur, 1.0)], post=(S.p("nu2"), 3)),
+    cx.fused(outs=[dict(out=u_out, terms=[(ws._ur, 1.0)], post=(S.p("nu2"), 3)),
                    dict(out=r_out, terms=[(ws._wy, 1.0), (ws._ur, -1.0, S.p("theta"))],
                         post=(S.p("nu2"), 3))],
           dots=[(2, None)], result=S.s[S.idx["rr"]:])()
@@ -146,12 +147,14 @@ def rayleigh_ritz_extract(workspace):
     return theta, workspace.u, dev.to_host(r)
 
 
-def _gemm(n, src, mrows, ycols, out):
-    """out[:p] = (src[:mrows] as columns) @ ycols on the device."""
+def _gemm(n, src, mrows, ycols, out, cx=None):
+    """out[:p] = (src[:mrows] as columns) @ ycols on the device (over this
+    rank's rows when cx is row-partitioned)."""
     from . import _native as nat
     yc = np.asfortranarray(np.asarray(ycols, dtype=np.float64))
-    nat.call("lg_gemm_small", n, src.data_ptr(), n, mrows, yc.ctypes.data,
-             yc.shape[1], out.data_ptr(), n, dev.stream_ptr())
+    lo, nl = (cx.lo, cx.nl) if cx is not None else (0, n)
+    nat.call("lg_gemm_small", nl, src.data_ptr() + 8 * lo, n, mrows, yc.ctypes.data,
+             yc.shape[1], out.data_ptr() + 8 * lo, n, dev.stream_ptr())
 
 
 def jd_restart(workspace):
@@ -179,12 +182,15 @@ def jd_restart(workspace):
 def jd_smallest(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
                 m_min=5, m_max=10, f=None, null_basis=None, *, seed=0,
                 max_outer_per_pair=300, stagnation_window=60,
-                counter=None, v0=None):
+                counter=None, v0=None, comm=None):
     """neig smallest strictly positive eigenpairs of a by Jacobi-Davidson
     (jd.py:100-255).  The outer iteration for a pair stops once
     ||r|| < delta * theta, after which the pair is verified with a fresh
     product and locked; the correction equation runs at relative tolerance
-    delta_pcg with at most itmax_inner PCG iterations."""
+    delta_pcg with at most itmax_inner PCG iterations.
+
+    comm (extension, not in the reference): a dist.RowComm -- one rank of a
+    row-partitioned solve, as for dacg_smallest."""
     with dev.solver_stream():
         return _jd_smallest_impl(**locals())
 
@@ -192,13 +198,18 @@ def jd_smallest(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
 def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
                 m_min=5, m_max=10, f=None, null_basis=None, *, seed=0,
                 max_outer_per_pair=300, stagnation_window=60,
-                counter=None, v0=None):
+                counter=None, v0=None, comm=None):
     t0 = time.perf_counter()
     if counter is None:
         counter = MvpCounter()
     if null_basis is None:
         null_basis = kernel_basis(a.n)
-    if f is None:
+    dist = comm is not None and comm.world > 1
+    if comm is not None and comm.world == 1 and isinstance(f, str):
+        # one rank: block-Jacobi IC(0) with one block is the reference IC(0)
+        from .precond import JacobiFactor
+        f = JacobiFactor(a) if f == "jacobi" else None
+    if f is None and not dist:
         f = ic0_factorize(a)
     if neig < 1:
         raise ValueError("neig must be at least 1")
@@ -211,8 +222,13 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
     rng = np.random.default_rng(seed)
     n = a.n
     draws = NormalStream(rng, n)
-    csr = device_csr(a)
-    prec = device_preconditioner(f, n)
+    cx = Ctx(n, comm)
+    if dist:
+        csr = comm.local_operator(a)
+        prec = comm.local_preconditioner(a, f)
+    else:
+        csr = device_csr(a)
+        prec = device_preconditioner(f, n)
     kg = null_basis.k
     kcap = kg + neig + m_max + 1
     if kcap > 64:
@@ -225,8 +241,8 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
     for nm, c in (("y", m_max + 1), ("theta", 1), ("nu2", 1), ("rr", 1), ("hd", 2 * m_max + 4),
                   ("vf", 4)):
         S.add(nm, c)
-    gs = DeviceGS(n)
-    engine = DevicePcg(csr, prec, n, "jd", kg + neig + 1)
+    gs = DeviceGS(n, cx=cx)
+    engine = DevicePcg(csr, prec, n, "jd", kg + neig + 1, cx=cx)
     u = dev.empty(n)
     r = dev.empty(n)
     ufix = dev.empty(n)
@@ -249,7 +265,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
     best_res, since_best, outer_here = np.inf, 0, 0
 
     def gemm(src, mrows, ycols, out):
-        _gemm(n, src, mrows, ycols, out)
+        _gemm(n, src, mrows, ycols, out, cx)
 
     while len(locked_vals) < neig:
         pair_idx = len(locked_vals)
@@ -272,11 +288,11 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
                         f"pair {pair_idx}: search space saturated the "
                         "complement without meeting the tolerance") from exc
             # w_new = A v_new with the epilogue col/diag = V'^T w_new
-            Spmv(csr, B[kg + m], W[m], q=B[kg:], nq=m + 1, result=S.s[S.idx["hd"]:])()
+            cx.spmv(csr, B[kg + m], W[m], q=B[kg:], nq=m + 1, result=S.s[S.idx["hd"]:])()
             counter.increment()
             outer_mvps += 1
             if m:
-                Fused(n, blocks=[(W, m, B[kg + m])], result=S.s[S.idx["hd"] + m + 1:])()
+                cx.fused(blocks=[(W, m, B[kg + m])], result=S.s[S.idx["hd"] + m + 1:])()
             hd = S.fetch()[0][S.idx["hd"]:S.idx["hd"] + 2 * m + 1]
             Hn = np.zeros((m + 1, m + 1))
             Hn[:m, :m] = H
@@ -286,7 +302,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
             H = 0.5 * (Hn + Hn.T)
             m += 1
         sp.V, sp.W, sp.h, sp.m = B[kg:], W, H, m
-        theta, rr, hvals, hvecs = _ritz(sp, S, u, r)
+        theta, rr, hvals, hvecs = _ritz(sp, S, u, r, cx)
         if theta <= 0:
             raise SolverError(f"pair {pair_idx}: nonpositive Ritz value {theta}")
         res = float(np.sqrt(rr))
@@ -297,12 +313,12 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
             since_best += 1
         if res < delta * theta:
             gs.run(u, [(B, kg)], ufix)
-            Spmv(csr, ufix, wfix, dots=[ufix], result=S.s[S.idx["vf"]:])()
+            cx.spmv(csr, ufix, wfix, dots=[ufix], result=S.s[S.idx["vf"]:])()
             counter.increment()
             verify_mvps += 1
             theta_fix = float(S.fetch()[0][S.idx["vf"]])
             S.set(theta=theta_fix)
-            Fused(n, outs=[dict(out=r, terms=[(wfix, 1.0), (ufix, -1.0, S.p("theta"))])],
+            cx.fused(outs=[dict(out=r, terms=[(wfix, 1.0), (ufix, -1.0, S.p("theta"))])],
                   dots=[(1, None)], result=S.s[S.idx["vf"] + 1:])()
             res_fix = float(np.sqrt(S.fetch()[0][S.idx["vf"] + 1]))
             if res_fix < delta * theta_fix:
@@ -347,21 +363,27 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
         counter.increment(its)
         outer_solves += 1
         inner_total += its
-        Fused(n, dots=[(X, None)], result=S.s[S.idx["vf"] + 2:])()
+        cx.fused(dots=[(X, None)], result=S.s[S.idx["vf"] + 2:])()
         if float(S.fetch()[0][S.idx["vf"] + 2]) == 0.0 and res > 0.0:
             # immediate indefinite direction: fall back to P M P (-r)
-            from .pcg import project_device
             qs = Slots(capacity=256)
-            t1 = project_device(B, kg, r, slots=qs)
-            t1 = project_device(u.view(1, n), 1, t1, slots=qs)
-            Fused(n, outs=[dict(out=t1, terms=[(t1, -1.0)])])()
+            t0v, t1 = dev.empty(n), dev.empty(n)
+            cx.project(B, kg, r, t0v, qs)
+            cx.project(u.view(1, n), 1, t0v, t1, qs, name="_pu")
+            cx.fused(outs=[dict(out=t1, terms=[(t1, -1.0)])])()
             t2 = dev.empty(n)
-            prec.apply(t1, t2)
-            t2 = project_device(B, kg, t2, slots=qs)
-            cand = project_device(u.view(1, n), 1, t2, slots=qs)
+            if cx.dist:
+                PrecApply(prec, cx.v(t1), cx.v(t2))()
+            else:
+                prec.apply(t1, t2)
+            cx.project(B, kg, t2, t0v, qs)
+            cand = dev.empty(n)
+            cx.project(u.view(1, n), 1, t0v, cand, qs, name="_pu")
         else:
             cand = X
 
+    for row in locked_vecs:
+        cx.gather(B[row])    # row-partitioned: every rank returns whole vectors
     order = np.argsort(locked_vals, kind="stable")
     vals = np.asarray(locked_vals)[order]
     vecs = dev.columns_to_host(B[[locked_vecs[i] for i in order]], n)

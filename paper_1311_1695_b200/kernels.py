@@ -37,9 +37,10 @@ class DeviceGS:
     writes its norm^2 and its Q^T v coefficients contiguously.
     """
 
-    def __init__(self, n, slots=None):
-        from ._plan import Slots
+    def __init__(self, n, slots=None, cx=None):
+        from ._plan import Ctx, Slots
         self.n = n
+        self.cx = cx or Ctx(n)
         self.S = slots or Slots()
         for nm in ("n0", "c1", "n1", "c2", "n2", "c3"):
             self.S.add(nm, 64 if nm[0] == "c" else 1)
@@ -49,19 +50,18 @@ class DeviceGS:
         """out = unit vector of v orthogonalised against blocks; returns
         (norm_out, norm_in).  blocks: list of ((k, n) tensor, k).  out may
         not alias v."""
-        from ._plan import Fused
-        S, n = self.S, self.n
+        S, cx = self.S, self.cx
         blocks = [(q, k) for q, k in blocks if k > 0]
         ktot = sum(k for _, k in blocks)
         if ktot > 64:
             raise ValueError("Gram-Schmidt block wider than 64 columns")
-        Fused(n, dots=[(v, None)], blocks=[(q, k, v) for q, k in blocks],
+        cx.fused(dots=[(v, None)], blocks=[(q, k, v) for q, k in blocks],
               result=S.s[S.idx["n0"]:])()
         nin = float(np.sqrt(S.fetch()[0][S.idx["n0"]]))
         if nin == 0.0:
             raise GramSchmidtBreakdown("zero vector cannot be orthonormalized")
         if ktot == 0:
-            Fused(n, outs=[dict(out=out, terms=[(v, 1.0 / nin)])])()
+            cx.fused(outs=[dict(out=out, terms=[(v, 1.0 / nin)])])()
             return nin, nin
 
         def sweep(src, dst, coef, res):
@@ -72,7 +72,7 @@ class DeviceGS:
             o = dict(out=dst, terms=[(src, 1.0)], upd=ups[0])
             if len(ups) > 1:
                 o["upd2"] = ups[1]
-            Fused(n, outs=[o], dots=[(1, None)], blocks=[(q, k, 1) for q, k in blocks],
+            cx.fused(outs=[o], dots=[(1, None)], blocks=[(q, k, 1) for q, k in blocks],
                   result=S.s[S.idx[res]:])()
             return float(np.sqrt(S.fetch()[0][S.idx[res]]))
 
@@ -84,7 +84,7 @@ class DeviceGS:
         if after < _BREAKDOWN_REL * nin:
             raise GramSchmidtBreakdown(
                 f"vector collapsed to {after:.3e} of its input norm {nin:.3e}")
-        Fused(n, outs=[dict(out=out, terms=[(cur, 1.0 / after)])])()
+        cx.fused(outs=[dict(out=out, terms=[(cur, 1.0 / after)])])()
         return after, nin
 
 

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _device as dev
-from ._plan import Fused, Graph, PrecApply, Prog, Slots, Spmv
+from ._plan import Ctx, Fused, Graph, PrecApply, Prog, Slots, Spmv
 from .sparse import device_csr
 
 _ORTHO_TOL = 1e-10
@@ -228,8 +228,9 @@ class DevicePcg:
     them (result = [dots..., block dots...] is written contiguously).
     """
 
-    def __init__(self, csr, prec, n, mode, kmax):
+    def __init__(self, csr, prec, n, mode, kmax, cx=None):
         self.n, self.mode, self.kmax = n, mode, max(1, kmax)
+        self.cx = cx or Ctx(n)
         self.csr = csr
         self.prec = prec
         kq = self.kmax + 1
@@ -311,7 +312,7 @@ class DevicePcg:
             raise ValueError("at most two projection blocks")
         self._sig = sig
         self.qb = qb
-        S, n = self.S, self.n
+        S, n, cx = self.S, self.n, self.cx
         jd = self.mode == "jd"
         has_q = bool(qb)
         stop = S.fp("stop")
@@ -320,15 +321,15 @@ class DevicePcg:
         # psolve(R) -> Z  (Q^T R already in "cr")
         ps = []
         if jd and has_q:
-            ps.append(Fused(n, outs=[self._upd(dict(out=T, terms=[(R, 1.0)]), "cr")],
+            ps.append(cx.fused(outs=[self._upd(dict(out=T, terms=[(R, 1.0)]), "cr")],
                             skip=stop))
-            ps.append(PrecApply(self.prec, T, Z0, skip=stop))
+            ps.append(PrecApply(self.prec, cx.v(T), cx.v(Z0), skip=stop))
         else:
-            ps.append(PrecApply(self.prec, R, Z0, skip=stop))
+            ps.append(PrecApply(self.prec, cx.v(R), cx.v(Z0), skip=stop))
         if has_q:
-            ps.append(Fused(n, blocks=self._qdots(Z0), result=self._res("cz1"), skip=stop))
+            ps.append(cx.fused(blocks=self._qdots(Z0), result=self._res("cz1"), skip=stop))
             if jd:
-                ps.append(Fused(n, outs=[self._upd(dict(out=Z1, terms=[(Z0, 1.0)]), "cz1")],
+                ps.append(cx.fused(outs=[self._upd(dict(out=Z1, terms=[(Z0, 1.0)]), "cz1")],
                                 blocks=self._qdots(1), result=self._res("cz2"), skip=stop))
                 zlast = lambda: self._upd(dict(out=Z, terms=[(Z1, 1.0)]), "cz2")  # noqa: E731
             else:
@@ -337,74 +338,76 @@ class DevicePcg:
             zlast = lambda: dict(out=Z, terms=[(Z0, 1.0)])  # noqa: E731
         self.ps = ps
         # z of the setup also initialises P = Z and rz = R.Z
-        self.zinit = Fused(n, outs=[zlast(), dict(out=P, terms=[(1, 1.0)])], dots=[(R, 1)],
+        self.zinit = cx.fused(outs=[zlast(), dict(out=P, terms=[(1, 1.0)])], dots=[(R, 1)],
                            result=self._res("rz"), skip=stop)
         body = []
         theta = S.p("theta")
         if jd:
-            body.append(Spmv(self.csr, P, Y, theta_d=theta, skip=stop))
+            body.append(cx.spmv(self.csr, P, Y, theta_d=theta, skip=stop))
             if has_q:
-                body.append(Fused(n, blocks=self._qdots(Y), result=self._res("cy1"), skip=stop))
-                body.append(Fused(n, outs=[self._upd(dict(out=T, terms=[(Y, 1.0)]), "cy1")],
+                body.append(cx.fused(blocks=self._qdots(Y), result=self._res("cy1"), skip=stop))
+                body.append(cx.fused(outs=[self._upd(dict(out=T, terms=[(Y, 1.0)]), "cy1")],
                                   blocks=self._qdots(1), result=self._res("cy2"), skip=stop))
-                body.append(Fused(n, outs=[self._upd(dict(out=AP, terms=[(T, 1.0)]), "cy2")],
+                body.append(cx.fused(outs=[self._upd(dict(out=AP, terms=[(T, 1.0)]), "cy2")],
                                   dots=[(P, 1)], result=self._res("pap"), skip=stop,
                                   prog=self.p_gamma))
             else:
-                body.append(Fused(n, outs=[dict(out=AP, terms=[(Y, 1.0)])], dots=[(P, 1)],
+                body.append(cx.fused(outs=[dict(out=AP, terms=[(Y, 1.0)])], dots=[(P, 1)],
                                   result=self._res("pap"), skip=stop, prog=self.p_gamma))
         else:
             if len(qb) == 1:
-                body.append(Spmv(self.csr, P, Y, q=qb[0][0], nq=qb[0][1],
+                body.append(cx.spmv(self.csr, P, Y, q=qb[0][0], nq=qb[0][1],
                                  result=self._res("cy1"), skip=stop))
             else:
-                body.append(Spmv(self.csr, P, Y, skip=stop))
+                body.append(cx.spmv(self.csr, P, Y, skip=stop))
                 if has_q:
-                    body.append(Fused(n, blocks=self._qdots(Y), result=self._res("cy1"),
+                    body.append(cx.fused(blocks=self._qdots(Y), result=self._res("cy1"),
                                       skip=stop))
             o = dict(out=AP, terms=[(Y, 1.0)])
             if has_q:
                 self._upd(o, "cy1")
-            body.append(Fused(n, outs=[o], dots=[(P, 1)], result=self._res("pap"), skip=stop,
+            body.append(cx.fused(outs=[o], dots=[(P, 1)], result=self._res("pap"), skip=stop,
                               prog=self.p_gamma))
         gam = S.p("gamma")
         if has_q:
-            body.append(Fused(n, outs=[dict(out=X, terms=[(X, 1.0), (P, 1.0, gam)]),
+            body.append(cx.fused(outs=[dict(out=X, terms=[(X, 1.0), (P, 1.0, gam)]),
                                        dict(out=T, terms=[(R, 1.0), (AP, -1.0, gam)])],
                               blocks=self._qdots(2), result=self._res("cr1"), skip=stop))
             # R = T - Q cr1, rr = R.R and Q^T R -> cr (rr is followed by cr)
-            body.append(Fused(n, outs=[self._upd(dict(out=R, terms=[(T, 1.0)]), "cr1")],
+            body.append(cx.fused(outs=[self._upd(dict(out=R, terms=[(T, 1.0)]), "cr1")],
                               dots=[(1, None)], blocks=self._qdots(1), result=self._res("rr"),
                               skip=stop, prog=self.p_relres))
         else:
-            body.append(Fused(n, outs=[dict(out=X, terms=[(X, 1.0), (P, 1.0, gam)]),
+            body.append(cx.fused(outs=[dict(out=X, terms=[(X, 1.0), (P, 1.0, gam)]),
                                        dict(out=R, terms=[(R, 1.0), (AP, -1.0, gam)])],
                               dots=[(2, None)], result=self._res("rr"), skip=stop,
                               prog=self.p_relres))
         body += ps
-        body.append(Fused(n, outs=[zlast()], dots=[(R, 1)], result=self._res("rzn"), skip=stop,
+        body.append(cx.fused(outs=[zlast()], dots=[(R, 1)], result=self._res("rzn"), skip=stop,
                           prog=self.p_beta))
-        body.append(Fused(n, outs=[dict(out=P, terms=[(Z, 1.0), (P, 1.0, S.p("beta"))])],
+        body.append(cx.fused(outs=[dict(out=P, terms=[(Z, 1.0), (P, 1.0, S.p("beta"))])],
                           skip=stop))
         self.body = body
         self.body_graph = Graph(body)
+        if cx.dist:
+            self.body_graph.eager = True   # host-issued collectives in the body
 
     def solve(self, b, qb, tol, maxit, theta=0.0, negate=False):
         """Solve op(x) = (-b if negate else b) from x0 = 0; returns
         (X, its, relres, converged, indefinite).  X is this engine's buffer."""
         self.build(qb)
-        S, n = self.S, self.n
+        S, cx = self.S, self.cx
         S.clear_flags()
         S.set(theta=theta, tol=tol)
         sign = -1.0 if negate else 1.0
         R, X = self.R, self.X
         if self.qb:
-            Fused(n, blocks=self._qdots(b), result=self._res("cb"))()
-            Fused(n, outs=[self._upd(dict(out=R, terms=[(b, sign)]), "cb", sign),
+            cx.fused(blocks=self._qdots(b), result=self._res("cb"))()
+            cx.fused(outs=[self._upd(dict(out=R, terms=[(b, sign)]), "cb", sign),
                            dict(out=X, terms=[])],
                   dots=[(1, None)], blocks=self._qdots(1), result=self._res("rr"))()
         else:
-            Fused(n, outs=[dict(out=R, terms=[(b, sign)]), dict(out=X, terms=[])],
+            cx.fused(outs=[dict(out=R, terms=[(b, sign)]), dict(out=X, terms=[])],
                   dots=[(1, None)], result=self._res("rr"))()
         self.p_setup()
         for f in self.ps:

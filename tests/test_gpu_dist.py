@@ -79,3 +79,48 @@ def test_row_partitioned_dacg_block_ic0():
     assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-8
     _, res = rayleigh_residuals(a, pairs.vectors)
     assert np.max(res) <= 1.5 * delta
+
+
+def _run_ranks_jd(a, world, f, neig, delta):
+    import torch
+
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200.dist import RowComm, RowPartition, ThreadWorld
+    tw = ThreadWorld(world)
+    part = RowPartition(a.row_ptr, world)
+    out, errs = [None] * world, []
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = L.jd_smallest(a, neig, delta=delta, f=f, seed=0,
+                                   comm=RowComm(part, r, tw))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            tw.bar.abort()
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("world,prec", [(2, "jacobi"), (3, "block_ic0")])
+def test_row_partitioned_jd(world, prec):
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200.results import rayleigh_residuals
+    a = _graph()
+    delta = 1e-8
+    ref, _ = L.jd_smallest(a, 4, delta=delta, seed=0)          # reference IC(0)
+    out = _run_ranks_jd(a, world, prec, 4, delta)
+    for pairs, _ in out:
+        assert np.array_equal(pairs.values, out[0][0].values)
+    pairs, rep = out[0]
+    assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-8
+    _, res = rayleigh_residuals(a, pairs.vectors)
+    assert np.max(res) <= 1.5 * delta
+    assert pairs.gram_defect() <= 1e-8 and pairs.kernel_overlap() <= 1e-8
