@@ -520,6 +520,22 @@ def main():
                "d2h_bytes_per_step": 8 * n,
                "path": "paper_1311_1695_b200.spmv(a, numpy x) -> numpy y"
                        + (" (rank 0, whole matrix)" if world > 1 else "")}
+        # the same through the C ABI a reference-side binding would call
+        # (lg_spmv_host: host x in, host y out)
+        import ctypes
+        from paper_1311_1695_b200 import _native as nat
+        yh = np.empty(n)
+        xd_, yd_ = dev.empty(n), dev.empty(n)
+        args_c = (a.device().handle, xh.ctypes.data, yh.ctypes.data,
+                  ctypes.c_void_p(xd_.data_ptr()), ctypes.c_void_p(yd_.data_ptr()),
+                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        for _ in range(3):
+            nat.call("lg_spmv_host", *args_c)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            nat.call("lg_spmv_host", *args_c)
+        e2e["cabi_value"] = reps / (time.perf_counter() - t0)
+        e2e["cabi_path"] = "lg_spmv_host(csr, x_h, y_h, ...) (C ABI, pinned staging)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

@@ -151,6 +151,34 @@ class Pinned:
                  self.nbytes, stream if stream is not None else stream_ptr())
 
 
+class _Staging:
+    __slots__ = ("n", "xin", "yout", "xd", "yd")
+
+    def __init__(self, n):
+        t = torch()
+        self.n = n
+        self.xin = t.empty(n, dtype=t.float64, pin_memory=True)
+        self.yout = t.empty(n, dtype=t.float64, pin_memory=True)
+        self.xd = empty(n)
+        self.yd = empty(n)
+
+
+def staging(n):
+    """Per-thread pinned host buffers + device buffers for host-array
+    products of length n (reused across calls; the caller synchronises
+    before returning)."""
+    cache = getattr(_state, "staging", None)
+    if cache is None:
+        cache = _state.staging = {}
+    key = (n, torch().cuda.current_device())
+    st = cache.get(key)
+    if st is None:
+        if len(cache) >= 4:
+            cache.clear()
+        st = cache[key] = _Staging(n)
+    return st
+
+
 _solver_streams = {}
 
 

@@ -26,7 +26,7 @@ INCLUDE = HERE.parent / "include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
-    "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v",
+    "-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-fopenmp", "-Xptxas", "-v",
     f"-I{INCLUDE}",
 ]
 
@@ -74,7 +74,7 @@ def build(force=False, jobs=None, verbose=False):
         objs = list(ex.map(_compile, srcs))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", *map(str, objs),
-           "-o", str(tmp), "-lpthread", "-ldl", "-lrt"]
+           "-o", str(tmp), "-lgomp", "-lpthread", "-ldl", "-lrt"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")

@@ -788,17 +788,80 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
   return launch<LG_MAXD + LG_MAXQ>(args, ws, s, pk);
 }
 
+}  // extern "C"
+
+namespace {
+// Pinned staging of the host-buffer SpMV (one pair per thread, grown on
+// demand).  A pageable cudaMemcpy goes through the driver's bounce buffers at
+// about half the PCIe rate and the D2H lands in pages the caller may never
+// have touched; instead the caller's x is copied by a few host threads into
+// pinned memory, moved by DMA, and y comes back the same way.
+struct HostStaging {
+  double* xin = nullptr;
+  double* yout = nullptr;
+  int64_t cap = 0;
+  ~HostStaging() {
+    if (xin) cudaFreeHost(xin);
+    if (yout) cudaFreeHost(yout);
+  }
+  bool ensure(int64_t n) {
+    if (n <= cap) return true;
+    if (xin) cudaFreeHost(xin);
+    if (yout) cudaFreeHost(yout);
+    xin = yout = nullptr;
+    cap = 0;
+    if (cudaHostAlloc(&xin, 8 * (size_t)n, cudaHostAllocDefault) != cudaSuccess ||
+        cudaHostAlloc(&yout, 8 * (size_t)n, cudaHostAllocDefault) != cudaSuccess)
+      return false;
+    cap = n;
+    return true;
+  }
+};
+thread_local HostStaging g_stage;
+// workspace of the host-buffer path (long-row partials); the call is
+// synchronous, so one per thread suffices
+struct HostWs {
+  lg_ws* ws = nullptr;
+  ~HostWs() {
+    if (ws) lg_ws_destroy(ws);
+  }
+};
+thread_local HostWs g_host_ws;
+
+void par_copy(double* dst, const double* src, int64_t n) {
+  // OpenMP's persistent pool: spawning threads per call would cost more than
+  // the copy (8 MB per vector at C4)
+  const int64_t kChunkD = 1 << 16;   // doubles per task
+  const int64_t nc = (n + kChunkD - 1) / kChunkD;
+#pragma omp parallel for schedule(static) num_threads(8) if (nc > 1)
+  for (int64_t c = 0; c < nc; ++c) {
+    const int64_t lo = c * kChunkD, hi = std::min(n, lo + kChunkD);
+    std::memcpy(dst + lo, src + lo, 8 * (size_t)(hi - lo));
+  }
+}
+}  // namespace
+
+extern "C" {
+
 int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,
                  double* yd, void* stream) {
   if (!a || !x_h || !y_h || !xd || !yd) return fail(LG_EINVAL, "lg_spmv_host: NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
-  size_t bytes = sizeof(double) * (size_t)a->n;
-  LG_CUDA(cudaMemcpyAsync(xd, x_h, bytes, cudaMemcpyHostToDevice, s));
+  const int64_t n = a->n;
+  size_t bytes = sizeof(double) * (size_t)n;
+  if (!g_stage.ensure(n)) return fail(LG_ENOMEM, "lg_spmv_host: pinned staging");
+  if (!g_host_ws.ws) {
+    int rc0 = lg_ws_create(&g_host_ws.ws);
+    if (rc0) return rc0;
+  }
+  par_copy(g_stage.xin, x_h, n);
+  LG_CUDA(cudaMemcpyAsync(xd, g_stage.xin, bytes, cudaMemcpyHostToDevice, s));
   int rc = lg_spmv(a, xd, yd, 0.0, nullptr, 0, 0, nullptr, nullptr, 0, 0,
-                   nullptr, nullptr, nullptr, stream);
+                   nullptr, g_host_ws.ws, nullptr, stream);
   if (rc) return rc;
-  LG_CUDA(cudaMemcpyAsync(y_h, yd, bytes, cudaMemcpyDeviceToHost, s));
+  LG_CUDA(cudaMemcpyAsync(g_stage.yout, yd, bytes, cudaMemcpyDeviceToHost, s));
   LG_CUDA(cudaStreamSynchronize(s));
+  par_copy(y_h, g_stage.yout, n);
   return LG_OK;
 }
 

@@ -444,3 +444,35 @@ def test_row_partitioned_spmv_device_sliced(L, world):
         assert torch.all(ys[:r0] == -7.0) and torch.all(ys[r1:] == -7.0)
         y[r0:r1] = ys[r0:r1]
     assert torch.equal(y, y_ref)
+
+
+def test_spmv_host_buffers_cabi_and_public():
+    """The host-buffer SpMV through the C ABI (lg_spmv_host: pinned staging,
+    H2D, product, D2H) and through the public numpy spmv both equal the
+    device product bit for bit, and match the oracle."""
+    import ctypes
+
+    import torch
+
+    import paper_1311_1695_b200 as L
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200 import _native as nat
+    # hubs above 1024 neighbours: the long-row path (needs the internal workspace)
+    g, _ = L.largest_component(L.generators.chung_lu_graph(20000, 2.1, 8.0, max_degree=4000,
+                                                           weighted=True, seed=11))
+    a = L.build_laplacian(g)
+    x = np.random.default_rng(3).standard_normal(a.n)
+    yd = dev.empty(a.n)
+    a.device().matvec(dev.to_device(x), yd)
+    want = yd.cpu().numpy()
+    y1 = L.spmv(a, x)
+    assert np.array_equal(y1, want)
+    y2 = np.empty(a.n)
+    xd, ydd = dev.empty(a.n), dev.empty(a.n)
+    nat.call("lg_spmv_host", a.device().handle, x.ctypes.data, y2.ctypes.data,
+             ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(ydd.data_ptr()),
+             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert np.array_equal(y2, want)
+    yr = O.spmv(O.Csr(a.n, a.row_ptr, a.col_idx, a.values), x)
+    assert np.max(np.abs(y2 - yr)) <= 1e-13 * np.max(np.abs(yr))
