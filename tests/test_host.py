@@ -181,3 +181,48 @@ def test_no_cpu_fallback():
     from paper_1311_1695_b200.graphs import EdgeList, build_laplacian
     with pytest.raises(RuntimeError):
         build_laplacian(EdgeList(2, [0], [1], [1.0]))
+
+
+def test_row_partitioned_pass_addresses():
+    """The plan context of a row-partitioned rank (_plan.Ctx): every pass
+    covers exactly the rank's rows of the full-length buffers (vectors and
+    column blocks offset by 8 r0 bytes, block leading dimension n), a pass
+    with dot products is followed by one all-reduce of its result slots and
+    then its scalar program, and a single rank folds nothing (no GPU needed:
+    the launches are only built)."""
+    import torch
+
+    from paper_1311_1695_b200._plan import AllReduce, Ctx, Fused, Seq
+
+    class FakeComm:
+        world, r0, r1 = 3, 100, 250
+        nl = 150
+
+        def __init__(self):
+            self.reduced = []
+
+        def allreduce_(self, t):
+            self.reduced.append(t.numel())
+
+    n, k = 400, 3
+    x, y = torch.zeros(n, dtype=torch.float64), torch.zeros(n, dtype=torch.float64)
+    C = torch.zeros((k, n), dtype=torch.float64)
+    res = torch.zeros(16, dtype=torch.float64)
+    comm = FakeComm()
+    cx = Ctx(n, comm)
+    assert cx.dist and cx.lo == 100 and cx.nl == 150
+    seq = cx.fused(outs=[dict(out=y, terms=[(x, 2.0)], upd=(C, k, 0))],
+                   dots=[(1, x)], blocks=[(C, k, 1)], result=res)
+    assert isinstance(seq, Seq) and isinstance(seq.steps[1], AllReduce)
+    f = seq.fused
+    a = f.args
+    assert a.n == 150
+    assert a.o[0].out == y.data_ptr() + 800 and a.o[0].t[0].v == x.data_ptr() + 800
+    assert a.o[0].uq == C.data_ptr() + 800 and a.o[0].uld == n and a.o[0].uk == k
+    assert a.db[0] == x.data_ptr() + 800
+    assert a.b[0].q == C.data_ptr() + 800 and a.b[0].ld == n and a.b[0].k == k
+    seq.steps[1]()
+    assert comm.reduced == [1 + k]          # one all-reduce over dots + Q^T v slots
+    # one rank: the plain single-GPU pass, nothing wrapped
+    one = Ctx(n, None).fused(dots=[(x, None)], result=res)
+    assert isinstance(one, Fused) and one.args.n == n
