@@ -152,21 +152,17 @@ class Pinned:
 
 
 class _Staging:
-    __slots__ = ("n", "xin", "yout", "xd", "yd")
+    __slots__ = ("n", "xd", "yd")
 
     def __init__(self, n):
-        t = torch()
         self.n = n
-        self.xin = t.empty(n, dtype=t.float64, pin_memory=True)
-        self.yout = t.empty(n, dtype=t.float64, pin_memory=True)
         self.xd = empty(n)
         self.yd = empty(n)
 
 
 def staging(n):
-    """Per-thread pinned host buffers + device buffers for host-array
-    products of length n (reused across calls; the caller synchronises
-    before returning)."""
+    """Per-thread device buffers for host-array products of length n (reused
+    across calls; the product is synchronous, so reuse is safe)."""
     cache = getattr(_state, "staging", None)
     if cache is None:
         cache = _state.staging = {}

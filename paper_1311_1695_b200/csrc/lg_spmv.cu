@@ -79,6 +79,11 @@ struct lg_csr {
   double* table = nullptr;         // distinct off-diagonal values [nvals]
   int32_t* long_nparts = nullptr;  // device [nlong]
   int64_t* long_first = nullptr;   // device [nlong] slot of part 0
+  // row chunks of the schedule for the host-buffer path (lg_spmv_host):
+  // blocks [chunk_b[c], chunk_b[c+1]) cover rows [chunk_row[c], chunk_row[c+1])
+  int nchunks = 0;
+  int64_t chunk_b[9] = {};
+  int64_t chunk_row[9] = {};
 };
 
 namespace lg {
@@ -417,6 +422,34 @@ static void build_schedule(int64_t n, const int64_t* rp,
   }
 }
 
+// Split the schedule into up to kHostChunks row chunks of about equal blocks
+// (never inside a long row's parts) so the host-buffer path can copy y back
+// chunk by chunk while the next chunk is computed.
+constexpr int kHostChunks = 4;
+static void set_chunks(lg_csr* a, const std::vector<SpmvBlock>& blocks) {
+  const int64_t nb = (int64_t)blocks.size();
+  a->nchunks = 0;
+  if (nb == 0) return;
+  int64_t prev = 0;
+  a->chunk_b[0] = 0;
+  a->chunk_row[0] = 0;
+  int c = 0;
+  for (int k = 1; k < kHostChunks; ++k) {
+    int64_t b = k * nb / kHostChunks;
+    while (b < nb && blocks[(size_t)b].lshift < 0 && b > 0 &&
+           blocks[(size_t)b - 1].lshift < 0 &&
+           blocks[(size_t)b - 1].nrows == blocks[(size_t)b].nrows)
+      ++b;   // inside one long row's parts
+    if (b <= prev || b >= nb) continue;
+    a->chunk_b[++c] = b;
+    a->chunk_row[c] = blocks[(size_t)b].row0;
+    prev = b;
+  }
+  a->chunk_b[c + 1] = nb;
+  a->chunk_row[c + 1] = a->n;
+  a->nchunks = c + 1;
+}
+
 static int ensure_long_ws(lg_ws* ws, const lg_csr* a) {
   if (a->nlong > ws->long_cap) {
     cudaFree(ws->long_dots);
@@ -471,6 +504,32 @@ static int launch_t(const SpmvArgs& args, lg_ws* ws, cudaStream_t s) {
 template <int NA>
 static int launch(const SpmvArgs& args, lg_ws* ws, cudaStream_t s, bool packed) {
   return packed ? launch_t<NA, true>(args, ws, s) : launch_t<NA, false>(args, ws, s);
+}
+
+// y = A x over the schedule blocks [b0, b1) only (a row chunk; no epilogue).
+static int spmv_range(const lg_csr* a, const double* x, double* y, int64_t b0, int64_t b1,
+                      lg_ws* ws, cudaStream_t s) {
+  if (b1 <= b0) return LG_OK;
+  SpmvArgs args{};
+  args.n = a->n;
+  args.row_ptr = a->packed ? a->prp : a->row_ptr;
+  args.col = a->col;
+  args.val = a->val;
+  args.pcol = a->packed ? a->pcol : nullptr;
+  args.pdiag = a->pdiag;
+  args.table = a->table;
+  args.nvals = a->nvals;
+  args.cbits = a->cbits;
+  args.blocks = a->blocks + b0;
+  args.nblocks = b1 - b0;
+  args.long_nparts = a->long_nparts;
+  args.long_first = a->long_first;
+  args.x = x;
+  args.y = y;
+  args.long_part = ws->long_part;
+  args.long_ticket = ws->long_ticket;
+  args.nlong = a->nlong;
+  return launch<0>(args, ws, s, a->packed != 0);
 }
 
 // Packed Laplacian format eligibility: every row stores its diagonal, the
@@ -589,6 +648,7 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
   a->n = n;
   a->nnz = nnz;
   a->nblocks = (int64_t)blocks.size();
+  set_chunks(a, blocks);
   a->nlong = (int64_t)lnp.size();
   a->packed = packed ? 1 : 0;
   a->cbits = cbits;
@@ -822,6 +882,20 @@ thread_local HostStaging g_stage;
 // synchronous, so one per thread suffices
 struct HostWs {
   lg_ws* ws = nullptr;
+  cudaStream_t d2h = nullptr;           // device -> host copies of y chunks
+  cudaEvent_t done[kHostChunks] = {};   // chunk product finished
+  cudaEvent_t copied[kHostChunks] = {}; // chunk copied to pinned memory
+  bool ok = false;
+  bool ready() {
+    if (ok) return true;
+    if (cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) != cudaSuccess) return false;
+    for (int c = 0; c < kHostChunks; ++c)
+      if (cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&copied[c], cudaEventDisableTiming) != cudaSuccess)
+        return false;
+    ok = true;
+    return true;
+  }
   ~HostWs() {
     if (ws) lg_ws_destroy(ws);
   }
@@ -848,20 +922,58 @@ int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,
   if (!a || !x_h || !y_h || !xd || !yd) return fail(LG_EINVAL, "lg_spmv_host: NULL argument");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t n = a->n;
-  size_t bytes = sizeof(double) * (size_t)n;
+  if (n == 0) return LG_OK;
   if (!g_stage.ensure(n)) return fail(LG_ENOMEM, "lg_spmv_host: pinned staging");
   if (!g_host_ws.ws) {
     int rc0 = lg_ws_create(&g_host_ws.ws);
     if (rc0) return rc0;
   }
-  par_copy(g_stage.xin, x_h, n);
-  LG_CUDA(cudaMemcpyAsync(xd, g_stage.xin, bytes, cudaMemcpyHostToDevice, s));
-  int rc = lg_spmv(a, xd, yd, 0.0, nullptr, 0, 0, nullptr, nullptr, 0, 0,
-                   nullptr, g_host_ws.ws, nullptr, stream);
-  if (rc) return rc;
-  LG_CUDA(cudaMemcpyAsync(g_stage.yout, yd, bytes, cudaMemcpyDeviceToHost, s));
-  LG_CUDA(cudaStreamSynchronize(s));
-  par_copy(y_h, g_stage.yout, n);
+  if (a->nlong) {
+    int rc0 = ensure_long_ws(g_host_ws.ws, a);
+    if (rc0) return rc0;
+  }
+  if (!g_host_ws.ready()) return fail(LG_ECUDA, "lg_spmv_host: stream / event setup");
+  // x: host copy of chunk c+1 overlaps the DMA of chunk c
+  const int kx = pipe ? 4 : 1;
+  const int64_t cx = (n + kx - 1) / kx;
+  for (int c = 0; c < kx; ++c) {
+    const int64_t lo = c * cx, hi = std::min(n, lo + cx);
+    if (lo >= hi) break;
+    par_copy(g_stage.xin + lo, x_h + lo, hi - lo);
+    LG_CUDA(cudaMemcpyAsync(xd + lo, g_stage.xin + lo, 8 * (size_t)(hi - lo),
+                            cudaMemcpyHostToDevice, s));
+  }
+  // y: the product runs in row chunks; each chunk's D2H (second stream)
+  // overlaps the next chunk's product, and the host copy of chunk c overlaps
+  // the DMA of chunk c+1
+  static const bool pipe = [] {
+    const char* e = getenv("LG_HOST_PIPE");   // 0: one product, one D2H
+    return !(e && atoi(e) == 0);
+  }();
+  const bool chunked = pipe && a->nchunks > 1;
+  const int nc = chunked ? a->nchunks : 1;
+  for (int c = 0; c < nc; ++c) {
+    const int64_t b0 = chunked ? a->chunk_b[c] : 0;
+    const int64_t b1 = chunked ? a->chunk_b[c + 1] : a->nblocks;
+    const int64_t r0 = chunked ? a->chunk_row[c] : 0;
+    const int64_t r1 = chunked ? a->chunk_row[c + 1] : n;
+    int rc = spmv_range(a, xd, yd, b0, b1, g_host_ws.ws, s);
+    if (rc) return rc;
+    LG_CUDA(cudaEventRecord(g_host_ws.done[c], s));
+    LG_CUDA(cudaStreamWaitEvent(g_host_ws.d2h, g_host_ws.done[c], 0));
+    if (r1 > r0)
+      LG_CUDA(cudaMemcpyAsync(g_stage.yout + r0, yd + r0, 8 * (size_t)(r1 - r0),
+                              cudaMemcpyDeviceToHost, g_host_ws.d2h));
+    LG_CUDA(cudaEventRecord(g_host_ws.copied[c], g_host_ws.d2h));
+  }
+  for (int c = 0; c < nc; ++c) {
+    const int64_t r0 = chunked ? a->chunk_row[c] : 0;
+    const int64_t r1 = chunked ? a->chunk_row[c + 1] : n;
+    LG_CUDA(cudaEventSynchronize(g_host_ws.copied[c]));
+    if (r1 > r0) par_copy(y_h + r0, g_stage.yout + r0, r1 - r0);
+  }
+  // the caller's stream is ordered after the copies (xd / yd reuse)
+  LG_CUDA(cudaStreamWaitEvent(s, g_host_ws.copied[nc - 1], 0));
   return LG_OK;
 }
 
@@ -1022,6 +1134,7 @@ extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
   std::vector<int64_t> lfirst;
   build_schedule(n, prp.data(), blocks, lnp, lfirst);
   a->nblocks = (int64_t)blocks.size();
+  set_chunks(a, blocks);
   a->nlong = (int64_t)lnp.size();
   for (int32_t v : lnp) a->nparts += v;
   if ((a->nblocks &&
@@ -1074,6 +1187,7 @@ extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr*
   b->nvals = a->nvals;
   b->noff = m;
   b->nblocks = (int64_t)blocks.size();
+  set_chunks(b, blocks);
   b->nlong = (int64_t)lnp.size();
   for (int32_t v : lnp) b->nparts += v;
   bool ok = cudaMalloc(&b->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
