@@ -124,3 +124,42 @@ def test_row_partitioned_jd(world, prec):
     _, res = rayleigh_residuals(a, pairs.vectors)
     assert np.max(res) <= 1.5 * delta
     assert pairs.gram_defect() <= 1e-8 and pairs.kernel_overlap() <= 1e-8
+
+
+def test_row_partitioned_dacg_device_only_matrix():
+    """A device-only matrix (the C5 pipeline at scale 14): each rank cuts its
+    row block on the device, Jacobi preconditioner; same pairs as the
+    single-GPU solve."""
+    import torch
+
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.dist import RowComm, RowPartition, ThreadWorld, matrix_row_ptr
+    from paper_1311_1695_b200.precond import JacobiFactor
+    A = rmat_laplacian_device(14, 8, seed=3)
+    f = JacobiFactor(A)
+    delta = 1e-8
+    ref, _ = L.dacg_smallest(A, 3, delta=delta, f=f, seed=0)
+    world = 2
+    tw = ThreadWorld(world)
+    part = RowPartition(matrix_row_ptr(A), world)
+    out, errs = [None] * world, []
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = L.dacg_smallest(A, 3, delta=delta, f=f, seed=0, comm=RowComm(part, r, tw))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            tw.bar.abort()
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    if errs:
+        raise errs[0]
+    pairs, _ = out[0]
+    assert np.array_equal(pairs.values, out[1][0].values)
+    assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-8
