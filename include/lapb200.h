@@ -135,6 +135,18 @@ int lg_lcc_device(int64_t n, int64_t m, int32_t** d_i, int32_t** d_j,
  * write y there); columns keep the global numbering, so each rank's slice of
  * an n-vector is exchanged in place. */
 int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** out);
+/* Interior / exterior split of a packed row block [r0, r1) (square
+ * partition): *inner holds the columns in [r0, r1) and the diagonal, *outer
+ * every other column and no diagonal; both are n x n with the other rows
+ * absent.  y = inner x can run while the other ranks' slices of x are still
+ * being exchanged; lg_spmv_acc(outer) then adds the rest.  (SURVEY 8(e):
+ * interior SpMV overlapped with the halo transfer; no reference
+ * counterpart.) */
+int lg_csr_split_cols(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** inner,
+                      lg_csr** outer);
+/* y += A x, no epilogue (the exterior half of a split row block). */
+int lg_spmv_acc(const lg_csr* a, const double* x, double* y, lg_ws* ws, const int* skip,
+                void* stream);
 /* Stream row pointers (packed: off-diagonal; plain: row_ptr), n + 1 int64. */
 int lg_csr_row_ptr(const lg_csr* a, int64_t* host_out);
 /* Unit-weight Laplacian of a canonical device edge list, built directly in

@@ -114,6 +114,8 @@ _SIGS = {
     "lg_fused": (c_int, [c_p, c_p, c_p]),
     "lg_csr_row_block": (c_int, [c_p, c_i64, c_i64, c_p]),
     "lg_csr_row_ptr": (c_int, [c_p, c_p]),
+    "lg_csr_split_cols": (c_int, [c_p, c_i64, c_i64, c_p, c_p]),
+    "lg_spmv_acc": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p]),
     "lg_fused_prog": (c_int, [c_p, c_p, c_p, c_p, c_int, c_p, c_int, c_p, c_p]),
     "lg_gemm_small": (c_int, [c_i64, c_p, c_i64, c_int, c_p, c_int, c_p, c_i64, c_p]),
     "lg_scalar_prog": (c_int, [c_p, c_p, c_p, c_int, c_p, c_int, c_p, c_p]),

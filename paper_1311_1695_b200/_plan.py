@@ -433,6 +433,50 @@ class Exchange:
         self.comm.exchange_(self.x)
 
 
+class ExchangeStart:
+    """Issue the slice exchange of x (completed by the paired ExchangeWait);
+    work launched in between overlaps the transfer."""
+
+    def __init__(self, comm, x):
+        self.comm, self.x, self.reqs = comm, x, None
+
+    def __call__(self, ws=None, stream=None):
+        self.reqs = self.comm.exchange_start(self.x)
+
+
+class ExchangeWait:
+    def __init__(self, start):
+        self.start = start
+
+    def __call__(self, ws=None, stream=None):
+        self.start.comm.exchange_wait(self.start.reqs)
+        self.start.reqs = None
+
+
+class SplitOp:
+    """A rank's row block as interior (own columns + diagonal) and exterior
+    (every other column) halves (dist.RowComm.solver_operator)."""
+
+    def __init__(self, inner, outer):
+        self.inner, self.outer = inner, outer
+        self.n = inner.n
+
+
+class SpmvAcc:
+    """y += A x (lg_spmv_acc): the exterior half of a split row block."""
+
+    def __init__(self, csr, x, y, skip=None):
+        self.h = csr.handle
+        self.x, self.y = _addr(x), _addr(y)
+        self.skip = skip
+
+    def __call__(self, ws=None, stream=None):
+        ws = ws or dev.workspace()
+        nat.check(nat.load().lg_spmv_acc(self.h, self.x, self.y, ws.handle, self.skip,
+                                         stream if stream is not None else dev.stream_ptr()),
+                  "lg_spmv_acc")
+
+
 class Seq:
     """Launches run in order (one plan entry of a row-partitioned solver)."""
 
@@ -519,8 +563,19 @@ class Ctx:
         if self.comm is None:
             return Spmv(csr, x, y, theta=theta, theta_d=theta_d, theta_neg=theta_neg,
                         dots=dots, q=q, nq=nq, result=result, skip=skip)
-        steps = [Exchange(self.comm, x),
-                 Spmv(csr, x, y, theta=theta, theta_d=theta_d, theta_neg=theta_neg, skip=skip)]
+        if isinstance(csr, SplitOp):
+            # the interior product (own slice of x, diagonal, theta shift)
+            # overlaps the exchange; the exterior product accumulates after it
+            st = ExchangeStart(self.comm, x)
+            steps = [st,
+                     Spmv(csr.inner, x, y, theta=theta, theta_d=theta_d, theta_neg=theta_neg,
+                          skip=skip),
+                     ExchangeWait(st),
+                     SpmvAcc(csr.outer, x, y, skip=skip)]
+        else:
+            steps = [Exchange(self.comm, x),
+                     Spmv(csr, x, y, theta=theta, theta_d=theta_d, theta_neg=theta_neg,
+                          skip=skip)]
         if dots or nq:
             steps.append(self.fused(dots=[(y, d) for d in dots],
                                     blocks=[(q, nq, y)] if nq else (), result=result,

@@ -106,6 +106,7 @@ struct SpmvArgs {
   const int64_t* long_first;
   const double* x;
   double* y;
+  int accum;        // y += A x (the second half of a split row block)
   double theta_h;
   const double* theta_d;
   int theta_neg;
@@ -183,6 +184,7 @@ __device__ __forceinline__ double finish_row(const SpmvArgs& a, int64_t r, doubl
                                              double theta) {
   if constexpr (PACKED) s += a.pdiag[r] * __ldg(a.x + r);
   if (theta != 0.0) s -= theta * __ldg(a.x + r);
+  if (a.accum) s = a.y[r] + s;
   return s;
 }
 
@@ -508,9 +510,10 @@ static int launch(const SpmvArgs& args, lg_ws* ws, cudaStream_t s, bool packed) 
 
 // y = A x over the schedule blocks [b0, b1) only (a row chunk; no epilogue).
 static int spmv_range(const lg_csr* a, const double* x, double* y, int64_t b0, int64_t b1,
-                      lg_ws* ws, cudaStream_t s) {
+                      lg_ws* ws, cudaStream_t s, int accum = 0) {
   if (b1 <= b0) return LG_OK;
   SpmvArgs args{};
+  args.accum = accum;
   args.n = a->n;
   args.row_ptr = a->packed ? a->prp : a->row_ptr;
   args.col = a->col;
@@ -1221,6 +1224,213 @@ extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr*
   *out = b;
   return LG_OK;
 }
+
+}  // extern "C"
+
+// ---- interior / exterior split of a row block (overlapped exchange) -------
+// Rank r's row block [r0, r1) splits by column into the interior part
+// (columns in [r0, r1), with the diagonal: only the rank's own slice of x)
+// and the exterior part (every other column, no diagonal).  The interior
+// product runs while the slices of x are exchanged; the exterior product
+// then accumulates into y (lg_spmv_acc).  Both stay in the packed format.
+namespace {
+__global__ void split_count(int64_t r0, int64_t r1, const int64_t* prp, const uint32_t* pcol,
+                            uint32_t cmask, int64_t* cin, int64_t* cout) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += st) {
+    int64_t ni = 0;
+    for (int64_t k = prp[r]; k < prp[r + 1]; ++k) {
+      const int64_t c = pcol[k] & cmask;
+      ni += (c >= r0 && c < r1);
+    }
+    cin[r - r0] = ni;
+    cout[r - r0] = (prp[r + 1] - prp[r]) - ni;
+  }
+}
+__global__ void split_scatter(int64_t r0, int64_t r1, const int64_t* prp, const uint32_t* pcol,
+                              uint32_t cmask, const int64_t* oin, const int64_t* oout,
+                              uint32_t* win, uint32_t* wout) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += st) {
+    int64_t pi = oin[r - r0], po = oout[r - r0];
+    for (int64_t k = prp[r]; k < prp[r + 1]; ++k) {
+      const uint32_t w = pcol[k];
+      const int64_t c = w & cmask;
+      if (c >= r0 && c < r1) win[pi++] = w;
+      else wout[po++] = w;
+    }
+  }
+}
+}  // namespace
+
+// one packed n x n operator holding rows [r0, r1) with the given per-row
+// counts (host) and words (device, already placed)
+static int make_part(const lg_csr* a, int64_t r0, int64_t r1, const std::vector<int64_t>& cnt,
+                     uint32_t* words, int64_t m, bool with_diag, lg_csr** out) {
+  const int64_t n = a->n, nloc = r1 - r0;
+  std::vector<int64_t> prp((size_t)n + 1, 0);
+  for (int64_t i = 0; i < nloc; ++i) prp[(size_t)(r0 + i + 1)] = prp[(size_t)(r0 + i)] + cnt[(size_t)i];
+  for (int64_t r = r1 + 1; r <= n; ++r) prp[(size_t)r] = prp[(size_t)r1];
+  std::vector<char> absent((size_t)n, 1);
+  for (int64_t r = r0; r < r1; ++r) absent[(size_t)r] = 0;
+  std::vector<SpmvBlock> blocks;
+  std::vector<int32_t> lnp;
+  std::vector<int64_t> lfirst;
+  build_schedule(n, prp.data(), blocks, lnp, lfirst, &absent);
+  lg_csr* b = new lg_csr();
+  b->n = n;
+  b->nnz = m + (with_diag ? nloc : 0);
+  b->packed = 1;
+  b->cbits = a->cbits;
+  b->nvals = a->nvals;
+  b->noff = m;
+  b->pcol = words;
+  b->nblocks = (int64_t)blocks.size();
+  set_chunks(b, blocks);
+  b->nlong = (int64_t)lnp.size();
+  for (int32_t v : lnp) b->nparts += v;
+  bool ok = cudaMalloc(&b->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
+            cudaMalloc(&b->pdiag, 8 * (size_t)n) == cudaSuccess &&
+            (b->nvals == 0 || cudaMalloc(&b->table, 8 * (size_t)b->nvals) == cudaSuccess) &&
+            (b->nblocks == 0 ||
+             cudaMalloc(&b->blocks, sizeof(SpmvBlock) * (size_t)b->nblocks) == cudaSuccess) &&
+            (b->nlong == 0 || (cudaMalloc(&b->long_nparts, 4 * (size_t)b->nlong) == cudaSuccess &&
+                               cudaMalloc(&b->long_first, 8 * (size_t)b->nlong) == cudaSuccess));
+  if (!ok) {
+    lg_csr_destroy(b);
+    return fail(LG_ENOMEM, "lg_csr_split_cols: allocation failed");
+  }
+  cudaMemcpy(b->prp, prp.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice);
+  cudaMemset(b->pdiag, 0, 8 * (size_t)n);
+  if (with_diag)
+    cudaMemcpy(b->pdiag + r0, a->pdiag + r0, 8 * (size_t)nloc, cudaMemcpyDeviceToDevice);
+  if (b->nvals) cudaMemcpy(b->table, a->table, 8 * (size_t)b->nvals, cudaMemcpyDeviceToDevice);
+  if (b->nblocks)
+    cudaMemcpy(b->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
+  if (b->nlong) {
+    cudaMemcpy(b->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(b->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
+  }
+  *out = b;
+  return LG_OK;
+}
+
+extern "C" int lg_csr_split_cols(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** inner,
+                                 lg_csr** outer) {
+  if (!a || !inner || !outer || r0 < 0 || r1 < r0 || r1 > a->n)
+    return fail(LG_EINVAL, "lg_csr_split_cols: bad argument");
+  if (!a->packed) return fail(LG_EINVAL, "lg_csr_split_cols: only for packed matrices");
+  const int64_t nloc = r1 - r0;
+  const uint32_t cmask = (a->cbits >= 32) ? 0xffffffffu : ((1u << a->cbits) - 1u);
+  int64_t *cin = nullptr, *cout = nullptr, *oin = nullptr, *oout = nullptr;
+  void* tmp = nullptr;
+  uint32_t *win = nullptr, *wout = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(cin);
+    cudaFree(cout);
+    cudaFree(oin);
+    cudaFree(oout);
+    cudaFree(tmp);
+  };
+  const size_t nb = 8 * (size_t)std::max<int64_t>(nloc, 1);
+  if (cudaMalloc(&cin, nb) != cudaSuccess || cudaMalloc(&cout, nb) != cudaSuccess ||
+      cudaMalloc(&oin, nb) != cudaSuccess || cudaMalloc(&oout, nb) != cudaSuccess) {
+    cleanup();
+    return fail(LG_ENOMEM, "lg_csr_split_cols: allocation failed");
+  }
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nloc + 255) / 256,
+                                                             (int64_t)dev_info().sm_count * 16));
+  if (nloc) split_count<<<g, 256>>>(r0, r1, a->prp, a->pcol, cmask, cin, cout);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cin, oin, std::max<int64_t>(nloc, 1));
+  if (cudaMalloc(&tmp, std::max<size_t>(tb, 16)) != cudaSuccess) {
+    cleanup();
+    return fail(LG_ENOMEM, "lg_csr_split_cols: scan scratch");
+  }
+  std::vector<int64_t> hin((size_t)nloc), hout((size_t)nloc);
+  int64_t mi = 0, mo = 0;
+  if (nloc) {
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cin, oin, nloc);
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cout, oout, nloc);
+    cudaMemcpy(hin.data(), cin, 8 * (size_t)nloc, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hout.data(), cout, 8 * (size_t)nloc, cudaMemcpyDeviceToHost);
+    for (int64_t i = 0; i < nloc; ++i) {
+      mi += hin[(size_t)i];
+      mo += hout[(size_t)i];
+    }
+  }
+  if (cudaMalloc(&win, 4 * (size_t)std::max<int64_t>(mi, 1)) != cudaSuccess ||
+      cudaMalloc(&wout, 4 * (size_t)std::max<int64_t>(mo, 1)) != cudaSuccess) {
+    cudaFree(win);
+    cleanup();
+    return fail(LG_ENOMEM, "lg_csr_split_cols: allocation failed");
+  }
+  if (nloc) split_scatter<<<g, 256>>>(r0, r1, a->prp, a->pcol, cmask, oin, oout, win, wout);
+  cudaError_t e = cudaDeviceSynchronize();
+  cleanup();
+  if (e != cudaSuccess) {
+    cudaFree(win);
+    cudaFree(wout);
+    return fail(LG_ECUDA, std::string("lg_csr_split_cols: ") + cudaGetErrorString(e));
+  }
+  lg_csr *bi = nullptr, *bo = nullptr;
+  int rc = make_part(a, r0, r1, hin, win, mi, true, &bi);
+  if (rc) {
+    cudaFree(win);
+    cudaFree(wout);
+    return rc;
+  }
+  rc = make_part(a, r0, r1, hout, wout, mo, false, &bo);
+  if (rc) {
+    lg_csr_destroy(bi);
+    cudaFree(wout);
+    return rc;
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    lg_csr_destroy(bi);
+    lg_csr_destroy(bo);
+    return fail(LG_ECUDA, std::string("lg_csr_split_cols: ") + cudaGetErrorString(e));
+  }
+  *inner = bi;
+  *outer = bo;
+  return LG_OK;
+}
+
+// y += A x (no epilogue): the exterior half of a split row block.
+extern "C" int lg_spmv_acc(const lg_csr* a, const double* x, double* y, lg_ws* ws,
+                           const int* skip, void* stream) {
+  if (!a || !x || !y || !ws) return fail(LG_EINVAL, "lg_spmv_acc: NULL argument");
+  if (a->n == 0 || a->nblocks == 0) return LG_OK;
+  if (a->nlong) {
+    int rc = ensure_long_ws(ws, a);
+    if (rc) return rc;
+  }
+  SpmvArgs args{};
+  args.accum = 1;
+  args.n = a->n;
+  args.row_ptr = a->packed ? a->prp : a->row_ptr;
+  args.col = a->col;
+  args.val = a->val;
+  args.pcol = a->packed ? a->pcol : nullptr;
+  args.pdiag = a->pdiag;
+  args.table = a->table;
+  args.nvals = a->nvals;
+  args.cbits = a->cbits;
+  args.blocks = a->blocks;
+  args.nblocks = a->nblocks;
+  args.long_nparts = a->long_nparts;
+  args.long_first = a->long_first;
+  args.x = x;
+  args.y = y;
+  args.skip = skip;
+  args.long_part = ws->long_part;
+  args.long_ticket = ws->long_ticket;
+  args.nlong = a->nlong;
+  return launch<0>(args, ws, (cudaStream_t)stream, a->packed != 0);
+}
+
+extern "C" {
 
 // Stream row pointers of a matrix (packed: off-diagonal row pointers; plain:
 // row_ptr) to the host, n + 1 entries -- what the nnz-balanced row

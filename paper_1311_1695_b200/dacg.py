@@ -168,7 +168,7 @@ class _DacgPlan:
         self.n = n
         self.cx = Ctx(n, comm)
         if self.cx.dist:
-            self.csr = self.cx.comm.local_operator(a)
+            self.csr = self.cx.comm.solver_operator(a)
             self.prec = self.cx.comm.local_preconditioner(a, f)
         else:
             self.csr = device_csr(a)

@@ -131,6 +131,27 @@ class TorchBackend:
     def exchange_(self, x, comm):
         SliceExchange(self.dist, comm.part, comm.rank)(x)
 
+    def exchange_start(self, x, comm):
+        """Issue the slice exchange; returns the requests to wait on (NCCL
+        runs it on its own stream, after the work already queued on the
+        current stream)."""
+        d, part, me = self.dist, comm.part, comm.rank
+        r0, r1 = part.rows(me)
+        ops = []
+        for p in range(part.world):
+            if p == me:
+                continue
+            q0, q1 = part.rows(p)
+            if r1 > r0:
+                ops.append(d.P2POp(d.isend, x[r0:r1], p))
+            if q1 > q0:
+                ops.append(d.P2POp(d.irecv, x[q0:q1], p))
+        return d.batch_isend_irecv(ops) if ops else []
+
+    def exchange_wait(self, reqs, comm):
+        for r in reqs:
+            r.wait()
+
     def barrier(self, comm):
         self.dist.barrier()
 
@@ -174,6 +195,13 @@ class ThreadWorld:
         self._sync()
         self.bar.wait()
 
+    def exchange_start(self, x, comm):
+        self.exchange_(x, comm)
+        return None
+
+    def exchange_wait(self, reqs, comm):
+        pass
+
     def barrier(self, comm):
         self._sync()
         self.bar.wait()
@@ -214,6 +242,30 @@ class RowComm:
         if self.world > 1:
             self.backend.barrier(self)
 
+    def exchange_start(self, x):
+        return self.backend.exchange_start(x, self) if self.world > 1 else None
+
+    def exchange_wait(self, reqs):
+        if self.world > 1:
+            self.backend.exchange_wait(reqs, self)
+
+    def split_operator(self, a):
+        """(inner, outer) halves of this rank's row block (lg_csr_split_cols):
+        inner reads only the rank's own slice of x (and holds the diagonal),
+        outer every other column; None when the block is not packed."""
+        op = self.local_operator(a)
+        if not op.packed:
+            return None
+        return split_cols(op, self.r0, self.r1)
+
+    def solver_operator(self, a):
+        """The operator a row-partitioned solver multiplies by: the split
+        row block (interior product overlapped with the exchange) when it
+        packs, else the plain row block."""
+        from ._plan import SplitOp
+        sp = self.split_operator(a)
+        return SplitOp(*sp) if sp is not None else self.local_operator(a)
+
     def local_operator(self, a):
         """This rank's row block of `a` (host CsrMatrix or device-only)."""
         if hasattr(a, "row_ptr") and getattr(a, "col_idx", None) is not None:
@@ -244,6 +296,23 @@ class RowComm:
         raise ValueError("row-partitioned solves take a JacobiFactor, 'jacobi' or "
                          "'block_ic0' as preconditioner (the natural-order IC(0) sweeps "
                          "do not shard, SURVEY 8(e))")
+
+
+def split_cols(dmat, r0, r1):
+    """Interior / exterior halves of a packed row-block operator."""
+    import ctypes
+
+    from . import _native as nat
+    from .sparse import DeviceCsr
+    hi, ho = ctypes.c_void_p(), ctypes.c_void_p()
+    nat.call("lg_csr_split_cols", dmat.handle, int(r0), int(r1), ctypes.byref(hi),
+             ctypes.byref(ho))
+    out = []
+    for h in (hi, ho):
+        info = [ctypes.c_int64() for _ in range(4)] + [ctypes.c_int(), ctypes.c_int64()]
+        nat.call("lg_csr_info", h, *[ctypes.byref(v) for v in info])
+        out.append(DeviceCsr.from_handle(h, dmat.n, info[1].value))
+    return tuple(out)
 
 
 def matrix_row_ptr(a):

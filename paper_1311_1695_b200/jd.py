@@ -224,7 +224,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
     draws = NormalStream(rng, n)
     cx = Ctx(n, comm)
     if dist:
-        csr = comm.local_operator(a)
+        csr = comm.solver_operator(a)
         prec = comm.local_preconditioner(a, f)
     else:
         csr = device_csr(a)

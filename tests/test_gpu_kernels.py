@@ -476,3 +476,41 @@ def test_spmv_host_buffers_cabi_and_public():
     assert np.array_equal(y2, want)
     yr = O.spmv(O.Csr(a.n, a.row_ptr, a.col_idx, a.values), x)
     assert np.max(np.abs(y2 - yr)) <= 1e-13 * np.max(np.abs(yr))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_row_block_interior_exterior(world):
+    """lg_csr_split_cols: a rank's row block = interior (own columns +
+    diagonal) + exterior (every other column); inner product then
+    lg_spmv_acc of the exterior equals the full product on the rank's rows
+    (to roundoff: the two halves are summed separately) and leaves every
+    other row untouched.  Host-built and device-built matrices."""
+    import torch
+
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200._plan import SpmvAcc
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.dist import (RowPartition, local_operator_device, matrix_row_ptr,
+                                           split_cols)
+    g, _ = L.largest_component(L.generators.chung_lu_graph(20000, 2.1, 8.0, max_degree=4000,
+                                                           weighted=True, seed=11))
+    for A in (L.build_laplacian(g), rmat_laplacian_device(13, 8, seed=2)):
+        full = A.device()
+        n = A.n
+        x = dev.to_device(np.random.default_rng(5).standard_normal(n))
+        want = dev.empty(n)
+        full.matvec(x, want)
+        part = RowPartition(matrix_row_ptr(A), world)
+        for r in range(world):
+            r0, r1 = part.rows(r)
+            op = local_operator_device(full, part, r)
+            inner, outer = split_cols(op, r0, r1)
+            assert inner.packed and outer.packed
+            y = torch.full((n,), 777.0, dtype=torch.float64, device="cuda")
+            inner.matvec(x, y)
+            SpmvAcc(outer, x, y)()
+            torch.cuda.synchronize()
+            assert torch.all(y[:r0] == 777.0) and torch.all(y[r1:] == 777.0)
+            err = (y[r0:r1] - want[r0:r1]).abs().max().item()
+            assert err <= 1e-12 * max(1.0, want.abs().max().item())
