@@ -151,6 +151,13 @@ def _comm_worker(rank, world, port, q):
         x[comm.r0:comm.r1] = torch.from_numpy(x_full[comm.r0:comm.r1])
         comm.exchange_(x)
         ok_x = np.array_equal(x.numpy(), x_full)
+        # the split (overlapped) form: issue, work on the own slice, wait
+        x2 = torch.full((n,), np.nan, dtype=torch.float64)
+        x2[comm.r0:comm.r1] = torch.from_numpy(x_full[comm.r0:comm.r1])
+        reqs = comm.exchange_start(x2)
+        own = float(x2[comm.r0:comm.r1].sum())          # interior work meanwhile
+        comm.exchange_wait(reqs)
+        ok_x = ok_x and np.array_equal(x2.numpy(), x_full) and np.isfinite(own)
         q.put((rank, ok_red, ok_x, comm.r0, comm.r1))
     finally:
         dist.destroy_process_group()
