@@ -37,16 +37,17 @@
 
 namespace lg {
 
-#ifndef LG_SPMV_THREADS
-#define LG_SPMV_THREADS 128
-#endif
-constexpr int kST = LG_SPMV_THREADS;       // CTA size of the SpMV
-constexpr int kSW = kST / 32;
-constexpr int kChunk = kST * 8;            // nonzeros per row block
+// The CTA size T is chosen per matrix (128 or 256 threads, lg_csr.cta); a
+// row block holds at most T * kPer nonzeros, so the schedule depends on it.
+// 256 pays on very large matrices (C5: rows of 1-2 K nonzeros stay in one
+// block instead of becoming ticketed long-row parts; 15.1 -> 13.0 ms), 128
+// on the rest (C3: 32.8 vs 34.8 us, C4 equal).
+constexpr int kPer = 8;        // stream words per thread per block
+constexpr int kST = 128;       // default CTA size (and of the build kernels)
 constexpr int kRowCap = 1024;  // rows per normal block
 constexpr int kShortRow = 32;  // rows up to this length: one thread each
 #ifndef LG_SPMV_MINB
-#define LG_SPMV_MINB 12
+#define LG_SPMV_MINB 12   // resident 128-thread CTAs per SM (register bound)
 #endif
 
 struct SpmvBlock {
@@ -81,6 +82,7 @@ struct lg_csr {
   int64_t* long_first = nullptr;   // device [nlong] slot of part 0
   // row chunks of the schedule for the host-buffer path (lg_spmv_host):
   // blocks [chunk_b[c], chunk_b[c+1]) cover rows [chunk_row[c], chunk_row[c+1])
+  int cta = 128;                   // CTA size the schedule was cut for
   int nchunks = 0;
   int64_t chunk_b[9] = {};
   int64_t chunk_row[9] = {};
@@ -138,7 +140,6 @@ __device__ __forceinline__ void epilogue_row(const SpmvArgs& a, int64_t r,
   }
 }
 
-constexpr int kPer = kChunk / kST;  // stream words per thread per block
 
 // Stream words of one block held in registers: issued one block ahead so the
 // DRAM latency of the column / value stream overlaps the current block's
@@ -149,13 +150,13 @@ struct Staged {
   double v[PACKED ? 1 : kPer];      // plain: values
 };
 
-template <bool PACKED>
+template <bool PACKED, int T>
 __device__ __forceinline__ void stage(const SpmvArgs& a, const SpmvBlock& blk, int tid,
                                       Staged<PACKED>& st) {
   const int cnt = (int)(blk.nz1 - blk.nz0);
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
-    const int e = tid + j * kST;
+    const int e = tid + j * T;
     if (e < cnt) {
       const int64_t k = blk.nz0 + e;
       if constexpr (PACKED) {
@@ -188,9 +189,13 @@ __device__ __forceinline__ double finish_row(const SpmvArgs& a, int64_t r, doubl
   return s;
 }
 
-template <int NA, bool PACKED>
-__global__ void __launch_bounds__(kST, (NA <= 4 ? LG_SPMV_MINB : (NA <= 16 ? 8 : 2)))
+template <int NA, bool PACKED, int T>
+__global__ void __launch_bounds__(T, (NA <= 4 ? LG_SPMV_MINB * 128 / T
+                                              : (NA <= 16 ? 1024 / T : 256 / T)))
 spmv_kernel(SpmvArgs a, lg_ws ws) {
+  constexpr int kST = T;
+  constexpr int kSW = T / 32;
+  constexpr int kChunk = T * kPer;
   if (a.skip && *a.skip) return;
   __shared__ double sm[kChunk];
   extern __shared__ double tab_sm[];   // packed value table (nvals)
@@ -217,7 +222,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
   }
   SpmvBlock blk = a.blocks[b];
   Staged<PACKED> cur;
-  stage<PACKED>(a, blk, tid, cur);
+  stage<PACKED, T>(a, blk, tid, cur);
 
   while (b < a.nblocks) {
     const int64_t bn = b + gridDim.x;
@@ -238,7 +243,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
         hi0 = (int)(a.row_ptr[blk.row0 + tid + 1] - blk.nz0);
       }
       Staged<PACKED> nxt;
-      if (bn < a.nblocks) stage<PACKED>(a, nblk, tid, nxt);
+      if (bn < a.nblocks) stage<PACKED, T>(a, nblk, tid, nxt);
       __syncthreads();
       // phase A: one thread per row for rows of at most kShortRow entries;
       // longer rows are compacted (in row order, via ballots) into a list
@@ -302,7 +307,7 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
         if (e < cnt) s += product<PACKED>(a, cur, j, tab_sm, cmask);
       }
       Staged<PACKED> nxt;
-      if (bn < a.nblocks) stage<PACKED>(a, nblk, tid, nxt);
+      if (bn < a.nblocks) stage<PACKED, T>(a, nblk, tid, nxt);
       s = warp_sum(s);
       if ((tid & 31) == 0) sm[tid >> 5] = s;
       __syncthreads();
@@ -366,11 +371,13 @@ spmv_kernel(SpmvArgs a, lg_ws ws) {
 // absent (optional): rows with no stored entry that are left out of the
 // schedule altogether (y is not written there) -- the row block of one rank
 // in the row-partitioned multi-GPU SpMV, embedded in the global index space.
-static void build_schedule(int64_t n, const int64_t* rp,
+static void build_schedule(int64_t n, const int64_t* rp, int cta,
                            std::vector<SpmvBlock>& blocks,
                            std::vector<int32_t>& long_nparts,
                            std::vector<int64_t>& long_first,
                            const std::vector<char>* absent = nullptr) {
+  const int kChunk = cta * kPer;
+  const int kST = cta;
   int64_t r = 0, part_total = 0;
   while (r < n) {
     if (absent && (*absent)[(size_t)r]) {
@@ -476,14 +483,14 @@ static int ensure_long_ws(lg_ws* ws, const lg_csr* a) {
   return LG_OK;
 }
 
-template <int NA, bool PACKED>
+template <int NA, bool PACKED, int T>
 static int grid_for(size_t dyn) {
   static thread_local size_t last_dyn = (size_t)-1;
   static thread_local int occ = 1;
   if (dyn != last_dyn) {
     int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, spmv_kernel<NA, PACKED>,
-                                                      kST, dyn) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, spmv_kernel<NA, PACKED, T>,
+                                                      T, dyn) != cudaSuccess ||
         o < 1)
       o = 1;
     occ = o;
@@ -492,20 +499,34 @@ static int grid_for(size_t dyn) {
   return occ * dev_info().sm_count;
 }
 
-template <int NA, bool PACKED>
+template <int NA, bool PACKED, int T>
 static int launch_t(const SpmvArgs& args, lg_ws* ws, cudaStream_t s) {
   const size_t dyn = PACKED ? sizeof(double) * (size_t)args.nvals : 0;
-  int64_t g = std::min<int64_t>(args.nblocks, grid_for<NA, PACKED>(dyn));
+  int64_t g = std::min<int64_t>(args.nblocks, grid_for<NA, PACKED, T>(dyn));
   if (NA > 0) g = std::min<int64_t>(g, kMaxRedBlocks);
   if (g < 1) g = 1;
-  spmv_kernel<NA, PACKED><<<(unsigned)g, kST, dyn, s>>>(args, *ws);
+  spmv_kernel<NA, PACKED, T><<<(unsigned)g, T, dyn, s>>>(args, *ws);
   LG_LAUNCH_CHECK("spmv_kernel");
   return LG_OK;
 }
 
+// NA > 0 (fused epilogue, LG_SPMV_EPILOGUE=1) is instantiated for 128-thread
+// schedules only; lg_spmv routes 256-thread matrices through the separate
+// epilogue pass.
 template <int NA>
-static int launch(const SpmvArgs& args, lg_ws* ws, cudaStream_t s, bool packed) {
-  return packed ? launch_t<NA, true>(args, ws, s) : launch_t<NA, false>(args, ws, s);
+static int launch(const SpmvArgs& args, lg_ws* ws, cudaStream_t s, bool packed, int cta) {
+  if constexpr (NA == 0) {
+    if (cta == 256)
+      return packed ? launch_t<0, true, 256>(args, ws, s) : launch_t<0, false, 256>(args, ws, s);
+  }
+  return packed ? launch_t<NA, true, 128>(args, ws, s) : launch_t<NA, false, 128>(args, ws, s);
+}
+
+// CTA size of a matrix's schedule (LG_SPMV_CTA overrides: 128 or 256).
+static int pick_cta(int64_t noff) {
+  const char* e = getenv("LG_SPMV_CTA");
+  if (e && (atoi(e) == 128 || atoi(e) == 256)) return atoi(e);
+  return noff >= ((int64_t)1 << 27) ? 256 : 128;
 }
 
 // y = A x over the schedule blocks [b0, b1) only (a row chunk; no epilogue).
@@ -532,7 +553,7 @@ static int spmv_range(const lg_csr* a, const double* x, double* y, int64_t b0, i
   args.long_part = ws->long_part;
   args.long_ticket = ws->long_ticket;
   args.nlong = a->nlong;
-  return launch<0>(args, ws, s, a->packed != 0);
+  return launch<0>(args, ws, s, a->packed != 0, a->cta);
 }
 
 // Packed Laplacian format eligibility: every row stores its diagonal, the
@@ -644,12 +665,14 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
     absent.resize((size_t)n);
     for (int64_t r = 0; r < n; ++r) absent[(size_t)r] = rp[r + 1] == rp[r];
   }
-  build_schedule(n, packed ? prp.data() : rp, blocks, lnp, lfirst,
+  const int cta = pick_cta(packed ? (int64_t)pcol.size() : nnz);
+  build_schedule(n, packed ? prp.data() : rp, cta, blocks, lnp, lfirst,
                  (flags & LG_CSR_SKIP_EMPTY) ? &absent : nullptr);
 
   lg_csr* a = new lg_csr();
   a->n = n;
   a->nnz = nnz;
+  a->cta = cta;
   a->nblocks = (int64_t)blocks.size();
   set_chunks(a, blocks);
   a->nlong = (int64_t)lnp.size();
@@ -816,17 +839,17 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
   cudaStream_t s = (cudaStream_t)stream;
   int na = ndots + nq;
   const bool pk = a->packed != 0;
-  if (na == 0) return launch<0>(args, ws, s, pk);
+  if (na == 0) return launch<0>(args, ws, s, pk, a->cta);
   static const bool fused_epilogue = [] {
     const char* e = getenv("LG_SPMV_EPILOGUE");
     return e && atoi(e) == 1;
   }();
-  if (!fused_epilogue) {
+  if (!fused_epilogue || a->cta != 128) {
     // The gather loop is latency-bound and wants every register for
     // occupancy: the dot / Q^T y epilogue costs less as one streaming pass
     // over y right behind the SpMV (measured on C4: +4-9 us instead of
     // +18-60 us inside the kernel).  Same result layout: dots, then Q^T y.
-    int rc = launch<0>(args, ws, s, pk);
+    int rc = launch<0>(args, ws, s, pk, a->cta);
     if (rc) return rc;
     lg_fused_args f{};
     f.n = a->n;
@@ -846,9 +869,9 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
     f.skip = skip;
     return lg_fused(&f, ws, stream);
   }
-  if (na <= 4) return launch<4>(args, ws, s, pk);
-  if (na <= 16) return launch<16>(args, ws, s, pk);
-  return launch<LG_MAXD + LG_MAXQ>(args, ws, s, pk);
+  if (na <= 4) return launch<4>(args, ws, s, pk, 128);
+  if (na <= 16) return launch<16>(args, ws, s, pk, 128);
+  return launch<LG_MAXD + LG_MAXQ>(args, ws, s, pk, 128);
 }
 
 }  // extern "C"
@@ -1135,7 +1158,8 @@ extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
   std::vector<SpmvBlock> blocks;
   std::vector<int32_t> lnp;
   std::vector<int64_t> lfirst;
-  build_schedule(n, prp.data(), blocks, lnp, lfirst);
+  a->cta = pick_cta(a->noff);
+  build_schedule(n, prp.data(), a->cta, blocks, lnp, lfirst);
   a->nblocks = (int64_t)blocks.size();
   set_chunks(a, blocks);
   a->nlong = (int64_t)lnp.size();
@@ -1180,9 +1204,10 @@ extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr*
   std::vector<SpmvBlock> blocks;
   std::vector<int32_t> lnp;
   std::vector<int64_t> lfirst;
-  build_schedule(n, prp.data(), blocks, lnp, lfirst, &absent);
+  build_schedule(n, prp.data(), a->cta, blocks, lnp, lfirst, &absent);
 
   lg_csr* b = new lg_csr();
+  b->cta = a->cta;
   b->n = n;
   b->nnz = m + nloc;
   b->packed = 1;
@@ -1276,8 +1301,9 @@ static int make_part(const lg_csr* a, int64_t r0, int64_t r1, const std::vector<
   std::vector<SpmvBlock> blocks;
   std::vector<int32_t> lnp;
   std::vector<int64_t> lfirst;
-  build_schedule(n, prp.data(), blocks, lnp, lfirst, &absent);
+  build_schedule(n, prp.data(), a->cta, blocks, lnp, lfirst, &absent);
   lg_csr* b = new lg_csr();
+  b->cta = a->cta;
   b->n = n;
   b->nnz = m + (with_diag ? nloc : 0);
   b->packed = 1;
@@ -1427,7 +1453,7 @@ extern "C" int lg_spmv_acc(const lg_csr* a, const double* x, double* y, lg_ws* w
   args.long_part = ws->long_part;
   args.long_ticket = ws->long_ticket;
   args.nlong = a->nlong;
-  return launch<0>(args, ws, (cudaStream_t)stream, a->packed != 0);
+  return launch<0>(args, ws, (cudaStream_t)stream, a->packed != 0, a->cta);
 }
 
 extern "C" {

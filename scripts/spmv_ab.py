@@ -1,8 +1,8 @@
 """SpMV A/B on the benchmark graphs: device product vs the oracle's
 restatement of the reference SpMV (sparse.py:128-139), and event time per
-matvec with L2 flushed.  Development aid; the kernel variant is picked by the
-environment (LG_SPMV_SEG=0: shared-memory row reduction) so run it once per
-variant.  Prints one JSON line per graph."""
+matvec with L2 flushed.  Development aid; run it once per library variant
+(LG_LIB_OVERRIDE=path/to/variant.so, LG_SPMV_CTA=128|256).  Prints one JSON
+line per graph."""
 import json
 import os
 import sys
@@ -36,7 +36,7 @@ def timed(step, reps=30, flush=True):
 
 def main():
     names = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
-    mode = "smem" if os.environ.get("LG_SPMV_SEG") == "0" else "seg"
+    mode = os.environ.get("LG_LIB_OVERRIDE", "default")
     for name in names:
         if name == "C5":
             from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
