@@ -7,12 +7,16 @@ reductions are deterministic (bitwise equal run to run).
 """
 
 import hashlib
+import os
+from pathlib import Path
 
 import numpy as np
 import pytest
 
 from oracle import lapeig_oracle as O
 from tests.conftest import golden_config, kat_edges
+
+ROOT = Path(__file__).resolve().parent.parent
 
 pytestmark = pytest.mark.gpu
 
@@ -514,3 +518,43 @@ def test_split_row_block_interior_exterior(world):
             assert torch.all(y[:r0] == 777.0) and torch.all(y[r1:] == 777.0)
             err = (y[r0:r1] - want[r0:r1]).abs().max().item()
             assert err <= 1e-12 * max(1.0, want.abs().max().item())
+
+
+def test_spmv_256_thread_schedule_parity():
+    """The 256-thread schedule (chosen for matrices with >= 2^27
+    off-diagonals, forced here with LG_SPMV_CTA=256 in a child process) gives
+    the same products as the oracle on fixtures with empty rows, hub rows
+    longer than one block, weighted values and a row-block operator."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch
+import paper_1311_1695_b200 as L
+from oracle import lapeig_oracle as O
+from paper_1311_1695_b200 import _device as dev
+from paper_1311_1695_b200.dist import RowPartition, local_operator
+rng = np.random.default_rng(7)
+gs = [L.largest_component(L.generators.chung_lu_graph(20000, 2.1, 8.0, max_degree=6000,
+                                                      weighted=True, seed=11))[0],
+      L.generators.star_graph(5000), L.generators.grid_graph(60, 70)]
+for g in gs:
+    a = L.build_laplacian(g)
+    x = rng.standard_normal(a.n)
+    want = O.spmv(O.Csr(a.n, a.row_ptr, a.col_idx, a.values), x)
+    y = L.spmv(a, x)
+    assert np.max(np.abs(y - want)) <= 1e-13 * np.max(np.abs(want)), "spmv"
+    part = RowPartition(a.row_ptr, 2)
+    yd = dev.empty(a.n)
+    full = dev.empty(a.n)
+    a.device().matvec(dev.to_device(x), full)
+    for r in range(2):
+        r0, r1 = part.rows(r)
+        local_operator(a, part, r).matvec(dev.to_device(x), yd)
+        torch.cuda.synchronize()
+        assert torch.equal(yd[r0:r1], full[r0:r1]), "row block"
+print("OK")
+'''
+    env = dict(os.environ, LG_SPMV_CTA="256")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
