@@ -170,6 +170,19 @@ int lg_ic0_factorize(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
                      int nsched, int64_t* l_row_ptr_h, int64_t* l_col_h,
                      double* l_val_h, double* shift, int* attempts);
 
+/* ---- FSAI preconditioner (flagged non-reference variant; the approximate
+ * inverse PAPER.md:704-706 proposes) ----------------
+ * M^{-1} = G^T G, G lower triangular on the lower pattern of A (at most kmax
+ * entries per row, diagonal last; hub rows keep their kmax - 1 largest
+ * |a_ij|), each row from one dense SPD solve A[P_i, P_i] g = e_last scaled by
+ * 1 / sqrt(g_last).  Host setup, OpenMP over rows; the apply is two device
+ * SpMVs (lg_csr of G and of G^T).  lg_fsai_nnz gives the size of G. */
+int lg_fsai_nnz(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h, int kmax,
+                int64_t* nnz);
+int lg_fsai_factorize(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
+                      const double* val_h, int kmax, int64_t* g_row_ptr_h, int64_t* g_col_h,
+                      double* g_val_h);
+
 /* ---- IC(0) apply (ic0.py:40-45) ---------------------------------------- */
 typedef struct lg_ic0 lg_ic0;
 /* Upload the lower factor L (CSR, diagonal last in each row) and build L^T

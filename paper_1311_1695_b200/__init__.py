@@ -34,7 +34,7 @@ from .irlm import irlm_smallest, ncv_for
 from .jd import jd_smallest
 from .kernels import GramSchmidtBreakdown, dense_sym_eig, mgs_orthonormalize, tridiag_eig
 from .pcg import DeflationBasis, PcgOutcome, jd_correction_solve, kernel_basis, pcg_solve
-from .precond import JacobiFactor
+from .precond import FsaiFactor, JacobiFactor, fsai_factorize
 from .results import EigenPairSet, SolverError, SolverReport, rayleigh_residuals
 from .sparse import CsrMatrix, MvpCounter, spmv
 
@@ -42,7 +42,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CsrMatrix", "DeflationBasis", "EdgeList", "EigenPairSet", "GramSchmidtBreakdown",
-    "Ic0Error", "Ic0Factor", "JacobiFactor", "MulticolorIc0Factor", "ic0_factorize_multicolor", "MvpCounter", "PcgOutcome", "SolverError",
+    "FsaiFactor", "fsai_factorize", "Ic0Error", "Ic0Factor", "JacobiFactor", "MulticolorIc0Factor", "ic0_factorize_multicolor", "MvpCounter", "PcgOutcome", "SolverError",
     "SolverReport", "ba_graph", "build_laplacian", "chung_lu_graph", "complete_graph",
     "config_graph", "connected_components", "cycle_graph", "dacg_smallest", "dense_sym_eig",
     "grid_graph", "ic0_factorize", "identity_factor", "irlm_smallest", "jd_correction_solve",

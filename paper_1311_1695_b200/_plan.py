@@ -582,6 +582,14 @@ class Ctx:
                                     skip=skip))
         return Seq(steps)
 
+    def prec_apply(self, prec, r, z, skip=None):
+        """z = M^{-1} r over this rank's rows: a local preconditioner gets the
+        slices; one whose apply needs other ranks' rows (dist.DistFsai)
+        contributes its own launch sequence with the exchanges."""
+        if self.comm is not None and hasattr(prec, "dist_steps"):
+            return Seq(prec.dist_steps(r, z, skip))
+        return PrecApply(prec, self.v(r), self.v(z), skip=skip)
+
     def project(self, c, k, v, out, slots, name=None):
         """out = v - C (C^T v) over this rank's rows (two passes)."""
         name = name or f"_pc{k}"

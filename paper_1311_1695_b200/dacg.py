@@ -353,7 +353,7 @@ class _DacgPlan:
         # scalar programs run in the finishing CTA of the pass whose dots
         # they consume (lg_fused_prog): no launch of their own
         cx = self.cx
-        L.append(PrecApply(self.prec, cx.v(G[c]), cx.v(Z0), skip=stop))
+        L.append(cx.prec_apply(self.prec, G[c], Z0, skip=stop))
         L.append(cx.fused(blocks=[(C, k, Z0)], result=res("cz"), skip=stop))
         # z = z0 - C cz; num = (g - g_prev).z; gz = g.z   (g_prev lives in G[o])
         L.append(cx.fused(outs=[dict(out=Z, terms=[(Z0, 1.0)], upd=(C, k, S.p("cz")))],
@@ -429,8 +429,8 @@ def _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0, comm
         null_basis = kernel_basis(a.n)
     if comm is not None and comm.world == 1 and isinstance(f, str):
         # one rank: block-Jacobi IC(0) with one block is the reference IC(0)
-        from .precond import JacobiFactor
-        f = JacobiFactor(a) if f == "jacobi" else None
+        from .precond import FsaiFactor, JacobiFactor
+        f = {"jacobi": JacobiFactor, "fsai": FsaiFactor}.get(f, lambda _: None)(a)
     if f is None and (comm is None or comm.world == 1):
         f = ic0_factorize(a)
     if neig < 1:

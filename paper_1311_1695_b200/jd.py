@@ -207,8 +207,8 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
     dist = comm is not None and comm.world > 1
     if comm is not None and comm.world == 1 and isinstance(f, str):
         # one rank: block-Jacobi IC(0) with one block is the reference IC(0)
-        from .precond import JacobiFactor
-        f = JacobiFactor(a) if f == "jacobi" else None
+        from .precond import FsaiFactor, JacobiFactor
+        f = {"jacobi": JacobiFactor, "fsai": FsaiFactor}.get(f, lambda _: None)(a)
     if f is None and not dist:
         f = ic0_factorize(a)
     if neig < 1:
@@ -373,7 +373,7 @@ def _jd_smallest_impl(a, neig, delta=1e-6, delta_pcg=1e-2, itmax_inner=20,
             cx.fused(outs=[dict(out=t1, terms=[(t1, -1.0)])])()
             t2 = dev.empty(n)
             if cx.dist:
-                PrecApply(prec, cx.v(t1), cx.v(t2))()
+                cx.prec_apply(prec, t1, t2)()
             else:
                 prec.apply(t1, t2)
             cx.project(B, kg, t2, t0v, qs)

@@ -323,9 +323,9 @@ class DevicePcg:
         if jd and has_q:
             ps.append(cx.fused(outs=[self._upd(dict(out=T, terms=[(R, 1.0)]), "cr")],
                             skip=stop))
-            ps.append(PrecApply(self.prec, cx.v(T), cx.v(Z0), skip=stop))
+            ps.append(cx.prec_apply(self.prec, T, Z0, skip=stop))
         else:
-            ps.append(PrecApply(self.prec, cx.v(R), cx.v(Z0), skip=stop))
+            ps.append(cx.prec_apply(self.prec, R, Z0, skip=stop))
         if has_q:
             ps.append(cx.fused(blocks=self._qdots(Z0), result=self._res("cz1"), skip=stop))
             if jd:

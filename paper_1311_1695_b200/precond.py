@@ -75,6 +75,88 @@ class JacobiFactor:
         return out if on_dev else dev.to_host(out)
 
 
+class FsaiFactor:
+    """Factorized sparse approximate inverse, z = G^T G r (lg_fsai.cu).
+
+    A flagged NON-reference variant: the approximate inverse the paper
+    proposes as the parallel-friendly alternative (SURVEY
+    8(f) item 3).  G is lower triangular on the lower pattern of A with at
+    most kmax entries per row (hub rows keep their kmax - 1 largest |a_ij|);
+    the apply is two SpMVs -- no triangular dependency chain, and across GPUs
+    two row-partitioned SpMVs without the block-Jacobi loss.  Same .apply
+    seam as Ic0Factor.  The scratch vector makes one factor usable by one
+    stream at a time.
+    """
+
+    def __init__(self, a, kmax=64):
+        import ctypes
+
+        from .sparse import CsrMatrix, DeviceCsr
+        n = int(a.n)
+        rp = np.ascontiguousarray(a.row_ptr, dtype=np.int64)
+        col = np.ascontiguousarray(a.col_idx, dtype=np.int64)
+        val = np.ascontiguousarray(a.values, dtype=np.float64)
+        nnz = ctypes.c_int64()
+        nat.call("lg_fsai_nnz", n, rp.ctypes.data, col.ctypes.data if col.size else None,
+                 int(kmax), ctypes.byref(nnz))
+        grp = np.zeros(n + 1, dtype=np.int64)
+        gcol = np.zeros(max(nnz.value, 1), dtype=np.int64)
+        gval = np.zeros(max(nnz.value, 1), dtype=np.float64)
+        nat.call("lg_fsai_factorize", n, rp.ctypes.data, col.ctypes.data if col.size else None,
+                 val.ctypes.data if val.size else None, int(kmax), grp.ctypes.data,
+                 gcol.ctypes.data, gval.ctypes.data)
+        gcol, gval = gcol[:nnz.value], gval[:nnz.value]
+        self.n = n
+        self.kmax = int(kmax)
+        self.shift = 0.0
+        self.attempts = 0
+        self.g = CsrMatrix(n, grp, gcol, gval)
+        # G^T by a stable sort on the column index (rows of G ascending)
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(grp))
+        order = np.argsort(gcol, kind="stable")
+        trp = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(trp, gcol + 1, 1)
+        self.gt = CsrMatrix(n, np.cumsum(trp), rows[order], gval[order])
+        self._dg = self._dgt = self._tmp = None
+        self._dev_ready = False
+        self._DeviceCsr = DeviceCsr
+
+    def _ensure(self):
+        if not self._dev_ready:
+            self._dg = self._DeviceCsr(self.n, self.g.row_ptr, self.g.col_idx, self.g.values)
+            self._dgt = self._DeviceCsr(self.n, self.gt.row_ptr, self.gt.col_idx,
+                                        self.gt.values)
+            self._tmp = dev.empty(self.n)
+            self._dev_ready = True
+
+    def apply_raw(self, r, z, skip, stream):
+        self._ensure()
+        ws = dev.workspace().handle
+        lib = nat.load()
+        for m, src, dst in ((self._dg, r, self._tmp.data_ptr()),
+                            (self._dgt, self._tmp.data_ptr(), z)):
+            nat.check(lib.lg_spmv(m.handle, src, dst, 0.0, None, 0, 0, None, None, 0, 0, None,
+                                  ws, skip, stream), "lg_spmv")
+
+    def device(self):
+        self._ensure()
+        return self
+
+    def apply(self, r, z=None):
+        on_dev = dev.is_device_array(r)
+        rd = dev.to_device(r)
+        if tuple(rd.shape) != (self.n,):
+            raise ValueError("vector length does not match factor dimension")
+        out = dev.empty(self.n) if z is None else z
+        self.apply_raw(rd.data_ptr(), out.data_ptr(), None, dev.stream_ptr())
+        return out if on_dev else dev.to_host(out)
+
+
+def fsai_factorize(a, kmax=64):
+    """FSAI preconditioner of a (flagged non-reference variant)."""
+    return FsaiFactor(a, kmax)
+
+
 class CallablePrec:
     """Wraps a user callable / object with .apply (not graph-capturable)."""
 
@@ -101,8 +183,8 @@ def device_preconditioner(f, n):
         return IdentityPrec(n)
     if isinstance(f, (Ic0Factor, MulticolorIc0Factor)):
         return f.device()
-    if isinstance(f, JacobiFactor):
-        return f
+    if isinstance(f, (JacobiFactor, FsaiFactor)):
+        return f.device()
     if hasattr(f, "l") and hasattr(f.l, "row_ptr"):
         hit = _cache.get(id(f))
         if hit is None or hit[0] is not f:

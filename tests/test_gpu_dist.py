@@ -163,3 +163,26 @@ def test_row_partitioned_dacg_device_only_matrix():
     pairs, _ = out[0]
     assert np.array_equal(pairs.values, out[1][0].values)
     assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-8
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_partitioned_fsai_same_iterations(world):
+    """FSAI across ranks (dist.DistFsai: G and G^T as row-partitioned SpMVs
+    with exchanges) is the same preconditioner at every rank count: DACG and
+    JD take the single-GPU FSAI solve's MVP counts (to roundoff in the
+    all-reduced dots) and return its eigenvalues."""
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200.results import rayleigh_residuals
+    a = _graph()
+    f = L.fsai_factorize(a)
+    delta = 1e-8
+    for fn, run in ((L.dacg_smallest, _run_ranks), (L.jd_smallest, _run_ranks_jd)):
+        ref, rrep = fn(a, 4, delta=delta, f=f, seed=0)
+        out = run(a, world, f, 4, delta)
+        pairs, rep = out[0]
+        for p, _ in out:
+            assert np.array_equal(p.values, pairs.values)
+        assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-8
+        assert abs(rep.mvp - rrep.mvp) <= 0.03 * rrep.mvp + 3
+        _, res = rayleigh_residuals(a, pairs.vectors)
+        assert np.max(res) <= 1.5 * delta

@@ -198,3 +198,23 @@ def test_multicolor_variant_converges_to_same_pairs(L, cfg):
     for sv in ("dacg", "jd"):
         pairs, rep = solver(L, sv)(a, ref["neig"], delta=ref["delta"], f=f)
         check_pairs(L, a, pairs, np.asarray(ref["solvers"][sv]["eigenvalues"]), ref["delta"])
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_fsai_variant_converges_to_same_pairs(L, cfg):
+    """FSAI (flagged non-reference preconditioner, z = G^T G r): the device
+    apply equals G^T (G r) computed on the host, and DACG / JD with it
+    return the reference's eigenvalues within 1e-8 with fresh residuals
+    <= delta (its MVP counts differ from the reference IC(0)'s)."""
+    ref = golden_config(cfg)
+    a = L.build_laplacian(L.config_graph(cfg))
+    f = L.fsai_factorize(a)
+    r = np.random.default_rng(2).standard_normal(a.n)
+    import scipy.sparse as sp
+    G = sp.csr_matrix((f.g.values, f.g.col_idx, f.g.row_ptr), shape=(a.n, a.n))
+    want = G.T @ (G @ r)
+    z = f.apply(r)
+    assert np.max(np.abs(z - want)) <= 1e-12 * np.max(np.abs(want))
+    for sv in ("dacg", "jd"):
+        pairs, rep = solver(L, sv)(a, ref["neig"], delta=ref["delta"], f=f)
+        check_pairs(L, a, pairs, np.asarray(ref["solvers"][sv]["eigenvalues"]), ref["delta"])

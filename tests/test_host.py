@@ -226,3 +226,53 @@ def test_row_partitioned_pass_addresses():
     # one rank: the plain single-GPU pass, nothing wrapped
     one = Ctx(n, None).fused(dots=[(x, None)], result=res)
     assert isinstance(one, Fused) and one.args.n == n
+
+
+def _fsai_numpy(n, rp, col, val, kmax):
+    """Test-side restatement of the FSAI rows (lg_fsai.cu): pattern = the
+    strictly lower columns cut to kmax - 1 by |a_ij| (ties to larger j) plus
+    the diagonal; A[P, P] g = e_last; row = g / sqrt(g_last)."""
+    import numpy.linalg as la
+    A = np.zeros((n, n))
+    for r in range(n):
+        A[r, col[rp[r]:rp[r + 1]]] = val[rp[r]:rp[r + 1]]
+    G = np.zeros((n, n))
+    for i in range(n):
+        c, v = col[rp[i]:rp[i + 1]], val[rp[i]:rp[i + 1]]
+        low = [(abs(x), j) for j, x in zip(c, v) if j < i]
+        low.sort(key=lambda t: (-t[0], -t[1]))
+        P = sorted(j for _, j in low[:kmax - 1]) + [i]
+        e = np.zeros(len(P))
+        e[-1] = 1.0
+        g = la.solve(A[np.ix_(P, P)], e)
+        G[i, P] = g / np.sqrt(g[-1])
+    return A, G
+
+
+@pytest.mark.parametrize("kmax", [4, 64])
+def test_fsai_factor_rows(kmax):
+    """lg_fsai_factorize (host C++) against the restatement, and the FSAI
+    property diag(G A G^T) = 1 (no GPU needed)."""
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200.generators import chung_lu_graph
+    from paper_1311_1695_b200.graphs import largest_component
+    from paper_1311_1695_b200.precond import FsaiFactor
+    from paper_1311_1695_b200.sparse import CsrMatrix
+    g, _ = largest_component(chung_lu_graph(300, 2.1, 5.0, max_degree=60, weighted=True, seed=4))
+    rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+    a = CsrMatrix(g.n_nodes, rp, col, val)
+    f = FsaiFactor(a, kmax=kmax)
+    n = a.n
+    A, Gw = _fsai_numpy(n, rp, col, val, kmax)
+    G = np.zeros((n, n))
+    for r in range(n):
+        G[r, f.g.col_idx[f.g.row_ptr[r]:f.g.row_ptr[r + 1]]] = \
+            f.g.values[f.g.row_ptr[r]:f.g.row_ptr[r + 1]]
+    assert np.array_equal(G != 0, Gw != 0)
+    assert np.max(np.abs(G - Gw)) <= 1e-11 * np.max(np.abs(Gw))
+    assert np.allclose(np.diag(G @ A @ G.T), 1.0, atol=1e-10)
+    GT = np.zeros((n, n))
+    for r in range(n):
+        GT[r, f.gt.col_idx[f.gt.row_ptr[r]:f.gt.row_ptr[r + 1]]] = \
+            f.gt.values[f.gt.row_ptr[r]:f.gt.row_ptr[r + 1]]
+    assert np.array_equal(GT, G.T)
