@@ -225,6 +225,10 @@ def solve_block(a, f, f_mc=None):
     if f_mc is not None:
         runs += [("dacg_multicolor", L.dacg_smallest, f_mc, "multicolour ic0 (flagged variant)"),
                  ("jd_multicolor", L.jd_smallest, f_mc, "multicolour ic0 (flagged variant)")]
+    f_fsai = L.fsai_factorize(a, kmax=32)
+    f_fsai.device()
+    runs += [("dacg_fsai", L.dacg_smallest, f_fsai, "fsai kmax 32 (flagged variant)"),
+             ("jd_fsai", L.jd_smallest, f_fsai, "fsai kmax 32 (flagged variant)")]
     for name, fn, prec, label in runs:
         walls = []
         for _ in range(2):   # first call (graph capture, lazy scratch) and steady state
@@ -274,23 +278,32 @@ def solve_configs_block(prebuilt=None):
             f.device()
             cache[base] = (a, f)
         a, f = cache[base]
+        variants = [("", f, "ic0 (reference)")]
+        if cfg in ("C3n20", "C4n10"):
+            # the flagged FSAI variant next to the parity mode (same pairs,
+            # different preconditioner: its MVPs are reported, not compared)
+            ff = L.fsai_factorize(a, kmax=32)
+            ff.device()
+            variants.append(("_fsai", ff, "fsai kmax 32 (flagged variant)"))
         for name in solvers:
-            walls = []
-            for _ in range(2):
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                pairs, rep = fns[name](a, gold["neig"], delta=gold["delta"], f=f)
-                torch.cuda.synchronize()
-                walls.append(time.perf_counter() - t0)
-            r = gold["solvers"][name]
-            ref_vals = np.asarray(r["eigenvalues"])
-            out[f"{cfg}_{name}"] = {
-                "neig": gold["neig"], "delta": gold["delta"], "wall_s": walls[1],
-                "wall_s_first_call": walls[0], "mvp": rep.mvp, "reference_mvp": r["mvp"],
-                "eig_relerr_vs_reference": float(np.max(np.abs(pairs.values - ref_vals)
-                                                        / np.abs(ref_vals))),
-                "reference_wall_s_build_container": r["wall_seconds"],
-                "speedup_vs_reference_wall": r["wall_seconds"] / walls[1]}
+            for suffix, prec, label in variants:
+                walls = []
+                for _ in range(2):
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    pairs, rep = fns[name](a, gold["neig"], delta=gold["delta"], f=prec)
+                    torch.cuda.synchronize()
+                    walls.append(time.perf_counter() - t0)
+                r = gold["solvers"][name]
+                ref_vals = np.asarray(r["eigenvalues"])
+                out[f"{cfg}_{name}{suffix}"] = {
+                    "neig": gold["neig"], "delta": gold["delta"], "preconditioner": label,
+                    "wall_s": walls[1], "wall_s_first_call": walls[0], "mvp": rep.mvp,
+                    "reference_mvp": r["mvp"],
+                    "eig_relerr_vs_reference": float(np.max(np.abs(pairs.values - ref_vals)
+                                                            / np.abs(ref_vals))),
+                    "reference_wall_s_build_container": r["wall_seconds"],
+                    "speedup_vs_reference_wall": r["wall_seconds"] / walls[1]}
     return out
 
 
