@@ -912,8 +912,22 @@ struct HostWs {
   cudaEvent_t done[kHostChunks] = {};   // chunk product finished
   cudaEvent_t copied[kHostChunks] = {}; // chunk copied to pinned memory
   bool ok = false;
+  int device = -1;
   bool ready() {
-    if (ok) return true;
+    int dv = 0;
+    if (cudaGetDevice(&dv) != cudaSuccess) return false;
+    if (ok && dv == device) return true;
+    if (ok) {   // the thread moved to another device: new stream and events
+      cudaStreamDestroy(d2h);
+      for (int c = 0; c < kHostChunks; ++c) {
+        cudaEventDestroy(done[c]);
+        cudaEventDestroy(copied[c]);
+      }
+      if (ws) lg_ws_destroy(ws);
+      ws = nullptr;
+      ok = false;
+    }
+    device = dv;
     if (cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking) != cudaSuccess) return false;
     for (int c = 0; c < kHostChunks; ++c)
       if (cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming) != cudaSuccess ||
@@ -950,6 +964,7 @@ int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,
   const int64_t n = a->n;
   if (n == 0) return LG_OK;
   if (!g_stage.ensure(n)) return fail(LG_ENOMEM, "lg_spmv_host: pinned staging");
+  if (!g_host_ws.ready()) return fail(LG_ECUDA, "lg_spmv_host: stream / event setup");
   if (!g_host_ws.ws) {
     int rc0 = lg_ws_create(&g_host_ws.ws);
     if (rc0) return rc0;
@@ -958,7 +973,6 @@ int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,
     int rc0 = ensure_long_ws(g_host_ws.ws, a);
     if (rc0) return rc0;
   }
-  if (!g_host_ws.ready()) return fail(LG_ECUDA, "lg_spmv_host: stream / event setup");
   // x: host copy of chunk c+1 overlaps the DMA of chunk c
   const int kx = pipe ? 4 : 1;
   const int64_t cx = (n + kx - 1) / kx;
