@@ -896,8 +896,8 @@ struct HostStaging {
     if (yout) cudaFreeHost(yout);
     xin = yout = nullptr;
     cap = 0;
-    if (cudaHostAlloc(&xin, 8 * (size_t)n, cudaHostAllocDefault) != cudaSuccess ||
-        cudaHostAlloc(&yout, 8 * (size_t)n, cudaHostAllocDefault) != cudaSuccess)
+    if (cudaHostAlloc(&xin, 8 * (size_t)n, cudaHostAllocPortable) != cudaSuccess ||
+        cudaHostAlloc(&yout, 8 * (size_t)n, cudaHostAllocPortable) != cudaSuccess)
       return false;
     cap = n;
     return true;
