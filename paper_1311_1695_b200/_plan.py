@@ -518,9 +518,12 @@ class Ctx:
         return self.comm is not None
 
     def v(self, t):
-        """A vector operand restricted to this rank's rows."""
-        if self.comm is None or t is None or isinstance(t, int):
+        """A vector operand restricted to this rank's rows (a tensor, or a raw
+        device address; small ints are references to a pass's own outputs)."""
+        if self.comm is None or t is None:
             return t
+        if isinstance(t, int):
+            return t if t < 16 else t + 8 * self.lo
         return t[self.lo:self.lo + self.nl]
 
     def q(self, c):
