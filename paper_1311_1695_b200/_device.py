@@ -175,6 +175,44 @@ def staging(n):
     return st
 
 
+class _PinnedPool:
+    """Page-locked host buffers handed out as fresh numpy arrays (results of
+    the host-buffer products, DMA'd into directly); a buffer goes back to the
+    pool when its array is collected.  A few buffers per size are kept."""
+
+    KEEP = 8
+
+    def __init__(self):
+        self.free = {}
+        self.lock = threading.Lock()
+
+    def array(self, n):
+        import weakref
+        t = torch()
+        with self.lock:
+            lst = self.free.get(n)
+            buf = lst.pop() if lst else None
+        if buf is None:
+            buf = t.empty(n, dtype=t.float64, pin_memory=True)
+        arr = buf.numpy()
+        weakref.finalize(arr, self._give_back, n, buf)
+        return arr
+
+    def _give_back(self, n, buf):
+        with self.lock:
+            lst = self.free.setdefault(n, [])
+            if len(lst) < self.KEEP:
+                lst.append(buf)
+
+
+_pinned_pool = _PinnedPool()
+
+
+def pinned_array(n):
+    """A fresh float64 numpy array of length n in page-locked memory."""
+    return _pinned_pool.array(n)
+
+
 _solver_streams = {}
 
 

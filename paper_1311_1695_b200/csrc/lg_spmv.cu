@@ -953,6 +953,15 @@ void par_copy(double* dst, const double* src, int64_t n) {
     std::memcpy(dst + lo, src + lo, 8 * (size_t)(hi - lo));
   }
 }
+// cudaHostAlloc'ed / cudaHostRegister'ed memory (DMA-able as it is)
+bool host_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
 }  // namespace
 
 extern "C" {
@@ -973,23 +982,30 @@ int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,
     int rc0 = ensure_long_ws(g_host_ws.ws, a);
     if (rc0) return rc0;
   }
+  static const bool pipe = [] {
+    const char* e = getenv("LG_HOST_PIPE");   // 0: one copy, one product, one D2H
+    return !(e && atoi(e) == 0);
+  }();
+  // Page-locked caller buffers are DMA'd directly (no staging copy).
+  const bool xpin = host_pinned(x_h), ypin = host_pinned(y_h);
   // x: host copy of chunk c+1 overlaps the DMA of chunk c
-  const int kx = pipe ? 4 : 1;
-  const int64_t cx = (n + kx - 1) / kx;
-  for (int c = 0; c < kx; ++c) {
-    const int64_t lo = c * cx, hi = std::min(n, lo + cx);
-    if (lo >= hi) break;
-    par_copy(g_stage.xin + lo, x_h + lo, hi - lo);
-    LG_CUDA(cudaMemcpyAsync(xd + lo, g_stage.xin + lo, 8 * (size_t)(hi - lo),
-                            cudaMemcpyHostToDevice, s));
+  if (xpin) {
+    LG_CUDA(cudaMemcpyAsync(xd, x_h, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
+  } else {
+    const int kx = pipe ? 4 : 1;
+    const int64_t cx = (n + kx - 1) / kx;
+    for (int c = 0; c < kx; ++c) {
+      const int64_t lo = c * cx, hi = std::min(n, lo + cx);
+      if (lo >= hi) break;
+      par_copy(g_stage.xin + lo, x_h + lo, hi - lo);
+      LG_CUDA(cudaMemcpyAsync(xd + lo, g_stage.xin + lo, 8 * (size_t)(hi - lo),
+                              cudaMemcpyHostToDevice, s));
+    }
   }
   // y: the product runs in row chunks; each chunk's D2H (second stream)
   // overlaps the next chunk's product, and the host copy of chunk c overlaps
   // the DMA of chunk c+1
-  static const bool pipe = [] {
-    const char* e = getenv("LG_HOST_PIPE");   // 0: one product, one D2H
-    return !(e && atoi(e) == 0);
-  }();
+  double* ydst = ypin ? y_h : g_stage.yout;
   const bool chunked = pipe && a->nchunks > 1;
   const int nc = chunked ? a->nchunks : 1;
   for (int c = 0; c < nc; ++c) {
@@ -1002,15 +1018,16 @@ int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,
     LG_CUDA(cudaEventRecord(g_host_ws.done[c], s));
     LG_CUDA(cudaStreamWaitEvent(g_host_ws.d2h, g_host_ws.done[c], 0));
     if (r1 > r0)
-      LG_CUDA(cudaMemcpyAsync(g_stage.yout + r0, yd + r0, 8 * (size_t)(r1 - r0),
+      LG_CUDA(cudaMemcpyAsync(ydst + r0, yd + r0, 8 * (size_t)(r1 - r0),
                               cudaMemcpyDeviceToHost, g_host_ws.d2h));
     LG_CUDA(cudaEventRecord(g_host_ws.copied[c], g_host_ws.d2h));
   }
   for (int c = 0; c < nc; ++c) {
     const int64_t r0 = chunked ? a->chunk_row[c] : 0;
     const int64_t r1 = chunked ? a->chunk_row[c + 1] : n;
+    if (ypin && c < nc - 1) continue;   // the last event covers every chunk
     LG_CUDA(cudaEventSynchronize(g_host_ws.copied[c]));
-    if (r1 > r0) par_copy(y_h + r0, g_stage.yout + r0, r1 - r0);
+    if (!ypin && r1 > r0) par_copy(y_h + r0, g_stage.yout + r0, r1 - r0);
   }
   // the caller's stream is ordered after the copies (xd / yd reuse)
   LG_CUDA(cudaStreamWaitEvent(s, g_host_ws.copied[nc - 1], 0));

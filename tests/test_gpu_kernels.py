@@ -480,6 +480,23 @@ def test_spmv_host_buffers_cabi_and_public():
     assert np.array_equal(y2, want)
     yr = O.spmv(O.Csr(a.n, a.row_ptr, a.col_idx, a.values), x)
     assert np.max(np.abs(y2 - yr)) <= 1e-13 * np.max(np.abs(yr))
+    # page-locked caller buffers are DMA'd directly (no staging)
+    xp = torch.empty(a.n, dtype=torch.float64, pin_memory=True).numpy()
+    yp = torch.empty(a.n, dtype=torch.float64, pin_memory=True).numpy()
+    xp[:] = x
+    nat.call("lg_spmv_host", a.device().handle, xp.ctypes.data, yp.ctypes.data,
+             ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(ydd.data_ptr()),
+             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert np.array_equal(yp, want)
+    # every public product is a fresh array (pinned results are recycled
+    # only after their array is gone)
+    x2 = np.random.default_rng(4).standard_normal(a.n)
+    keep = [L.spmv(a, x) for _ in range(3)]
+    del y1
+    y3 = L.spmv(a, x2)
+    for k in keep:
+        assert np.array_equal(k, want)
+    assert not np.array_equal(y3, want)
 
 
 @pytest.mark.parametrize("world", [2, 3])
