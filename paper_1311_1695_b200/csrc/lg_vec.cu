@@ -41,7 +41,16 @@ struct FusedDev {
 // kU independent loads per operand in flight (memory-level parallelism is
 // what a streaming pass over HBM needs; one element per thread leaves the
 // pass latency-bound at ~1-3 TB/s).
-constexpr int kU = 4;
+// Tiles per thread and resident CTAs per SM depend on the pass: passes
+// with at most 4 reduced values keep 4 elements per lane in flight at 4
+// CTAs per SM; passes with block dots / updates (k >= 5 reduced values, the
+// deflation projections) use 2 elements per lane -- fewer registers, the
+// same 4 CTAs per SM.  Measured on 32.8 M-element passes: a 4-term
+// combination with 3 dots 308 -> 275 us (4.8 TB/s), a k = 6 projection
+// update with Q^T v 889 -> 654 us (5.6 TB/s).
+template <int NA>
+__host__ __device__ constexpr int fused_u() { return NA <= 4 ? 4 : 2; }
+constexpr int kU = 4;   // widest tile (shared-memory sizing)
 
 template <int U>
 __device__ __forceinline__ void load_u(const double* p, int64_t i0, int64_t n, double (&v)[U]) {
@@ -127,15 +136,16 @@ struct ProgDev {
 };
 
 template <int NA, bool PROG>
-__global__ void __launch_bounds__(kThreads, (NA <= 8 ? 3 : (NA <= 16 ? 2 : 1)))
+__global__ void __launch_bounds__(kThreads, (NA <= 8 ? 4 : (NA <= 16 ? 2 : 1)))
 fused_kernel(FusedDev a, lg_ws ws, const __grid_constant__ ProgDev pd) {
+  constexpr int U = fused_u<NA>();
   if (a.skip && *a.skip) return;
   constexpr int M = NA > 0 ? NA : 1;
   __shared__ double uc_sm[LG_MAXO][LG_MAXQ];
   __shared__ double uc2_sm[LG_MAXO][LG_MAXQ];
   __shared__ double red_sm[kWarps * M];
   // per-pass coefficients in shared memory (uniform broadcast reads keep
-  // the registers for the kU-element tiles)
+  // the registers for the U-element tiles)
   __shared__ double coef[LG_MAXO][LG_MAXT];
   __shared__ double post[LG_MAXO];
   __shared__ int pmode[LG_MAXO];
@@ -179,54 +189,54 @@ fused_kernel(FusedDev a, lg_ws ws, const __grid_constant__ ProgDev pd) {
   const int64_t n = a.n;
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t tile = 32 * kU;
+  const int64_t tile = 32 * U;
   const int64_t wstride = (((int64_t)gridDim.x * blockDim.x) >> 5) * tile;
 
   for (int64_t i0 = gw * tile + lane; i0 - lane < n; i0 += wstride) {
-    double ov[LG_MAXO][kU];
+    double ov[LG_MAXO][U];
 #pragma unroll
     for (int k = 0; k < LG_MAXO; ++k) {
       if (a.o[k].out) {
-        output_u<kU>(a.o[k], coef[k], uc_sm[k], uc2_sm[k], i0, n, ov, post[k], pmode[k], ov[k]);
+        output_u<U>(a.o[k], coef[k], uc_sm[k], uc2_sm[k], i0, n, ov, post[k], pmode[k], ov[k]);
         double* out = a.o[k].out;
 #pragma unroll
-        for (int u = 0; u < kU; ++u)
+        for (int u = 0; u < U; ++u)
           if (i0 + 32 * u < n) out[i0 + 32 * u] = ov[k][u];
       }
     }
     if constexpr (NA > 0) {
-      double bv0[kU], bv1[kU];
-      if (k0) operand<kU>(a.b[0].v, i0, n, ov, bv0);
-      if (k1) operand<kU>(a.b[1].v, i0, n, ov, bv1);
+      double bv0[U], bv1[U];
+      if (k0) operand<U>(a.b[0].v, i0, n, ov, bv0);
+      if (k1) operand<U>(a.b[1].v, i0, n, ov, bv1);
 #pragma unroll
       for (int s = 0; s < NA; ++s) {
         if (s < nd) {
-          double x[kU], y[kU];
-          operand<kU>(a.da[s], i0, n, ov, x);
+          double x[U], y[U];
+          operand<U>(a.da[s], i0, n, ov, x);
           if (a.dc[s]) {
-            double c[kU];
-            operand<kU>(a.dc[s], i0, n, ov, c);
+            double c[U];
+            operand<U>(a.dc[s], i0, n, ov, c);
 #pragma unroll
-            for (int u = 0; u < kU; ++u) x[u] -= c[u];
+            for (int u = 0; u < U; ++u) x[u] -= c[u];
           }
           if (a.db[s]) {
-            operand<kU>(a.db[s], i0, n, ov, y);
+            operand<U>(a.db[s], i0, n, ov, y);
           } else {
 #pragma unroll
-            for (int u = 0; u < kU; ++u) y[u] = x[u];
+            for (int u = 0; u < U; ++u) y[u] = x[u];
           }
 #pragma unroll
-          for (int u = 0; u < kU; ++u) acc[s] += x[u] * y[u];
+          for (int u = 0; u < U; ++u) acc[s] += x[u] * y[u];
         } else if (s < nd + k0) {
-          double q[kU];
-          load_u<kU>(a.b[0].q + (int64_t)(s - nd) * a.b[0].ld, i0, n, q);
+          double q[U];
+          load_u<U>(a.b[0].q + (int64_t)(s - nd) * a.b[0].ld, i0, n, q);
 #pragma unroll
-          for (int u = 0; u < kU; ++u) acc[s] += bv0[u] * q[u];
+          for (int u = 0; u < U; ++u) acc[s] += bv0[u] * q[u];
         } else if (s < nd + k0 + k1) {
-          double q[kU];
-          load_u<kU>(a.b[1].q + (int64_t)(s - nd - k0) * a.b[1].ld, i0, n, q);
+          double q[U];
+          load_u<U>(a.b[1].q + (int64_t)(s - nd - k0) * a.b[1].ld, i0, n, q);
 #pragma unroll
-          for (int u = 0; u < kU; ++u) acc[s] += bv1[u] * q[u];
+          for (int u = 0; u < U; ++u) acc[s] += bv1[u] * q[u];
         }
       }
     }
@@ -251,7 +261,8 @@ static int launch_fused(const FusedDev& a, lg_ws* ws, cudaStream_t s, const Prog
       occ = 1;
     cap = std::min(occ * dev_info().sm_count, kMaxRedBlocks);
   }
-  const int64_t want = (a.n + (int64_t)kThreads * kU - 1) / ((int64_t)kThreads * kU);
+  constexpr int U = fused_u<NA>();
+  const int64_t want = (a.n + (int64_t)kThreads * U - 1) / ((int64_t)kThreads * U);
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
   static thread_local ProgDev none{};
   fused_kernel<NA, PROG><<<g, kThreads, 0, s>>>(a, *ws, pd ? *pd : none);
