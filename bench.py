@@ -106,7 +106,7 @@ def build_graph(config):
     return config_graph(config)
 
 
-from paper_1311_1695_b200.dist import (RowPartition, SliceExchange,  # noqa: E402
+from paper_1311_1695_b200.dist import (RowPartition,  # noqa: E402
                                       device_row_ptr, local_operator,
                                       local_operator_device, partition_rows)
 

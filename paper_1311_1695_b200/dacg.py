@@ -38,10 +38,10 @@ import time
 import numpy as np
 
 from . import _device as dev
-from ._plan import Ctx, Fused, Graph, PrecApply, Prog, Slots, Spmv
+from ._plan import Ctx, Fused, Graph, Prog, Slots
 from ._rng import NormalStream
 from .ic0 import ic0_factorize
-from .pcg import kernel_basis, project_device
+from .pcg import kernel_basis
 from .precond import device_preconditioner
 from .results import EigenPairSet, SolverError, SolverReport
 from .sparse import MvpCounter, device_csr, spmv

@@ -21,7 +21,7 @@ import time
 import numpy as np
 
 from . import _device as dev
-from ._plan import Ctx, Fused, PrecApply, Slots, Spmv
+from ._plan import Ctx, Fused, Slots
 from ._rng import NormalStream
 from .ic0 import ic0_factorize
 from .kernels import DeviceGS, GramSchmidtBreakdown, dense_sym_eig

@@ -24,8 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _device as dev
-from ._plan import Ctx, Fused, Graph, PrecApply, Prog, Slots, Spmv
-from .sparse import device_csr
+from ._plan import Ctx, Fused, Graph, Prog, Slots
 
 _ORTHO_TOL = 1e-10
 
