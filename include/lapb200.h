@@ -44,6 +44,7 @@ extern "C" {
 #define LG_ECUDA -2       /* CUDA runtime failure (maps to RuntimeError)    */
 #define LG_ENOMEM -3      /* allocation failure                             */
 #define LG_EBREAKDOWN -4  /* IC(0) pivot breakdown at every shift (Ic0Error) */
+#define LG_EFORMAT -5     /* malformed graph file (GraphFormatError)         */
 
 /* ---- library / device -------------------------------------------------- */
 const char* lg_last_error(void);
@@ -169,6 +170,19 @@ int lg_ic0_factorize(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
                      const double* val_h, double shift0, const double* sched_h,
                      int nsched, int64_t* l_row_ptr_h, int64_t* l_col_h,
                      double* l_val_h, double* shift, int* attempts);
+
+/* ---- graph file ingest (graphs.py:126-247) ------------------------------
+ * Parse a text edge list (format 0: first line n, then 'i j w' lines, '#'
+ * comments) or Matrix Market coordinate file (format 1: diagonal entries
+ * dropped, off-diagonal magnitudes become weights) held in memory, with the
+ * reference's rules and messages: the canonical edge list (i < j, sorted by
+ * (i, j)) comes back in malloc'ed arrays (free with lg_host_free); a
+ * repeated pair is an error unless symmetrize (then the maximum weight).
+ * LG_EFORMAT + lg_last_error() + *err_line (1-based, 0 = none) on bad input. */
+int lg_graph_parse(const char* text, int64_t len, int format, int symmetrize, int64_t* n_out,
+                   int64_t* m_out, int64_t** i_out, int64_t** j_out, double** w_out,
+                   int64_t* err_line);
+int lg_host_free(void* p);
 
 /* ---- FSAI preconditioner (flagged non-reference variant; the approximate
  * inverse PAPER.md:704-706 proposes) ----------------

@@ -21,7 +21,9 @@ from .generators import (
     rmat_graph,
     star_graph,
 )
-from .graphs import EdgeList, build_laplacian, connected_components, largest_component
+from .graphs import (EdgeList, GraphFormatError, GraphStats, build_laplacian,
+                     connected_components, csr_connected_components, largest_component,
+                     load_edge_list, stats, write_matrix_market)
 from .ic0 import (
     Ic0Error,
     Ic0Factor,
@@ -42,7 +44,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CsrMatrix", "DeflationBasis", "EdgeList", "EigenPairSet", "GramSchmidtBreakdown",
-    "FsaiFactor", "fsai_factorize", "Ic0Error", "Ic0Factor", "JacobiFactor", "MulticolorIc0Factor", "ic0_factorize_multicolor", "MvpCounter", "PcgOutcome", "SolverError",
+    "FsaiFactor", "fsai_factorize", "GraphFormatError", "GraphStats", "load_edge_list",
+    "stats", "csr_connected_components", "write_matrix_market", "Ic0Error", "Ic0Factor", "JacobiFactor", "MulticolorIc0Factor", "ic0_factorize_multicolor", "MvpCounter", "PcgOutcome", "SolverError",
     "SolverReport", "ba_graph", "build_laplacian", "chung_lu_graph", "complete_graph",
     "config_graph", "connected_components", "cycle_graph", "dacg_smallest", "dense_sym_eig",
     "grid_graph", "ic0_factorize", "identity_factor", "irlm_smallest", "jd_correction_solve",

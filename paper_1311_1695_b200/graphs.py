@@ -10,15 +10,36 @@ Mirrors the parts of the reference graphs.py on the hot path's input side:
                         graphs.py:278-316 same numbering (components by
                                           smallest node, ties -> smallest id)
 
-File loaders, stats and Matrix Market output (graphs.py:86-247,319-361) are
-one-time host ingest and stay out of scope.
+    GraphFormatError, load_edge_list
+                        graphs.py:18-25,126-247 text edge lists and Matrix
+                                          Market files parsed in C++
+                                          (lg_graph_parse, lg_load.cu): same
+                                          rules, messages and line numbers
+    GraphStats, stats, csr_connected_components, write_matrix_market
+                        graphs.py:86-92,319-361
 """
+
+import ctypes
+import io
+from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
 
 from . import _native as nat
 from . import _device as dev
 from .sparse import CsrMatrix
+
+
+class GraphFormatError(ValueError):
+    """Malformed graph input; carries a 1-based line number when known
+    (graphs.py:18-25)."""
+
+    def __init__(self, message, line=None):
+        self.line = line
+        if line is not None:
+            message = f"line {line}: {message}"
+        super().__init__(message)
 
 
 class EdgeList:
@@ -146,3 +167,101 @@ def largest_component(g):
     sub = EdgeList.from_canonical(int(keep.sum()), node_map[g.i[mask]], node_map[g.j[mask]],
                                   g.w[mask])
     return sub, node_map
+
+
+@dataclass(frozen=True)
+class GraphStats:
+    n: int
+    nnz: int
+    anzr: float
+    components: int
+
+
+def load_edge_list(source, format="edgelist", symmetrize=False):
+    """Read a graph from a path or open text stream (graphs.py:231-247).
+
+    format is "edgelist" (first line n, then 'i j w' lines, # comments) or
+    "mtx" (Matrix Market coordinate; diagonal entries are dropped,
+    off-diagonal magnitudes become weights).  The text is parsed by the
+    library's C++ parser (lg_graph_parse); errors raise GraphFormatError with
+    the reference's message and 1-based line number.
+    """
+    if format not in ("edgelist", "mtx"):
+        raise ValueError(f"unknown format {format!r}")
+    if isinstance(source, (str, Path)):
+        with open(source, "rb") as fh:
+            data = fh.read()
+        data.decode("utf-8")          # same encoding errors as the reference
+    elif isinstance(source, bytes):
+        data = source
+        data.decode("utf-8")
+    else:
+        text = source.read()
+        data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    # universal newlines, as Python's text I/O reads files
+    if b"\r" in data:
+        data = data.replace(b"\r\n", b"\n").replace(b"\r", b"\n")
+    lib = nat.load()
+    n, m = ctypes.c_int64(), ctypes.c_int64()
+    pi, pj, pw = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+    line = ctypes.c_int64()
+    rc = lib.lg_graph_parse(data, len(data), 0 if format == "edgelist" else 1,
+                            1 if symmetrize else 0, ctypes.byref(n), ctypes.byref(m),
+                            ctypes.byref(pi), ctypes.byref(pj), ctypes.byref(pw),
+                            ctypes.byref(line))
+    if rc == nat.LG_EFORMAT:
+        raise GraphFormatError(nat.last_error(), line.value or None)
+    nat.check(rc, "lg_graph_parse")
+    try:
+        mm = m.value
+        i = np.ctypeslib.as_array(ctypes.cast(pi, ctypes.POINTER(ctypes.c_int64)),
+                                  (max(mm, 1),))[:mm].copy()
+        j = np.ctypeslib.as_array(ctypes.cast(pj, ctypes.POINTER(ctypes.c_int64)),
+                                  (max(mm, 1),))[:mm].copy()
+        w = np.ctypeslib.as_array(ctypes.cast(pw, ctypes.POINTER(ctypes.c_double)),
+                                  (max(mm, 1),))[:mm].copy()
+    finally:
+        for p in (pi, pj, pw):
+            lib.lg_host_free(p)
+    return EdgeList.from_canonical(n.value, i, j, w)
+
+
+def stats(g):
+    """Size summary: n, Laplacian nonzeros n + 2m, average per row,
+    components (graphs.py:319-323)."""
+    count, _ = connected_components(g)
+    nnz = g.n_nodes + 2 * g.m
+    return GraphStats(n=g.n_nodes, nnz=nnz, anzr=nnz / g.n_nodes, components=count)
+
+
+def csr_connected_components(a):
+    """Component count and labels from the off-diagonal pattern of a CSR
+    matrix (graphs.py:326-344); components numbered by their smallest node."""
+    rp = np.asarray(a.row_ptr)
+    col = np.asarray(a.col_idx)
+    n = int(a.n)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    off = rows != col
+    lo = np.minimum(rows[off], col[off])
+    hi = np.maximum(rows[off], col[off])
+    key = np.unique(lo * max(n, 1) + hi)
+    g = EdgeList.from_canonical(n, key // max(n, 1), key % max(n, 1), np.ones(key.size))
+    return connected_components(g)
+
+
+def write_matrix_market(a, stream=None):
+    """Serialize a symmetric CSR matrix in coordinate format, lower triangle
+    (graphs.py:347-361); returns the text when no stream is given."""
+    rp = np.asarray(a.row_ptr)
+    col = np.asarray(a.col_idx)
+    val = np.asarray(a.values, dtype=np.float64)
+    n = int(a.n)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    keep = col <= rows
+    out = io.StringIO() if stream is None else stream
+    out.write("%%MatrixMarket matrix coordinate real symmetric\n")
+    out.write(f"{n} {n} {int(keep.sum())}\n")
+    out.writelines(f"{i + 1} {j + 1} {float(v)!r}\n"
+                   for i, j, v in zip(rows[keep].tolist(), col[keep].tolist(),
+                                      val[keep].tolist()))
+    return out.getvalue() if stream is None else None

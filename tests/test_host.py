@@ -276,3 +276,55 @@ def test_fsai_factor_rows(kmax):
         GT[r, f.gt.col_idx[f.gt.row_ptr[r]:f.gt.row_ptr[r + 1]]] = \
             f.gt.values[f.gt.row_ptr[r]:f.gt.row_ptr[r + 1]]
     assert np.array_equal(GT, G.T)
+
+
+def test_graph_loader_matches_reference_cases():
+    """load_edge_list (C++ lg_graph_parse) on the golden inputs: the same
+    canonical edge list (bitwise weights) or the same GraphFormatError
+    message and line as the reference's parsers (graphs.py:126-247;
+    tests/golden/make_loader_golden.py ran them)."""
+    import json
+
+    import paper_1311_1695_b200 as L
+    cases = json.loads((Path(__file__).parent / "golden" / "loader_cases.json").read_text())
+    for rec in cases:
+        src = rec["text"].encode()
+        if "error" in rec:
+            with pytest.raises(L.GraphFormatError) as err:
+                L.load_edge_list(src, format=rec["format"], symmetrize=rec["symmetrize"])
+            assert str(err.value) == rec["error"], (rec["text"], str(err.value))
+            assert err.value.line == rec["line"]
+        else:
+            g = L.load_edge_list(src, format=rec["format"], symmetrize=rec["symmetrize"])
+            assert g.n_nodes == rec["n"]
+            assert g.i.tolist() == rec["i"] and g.j.tolist() == rec["j"]
+            assert [float(x).hex() for x in g.w] == rec["w"]
+
+
+def test_graph_loader_paths_streams_and_round_trip(tmp_path):
+    """Paths, text streams and bytes give the same graph; Matrix Market
+    output of a Laplacian reads back as the same graph (graphs.py:347-361);
+    stats and csr_connected_components count components."""
+    import io
+
+    import paper_1311_1695_b200 as L
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200.sparse import CsrMatrix
+    text = "6\n0 1 1.5\n1 2 2\n# gap\n3 4 0.5\n"
+    p = tmp_path / "g.txt"
+    p.write_text(text)
+    a = L.load_edge_list(str(p))
+    b = L.load_edge_list(io.StringIO(text))
+    c = L.load_edge_list(text.encode())
+    assert a.pairs() == b.pairs() == c.pairs() == [(0, 1, 1.5), (1, 2, 2.0), (3, 4, 0.5)]
+    st = L.stats(a)
+    assert (st.n, st.nnz, st.components) == (6, 12, 3)
+    rp, col, val = O.build_laplacian(a.n_nodes, a.i, a.j, a.w)
+    lap = CsrMatrix(a.n_nodes, rp, col, val, symmetric=True)
+    blob = L.write_matrix_market(lap)
+    back = L.load_edge_list(blob.encode(), format="mtx")
+    assert back.pairs() == a.pairs()
+    count, labels = L.csr_connected_components(lap)
+    assert count == 3 and labels.tolist() == [0, 0, 0, 1, 1, 2]
+    with pytest.raises(ValueError):
+        L.load_edge_list(b"", format="csv")
