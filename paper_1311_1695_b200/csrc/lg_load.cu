@@ -12,6 +12,7 @@
 // nan); digit-group underscores, which Python also accepts, are not.
 #include <algorithm>
 #include <charconv>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -191,44 +192,47 @@ struct Raw {
 };
 
 // _merge_triples: canonical (lo, hi) order (stable in file order), repeated
-// pairs an error without symmetrize, maximum weight with it
-bool merge(int64_t n, Raw& raw, bool sym, std::vector<int64_t>& I, std::vector<int64_t>& J,
-           std::vector<double>& W, ParseError& err) {
-  const size_t m = raw.a.size();
-  std::vector<int64_t> lo(m), hi(m);
-  for (size_t k = 0; k < m; ++k) {
-    lo[k] = std::min(raw.a[k], raw.b[k]);
-    hi[k] = std::max(raw.a[k], raw.b[k]);
-  }
-  std::vector<size_t> ord(m);
-  for (size_t k = 0; k < m; ++k) ord[k] = k;
+// pairs an error without symmetrize, maximum weight with it.  Writes at most
+// m entries into I / J / W and returns the count through mo.
+bool merge(const Raw& raw, bool sym, int64_t* I, int64_t* J, double* W, int64_t& mo,
+           ParseError& err) {
+  const int64_t m = (int64_t)raw.a.size();
+  auto lo = [&](int64_t k) { return std::min(raw.a[(size_t)k], raw.b[(size_t)k]); };
+  auto hi = [&](int64_t k) { return std::max(raw.a[(size_t)k], raw.b[(size_t)k]); };
   bool sorted = true;   // canonical files skip the sort
-  for (size_t k = 1; k < m && sorted; ++k)
-    sorted = lo[k - 1] < lo[k] || (lo[k - 1] == lo[k] && hi[k - 1] <= hi[k]);
-  if (!sorted)
-    std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) {
-      return lo[x] != lo[y] ? lo[x] < lo[y] : hi[x] < hi[y];
+  for (int64_t k = 1; k < m && sorted; ++k) {
+    const int64_t l0 = lo(k - 1), l1 = lo(k);
+    sorted = l0 < l1 || (l0 == l1 && hi(k - 1) <= hi(k));
+  }
+  std::vector<int64_t> ord;
+  if (!sorted) {
+    ord.resize((size_t)m);
+    for (int64_t k = 0; k < m; ++k) ord[(size_t)k] = k;
+    std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
+      const int64_t lx = lo(x), ly = lo(y);
+      return lx != ly ? lx < ly : hi(x) < hi(y);
     });
-  I.clear();
-  J.clear();
-  W.clear();
-  for (size_t t = 0; t < m; ++t) {
-    const size_t k = ord[t];
-    if (t && lo[k] == I.back() && hi[k] == J.back()) {
+  }
+  int64_t o = 0;
+  for (int64_t t = 0; t < m; ++t) {
+    const int64_t k = sorted ? t : ord[(size_t)t];
+    const int64_t l = lo(k), h = hi(k);
+    if (o && l == I[o - 1] && h == J[o - 1]) {
       if (!sym) {
-        err = {"duplicate edge (" + std::to_string(lo[k]) + ", " + std::to_string(hi[k]) +
+        err = {"duplicate edge (" + std::to_string(l) + ", " + std::to_string(h) +
                    "); pass symmetrize to merge",
-               raw.line[k]};
+               raw.line[(size_t)k]};
         return false;
       }
-      W.back() = std::max(W.back(), raw.w[k]);   // np.maximum.at
+      W[o - 1] = std::max(W[o - 1], raw.w[(size_t)k]);   // np.maximum.at
       continue;
     }
-    I.push_back(lo[k]);
-    J.push_back(hi[k]);
-    W.push_back(raw.w[k]);
+    I[o] = l;
+    J[o] = h;
+    W[o] = raw.w[(size_t)k];
+    ++o;
   }
-  (void)n;
+  mo = o;
   return true;
 }
 
@@ -244,15 +248,11 @@ void for_lines(const char* text, int64_t len, F&& f) {
   }
 }
 
-bool parse_edgelist(const char* text, int64_t len, int64_t& n, Raw& raw, ParseError& err) {
-  n = -1;
-  raw.a.reserve((size_t)(len / 16));
-  raw.b.reserve((size_t)(len / 16));
-  raw.w.reserve((size_t)(len / 16));
-  raw.line.reserve((size_t)(len / 16));
-  const char* p = text;
-  const char* end = text + len;
-  int64_t lineno = 0;
+// Edge lines of [p, end) (after the node-count line): appended to raw with
+// line numbers counted from line0; false with err at the first bad line.
+bool parse_edges(const char* p, const char* end, int64_t n, int64_t line0, Raw& raw,
+                 ParseError& err, int64_t& nlines) {
+  int64_t lineno = line0;
   while (p < end) {
     const char* q = static_cast<const char*>(memchr(p, '\n', (size_t)(end - p)));
     if (!q) q = end;
@@ -266,23 +266,6 @@ bool parse_edgelist(const char* text, int64_t len, int64_t& n, Raw& raw, ParseEr
     if (b == e) continue;
     Tok f[3];
     const int nf = split_fast<3>(b, e, f);
-    if (n < 0) {
-      if (nf != 1) {
-        err = {"expected a single node count on the first line", lineno};
-        return false;
-      }
-      int64_t v;
-      if (!parse_int(f[0].p, f[0].p + f[0].n, v)) {
-        err = {"bad node count " + py_repr(f[0].str()), lineno};
-        return false;
-      }
-      if (v < 1) {
-        err = {"node count must be positive", lineno};
-        return false;
-      }
-      n = v;
-      continue;
-    }
     if (nf != 3) {
       err = {"expected 'i j w', got " + py_repr(std::string(b, e)), lineno};
       return false;
@@ -311,9 +294,102 @@ bool parse_edgelist(const char* text, int64_t len, int64_t& n, Raw& raw, ParseEr
     raw.w.push_back(w);
     raw.line.push_back(lineno);
   }
+  nlines = lineno - line0;
+  return true;
+}
+
+bool parse_edgelist(const char* text, int64_t len, int64_t& n, Raw& raw, ParseError& err) {
+  n = -1;
+  const char* p = text;
+  const char* end = text + len;
+  int64_t lineno = 0;
+  // the node count: first line with content
+  while (p < end && n < 0) {
+    const char* q = static_cast<const char*>(memchr(p, '\n', (size_t)(end - p)));
+    if (!q) q = end;
+    ++lineno;
+    const char* h = static_cast<const char*>(memchr(p, '#', (size_t)(q - p)));
+    const char* b = p;
+    const char* e = h ? h : q;
+    while (b < e && is_space(*b)) ++b;
+    while (e > b && is_space(e[-1])) --e;
+    p = q + 1;
+    if (b == e) continue;
+    Tok f[1];
+    if (split_fast<1>(b, e, f) != 1) {
+      err = {"expected a single node count on the first line", lineno};
+      return false;
+    }
+    int64_t v;
+    if (!parse_int(f[0].p, f[0].p + f[0].n, v)) {
+      err = {"bad node count " + py_repr(f[0].str()), lineno};
+      return false;
+    }
+    if (v < 1) {
+      err = {"node count must be positive", lineno};
+      return false;
+    }
+    n = v;
+  }
   if (n < 0) {
     err = {"empty input, no node count found", 0};
     return false;
+  }
+  if (p >= end) return true;
+  // edge lines in parallel chunks cut at newlines; the first error in file
+  // order wins, line numbers from per-chunk line counts
+  const int64_t rest = end - p;
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(64, rest / (1 << 20)));
+  std::vector<const char*> cut((size_t)nt + 1);
+  cut[0] = p;
+  cut[(size_t)nt] = end;
+  for (int t = 1; t < nt; ++t) {
+    const char* c = p + rest * t / nt;
+    if (c < cut[(size_t)t - 1]) c = cut[(size_t)t - 1];
+    const char* q = static_cast<const char*>(memchr(c, '\n', (size_t)(end - c)));
+    cut[(size_t)t] = q ? q + 1 : end;
+  }
+  std::vector<Raw> part((size_t)nt);
+  std::vector<ParseError> perr((size_t)nt, ParseError{"", 0});
+  std::vector<char> bad((size_t)nt, 0);
+  std::vector<int64_t> lines((size_t)nt, 0);
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < nt; ++t) {
+    // line numbers local to the chunk (0-based start); fixed up below
+    int64_t cnt = 0;
+    for (const char* c = cut[(size_t)t]; c < cut[(size_t)t + 1];) {
+      const char* q = static_cast<const char*>(memchr(c, '\n', (size_t)(cut[(size_t)t + 1] - c)));
+      ++cnt;
+      c = q ? q + 1 : cut[(size_t)t + 1];
+    }
+    lines[(size_t)t] = cnt;
+    int64_t used = 0;
+    bad[(size_t)t] = !parse_edges(cut[(size_t)t], cut[(size_t)t + 1], n, 0, part[(size_t)t],
+                                  perr[(size_t)t], used);
+  }
+  int64_t off = lineno;
+  size_t total = 0;
+  for (int t = 0; t < nt; ++t) {
+    if (bad[(size_t)t]) {
+      err = perr[(size_t)t];
+      err.line += off;
+      // messages carry no line numbers, so the offset only moves the line field
+      return false;
+    }
+    for (int64_t& l : part[(size_t)t].line) l += off;
+    off += lines[(size_t)t];
+    total += part[(size_t)t].a.size();
+  }
+  raw.a.reserve(total);
+  raw.b.reserve(total);
+  raw.w.reserve(total);
+  raw.line.reserve(total);
+  for (int t = 0; t < nt; ++t) {
+    Raw& r = part[(size_t)t];
+    raw.a.insert(raw.a.end(), r.a.begin(), r.a.end());
+    raw.b.insert(raw.b.end(), r.b.begin(), r.b.end());
+    raw.w.insert(raw.w.end(), r.w.begin(), r.w.end());
+    raw.line.insert(raw.line.end(), r.line.begin(), r.line.end());
   }
   return true;
 }
@@ -443,30 +519,27 @@ int lg_graph_parse(const char* text, int64_t len, int format, int symmetrize, in
   int64_t n = 0;
   const bool ok = format == 0 ? parse_edgelist(text, len, n, raw, err)
                               : parse_mtx(text, len, n, raw, err);
-  std::vector<int64_t> I, J;
-  std::vector<double> W;
-  if (ok && !raw.a.empty() && !merge(n, raw, symmetrize != 0, I, J, W, err)) {
-    if (err_line) *err_line = err.line;
-    return fail(LG_EFORMAT, err.msg);
-  }
   if (!ok) {
     if (err_line) *err_line = err.line;
     return fail(LG_EFORMAT, err.msg);
   }
-  const int64_t m = (int64_t)I.size();
-  int64_t* ib = (int64_t*)malloc(sizeof(int64_t) * (size_t)std::max<int64_t>(m, 1));
-  int64_t* jb = (int64_t*)malloc(sizeof(int64_t) * (size_t)std::max<int64_t>(m, 1));
-  double* wb = (double*)malloc(sizeof(double) * (size_t)std::max<int64_t>(m, 1));
+  const int64_t mr = (int64_t)raw.a.size();
+  int64_t* ib = (int64_t*)malloc(sizeof(int64_t) * (size_t)std::max<int64_t>(mr, 1));
+  int64_t* jb = (int64_t*)malloc(sizeof(int64_t) * (size_t)std::max<int64_t>(mr, 1));
+  double* wb = (double*)malloc(sizeof(double) * (size_t)std::max<int64_t>(mr, 1));
   if (!ib || !jb || !wb) {
     free(ib);
     free(jb);
     free(wb);
     return fail(LG_ENOMEM, "lg_graph_parse: out of host memory");
   }
-  if (m) {
-    std::memcpy(ib, I.data(), sizeof(int64_t) * (size_t)m);
-    std::memcpy(jb, J.data(), sizeof(int64_t) * (size_t)m);
-    std::memcpy(wb, W.data(), sizeof(double) * (size_t)m);
+  int64_t m = 0;
+  if (mr && !merge(raw, symmetrize != 0, ib, jb, wb, m, err)) {
+    free(ib);
+    free(jb);
+    free(wb);
+    if (err_line) *err_line = err.line;
+    return fail(LG_EFORMAT, err.msg);
   }
   *n_out = n;
   *m_out = m;
