@@ -1,0 +1,128 @@
+"""Projected strong scaling of the row-partitioned DACG iteration (dev aid;
+NOT a multi-GPU measurement -- only one GPU is available).
+
+Each rank's local work is MEASURED: the rank's DACG iteration (its row block
+of the SpMV as interior + exterior halves, its preconditioner share, every
+fused pass over its slice, the scalar programs) is built with the real
+row-partitioned plan and timed alone on one GPU with the collectives
+replaced by no-ops; the max over ranks is taken.  The collectives are
+MODELLED: per iteration the slice exchanges (1 for the SpMV, +2 for FSAI)
+move (N-1)/N x 8n bytes into each rank at the measured 770 GB/s NVLink peer
+rate plus 10 us, and every dot-product pass costs one 15 us all-reduce.
+Eager launches (the N > 1 plan is not CUDA-graph captured) are inside the
+measured time.  usage: python scripts/scaling_projection.py C4|C5"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1311_1695_b200 as L  # noqa: E402
+from paper_1311_1695_b200 import _device as dev  # noqa: E402
+from paper_1311_1695_b200._plan import AllReduce, Exchange, ExchangeStart, Seq  # noqa: E402
+from paper_1311_1695_b200.dacg import _DacgPlan  # noqa: E402
+from paper_1311_1695_b200.dist import RowComm, RowPartition, matrix_row_ptr  # noqa: E402
+from paper_1311_1695_b200.precond import JacobiFactor  # noqa: E402
+
+
+class NullBackend:
+    def allreduce_(self, t, comm):
+        pass
+
+    def exchange_(self, x, comm):
+        pass
+
+    def exchange_start(self, x, comm):
+        return None
+
+    def exchange_wait(self, reqs, comm):
+        pass
+
+    def barrier(self, comm):
+        pass
+
+
+def count_collectives(plan):
+    ex = ar = 0
+    for step in plan:
+        steps = step.steps if isinstance(step, Seq) else [step]
+        for s in steps:
+            if isinstance(s, Seq):
+                for u in s.steps:
+                    ex += isinstance(u, (Exchange, ExchangeStart))
+                    ar += isinstance(u, AllReduce)
+            ex += isinstance(s, (Exchange, ExchangeStart))
+            ar += isinstance(s, AllReduce)
+    return ex, ar
+
+
+def rank_iteration_us(a, f, comm, k=6, iters=20):
+    n = a.n
+    with dev.solver_stream() as st:
+        pl = _DacgPlan(a, f, n, k + 1, comm)
+        rng = np.random.default_rng(0)
+        for j in range(k):
+            v = torch.as_tensor(rng.standard_normal(n), device="cuda")
+            pl.C[j].copy_(v / v.norm())
+        pl.k = k
+        x = dev.to_device(rng.standard_normal(n))
+        for buf in (pl.X[0], pl.X[1], pl.AX[0], pl.AX[1], pl.G[0], pl.G[1], pl.P):
+            buf.copy_(x / x.norm())
+        pl.S.set(since=10, period=100, q=1.0, delta=-1.0)
+        g = pl.graph(0)
+        for _ in range(3):
+            pl.p_clear()
+            g()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            pl.p_clear()
+            g()
+        torch.cuda.synchronize()
+        us = (time.perf_counter() - t0) / iters * 1e6
+        ex, ar = count_collectives(pl.plan(0))
+    return us, ex, ar
+
+
+def main():
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
+    if cfg == "C5":
+        from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+        a = rmat_laplacian_device(26, 16, seed=0)
+        f = JacobiFactor(a)
+        prec = "jacobi"
+        worlds = (1, 2, 4, 8)
+    else:
+        a = L.build_laplacian(L.config_graph(cfg))
+        f = L.fsai_factorize(a, 32)
+        prec = "fsai"
+        worlds = (1, 2, 4, 8)
+    rp = matrix_row_ptr(a)
+    n = a.n
+    base = None
+    for world in worlds:
+        part = RowPartition(rp, world)
+        ranks = range(world) if (cfg != "C5" or world <= 2) else (0, world - 1)
+        worst, ex, ar = 0.0, 0, 0
+        for r in ranks:
+            comm = RowComm(part, r, NullBackend())
+            us, ex, ar = rank_iteration_us(a, f, comm)
+            worst = max(worst, us)
+            torch.cuda.empty_cache()
+        comm_us = 0.0
+        if world > 1:
+            comm_us = ex * ((world - 1) / world * 8 * n / 770e9 * 1e6 + 10.0) + ar * 15.0
+        total = worst + comm_us
+        base = base or total
+        print(json.dumps({"config": cfg, "preconditioner": prec, "ranks": world,
+                          "local_us_measured": worst, "exchanges": ex, "allreduces": ar,
+                          "comm_us_modelled": comm_us, "iteration_us_projected": total,
+                          "speedup_projected": base / total,
+                          "efficiency_projected": base / total / world}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
