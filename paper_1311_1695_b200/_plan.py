@@ -348,6 +348,9 @@ class Graph:
     eagerly instead -- same kernels, more host overhead.
     """
 
+    captured = 0     # graphs captured / capture failures (process-wide, for tests)
+    failed = 0
+
     def __init__(self, fns):
         self.fns = list(fns)
         self.exec = None
@@ -361,19 +364,24 @@ class Graph:
         rc = lib.lg_capture_begin(stream)
         if rc != 0:
             self.eager = True
+            Graph.failed += 1
             _graph_note("capture begin failed: " + nat.last_error())
             return
         try:
             for f in self.fns:
                 f(stream=stream)
+        except Exception as exc:   # a launch refused under capture (e.g. a collective)
+            _graph_note(f"capture raised {exc!r}")
         finally:
             rc = lib.lg_capture_end(stream, ctypes.byref(h))
         if rc != 0:
             self.eager = True
+            Graph.failed += 1
             _graph_note("capture failed, replaying eagerly: " + nat.last_error())
             return
         self.exec = h
         self.stream = stream
+        Graph.captured += 1
 
     def __call__(self, stream=None):
         stream = stream if stream is not None else dev.stream_ptr()
@@ -509,13 +517,19 @@ class Ctx:
 
     def __init__(self, n, comm=None):
         self.n = n
-        self.comm = comm if (comm is not None and comm.world > 1) else None
+        self.comm = comm if (comm is not None and (comm.world > 1 or
+                                                    getattr(comm, "force_dist", False))) else None
         self.lo = self.comm.r0 if self.comm else 0
         self.nl = self.comm.nl if self.comm else n
 
     @property
     def dist(self):
         return self.comm is not None
+
+    @property
+    def eager(self):
+        """Launch sequences with collectives that cannot be captured."""
+        return self.comm is not None and not self.comm.graph_safe
 
     def v(self, t):
         """A vector operand restricted to this rank's rows (a tensor, or a raw

@@ -391,8 +391,8 @@ class _DacgPlan:
         g = self.plans.get(key)
         if g is None:
             g = Graph(self.plan(b))
-            if self.cx.dist:
-                g.eager = True   # host-issued collectives inside the iteration
+            if self.cx.eager:
+                g.eager = True   # host-synchronous collectives inside the iteration
             self.plans[key] = g
         return g
 

@@ -124,6 +124,12 @@ class TorchBackend:
 
     def __init__(self, dist):
         self.dist = dist
+        # NCCL collectives are stream-ordered and can be captured into the
+        # solver's CUDA graphs; gloo's are host-synchronous
+        try:
+            self.graph_safe = dist.get_backend() == "nccl"
+        except Exception:
+            self.graph_safe = False
 
     def allreduce_(self, t, comm):
         self.dist.all_reduce(t)
@@ -214,12 +220,20 @@ class RowComm:
         comm = RowComm.from_torch(a, torch.distributed)        # NCCL / gloo
     """
 
-    def __init__(self, part, rank, backend):
+    def __init__(self, part, rank, backend, force_dist=False):
         self.part = part
         self.rank = int(rank)
         self.world = part.world
         self.r0, self.r1 = part.rows(self.rank)
         self.backend = backend
+        # force_dist: run the row-partitioned code path even at one rank
+        # (tests of the collectives' plumbing on a single GPU)
+        self.force_dist = bool(force_dist)
+
+    @property
+    def graph_safe(self):
+        """Collectives can be captured into CUDA graphs (NCCL)."""
+        return bool(getattr(self.backend, "graph_safe", False))
 
     @classmethod
     def from_torch(cls, a, dist):
@@ -231,7 +245,7 @@ class RowComm:
         return self.r1 - self.r0
 
     def allreduce_(self, t):
-        if self.world > 1:
+        if self.world > 1 or self.force_dist:
             self.backend.allreduce_(t, self)
 
     def exchange_(self, x):

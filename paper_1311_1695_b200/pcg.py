@@ -388,8 +388,8 @@ class DevicePcg:
                           skip=stop))
         self.body = body
         self.body_graph = Graph(body)
-        if cx.dist:
-            self.body_graph.eager = True   # host-issued collectives in the body
+        if cx.eager:
+            self.body_graph.eager = True   # host-synchronous collectives in the body
 
     def solve(self, b, qb, tol, maxit, theta=0.0, negate=False):
         """Solve op(x) = (-b if negate else b) from x0 = 0; returns

@@ -9,8 +9,8 @@ replaced by no-ops; the max over ranks is taken.  The collectives are
 MODELLED: per iteration the slice exchanges (1 for the SpMV, +2 for FSAI)
 move (N-1)/N x 8n bytes into each rank at the measured 770 GB/s NVLink peer
 rate plus 10 us, and every dot-product pass costs one 15 us all-reduce.
-Eager launches (the N > 1 plan is not CUDA-graph captured) are inside the
-measured time.  usage: python scripts/scaling_projection.py C4|C5"""
+As with NCCL, the N > 1 iteration is captured into CUDA graphs (collectives
+included; tests/test_gpu_dist.py::test_nccl_collectives_captured_in_solver_graphs).  usage: python scripts/scaling_projection.py C4|C5"""
 import json
 import os
 import sys
@@ -29,6 +29,8 @@ from paper_1311_1695_b200.precond import JacobiFactor  # noqa: E402
 
 
 class NullBackend:
+    graph_safe = True   # as NCCL: the iteration is captured into CUDA graphs
+
     def allreduce_(self, t, comm):
         pass
 

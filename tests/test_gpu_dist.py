@@ -227,3 +227,41 @@ def test_row_partitioned_irlm(world, prec):
     assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-8
     _, res = rayleigh_residuals(a, pairs.vectors)
     assert np.max(res) <= 1.5 * delta
+
+
+def test_nccl_collectives_captured_in_solver_graphs():
+    """With the NCCL backend the row-partitioned DACG iteration -- passes,
+    all-reduces of their dot partials, scalar programs -- is captured into
+    CUDA graphs (no eager fallback).  One rank, forced onto the
+    row-partitioned path; the pairs equal the plain single-GPU solve's."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200._plan import Graph
+    from paper_1311_1695_b200.dist import RowComm, RowPartition, TorchBackend
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        a = _graph()
+        f = L.fsai_factorize(a)
+        ref, rrep = L.dacg_smallest(a, 4, delta=1e-8, f=f, seed=0)
+        comm = RowComm(RowPartition(a.row_ptr, 1), 0, TorchBackend(dist), force_dist=True)
+        assert comm.graph_safe
+        cap0, fail0 = Graph.captured, Graph.failed
+        pairs, rep = L.dacg_smallest(a, 4, delta=1e-8, f=f, seed=0, comm=comm)
+        assert Graph.failed == fail0
+        assert Graph.captured > cap0
+        assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-12
+        assert rep.mvp == rrep.mvp
+    finally:
+        dist.destroy_process_group()
