@@ -196,6 +196,10 @@ int lg_fsai_nnz(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h, int k
 int lg_fsai_factorize(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
                       const double* val_h, int kmax, int64_t* g_row_ptr_h, int64_t* g_col_h,
                       double* g_val_h);
+/* The same preconditioner built on the device for a packed matrix with one
+ * off-diagonal value (unit-weight Laplacians, e.g. the device-built C5), one
+ * warp per row (kmax <= 32); returns G and G^T as plain-format matrices. */
+int lg_fsai_device(const lg_csr* a, int kmax, lg_csr** g_out, lg_csr** gt_out);
 
 /* ---- IC(0) apply (ic0.py:40-45) ---------------------------------------- */
 typedef struct lg_ic0 lg_ic0;

@@ -120,6 +120,7 @@ _SIGS = {
     "lg_graph_parse": (c_int, [c_p, c_i64, c_int, c_int, c_p, c_p, c_p, c_p, c_p, c_p]),
     "lg_host_free": (c_int, [c_p]),
     "lg_fsai_factorize": (c_int, [c_i64, c_p, c_p, c_p, c_int, c_p, c_p, c_p]),
+    "lg_fsai_device": (c_int, [c_p, c_int, c_p, c_p]),
     "lg_spmv_acc": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p]),
     "lg_fused_prog": (c_int, [c_p, c_p, c_p, c_p, c_int, c_p, c_int, c_p, c_p]),
     "lg_gemm_small": (c_int, [c_i64, c_p, c_i64, c_int, c_p, c_int, c_p, c_i64, c_p]),

@@ -1509,3 +1509,312 @@ extern "C" int lg_csr_diagonal(const lg_csr* a, double* d_out) {
 }
 
 }  // extern "C"
+
+// ---- FSAI setup on the device (packed single-valued matrices) -------------
+// The host setup (lg_fsai.cu) needs the matrix on the host; a device-only
+// matrix (C5: 2.1e9 nonzeros built on the GPU) gets the same preconditioner
+// built here, one warp per row:
+//   P_i = the last kmax - 1 strictly lower columns of row i (with a single
+//         off-diagonal value every |a_ij| ties, and the reference tie rule
+//         of lg_fsai.cu keeps the larger columns) + {i};
+//   M = A[P_i, P_i] in shared memory (adjacency by binary search in the rows
+//       of P_i, diagonal from the stored diagonal), right-looking Cholesky
+//       M = C C^T by the warp (lane r owns row r), C C^T g = e_last,
+//   G[i, P_i] = g / sqrt(g_last).
+// Then G^T by a stable radix sort of the entries on their column.  Both come
+// back as plain-format matrices (the apply is lg_spmv on each).
+namespace {
+constexpr int kFsaiMax = 32;   // kmax limit of the device setup (one warp)
+
+__global__ void fsai_count(int64_t n, const int64_t* prp, const uint32_t* pcol, uint32_t cmask,
+                           int kmax, int64_t* cnt) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+    int64_t lo = prp[i], hi = prp[i + 1];
+    while (lo < hi) {   // first column >= i
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)(pcol[mid] & cmask) < i) lo = mid + 1;
+      else hi = mid;
+    }
+    const int64_t low = lo - prp[i];
+    cnt[i] = (low < kmax - 1 ? low : kmax - 1) + 1;
+  }
+}
+
+__device__ __forceinline__ bool has_col(const int64_t* prp, const uint32_t* pcol, uint32_t cmask,
+                                        int64_t r, int64_t c) {
+  int64_t lo = prp[r], hi = prp[r + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int64_t v = pcol[mid] & cmask;
+    if (v == c) return true;
+    if (v < c) lo = mid + 1;
+    else hi = mid;
+  }
+  return false;
+}
+
+constexpr int kFsaiWarps = 4;
+
+__global__ void __launch_bounds__(32 * kFsaiWarps) fsai_rows(
+    int64_t n, const int64_t* prp, const uint32_t* pcol, uint32_t cmask, const double* pdiag,
+    double offv, const int64_t* g_rp, int32_t* g_col, double* g_val, int* bad) {
+  __shared__ double M_sm[kFsaiWarps][kFsaiMax][kFsaiMax + 1];
+  __shared__ int64_t P_sm[kFsaiWarps][kFsaiMax];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double (*M)[kFsaiMax + 1] = M_sm[w];
+  int64_t* P = P_sm[w];
+  const int64_t gw = (int64_t)blockIdx.x * kFsaiWarps + w;
+  const int64_t nw = (int64_t)gridDim.x * kFsaiWarps;
+  for (int64_t i = gw; i < n; i += nw) {
+    const int64_t o = g_rp[i];
+    const int m = (int)(g_rp[i + 1] - o);
+    // pattern: the m - 1 lower columns just below the diagonal's position
+    int64_t lo = prp[i], hi = prp[i + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)(pcol[mid] & cmask) < i) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lane < m - 1) P[lane] = pcol[lo - (m - 1) + lane] & cmask;
+    if (lane == m - 1) P[lane] = i;
+    __syncwarp();
+    if (lane < m) {
+      const int64_t pa = P[lane];
+      for (int b = 0; b < lane; ++b) {
+        const double v = has_col(prp, pcol, cmask, pa, P[b]) ? offv : 0.0;
+        M[lane][b] = v;
+        M[b][lane] = v;
+      }
+      M[lane][lane] = pdiag[pa];
+    }
+    __syncwarp();
+    // right-looking Cholesky, lane r owns row r (lower part)
+    bool ok = true;
+    for (int j = 0; j < m; ++j) {
+      const double d = M[j][j];
+      if (!(d > 0.0)) ok = false;
+      const double c = sqrt(d);
+      __syncwarp();
+      if (lane == j) M[j][j] = c;
+      if (lane > j && lane < m) M[lane][j] /= c;
+      __syncwarp();
+      if (lane > j && lane < m) {
+        const double lj = M[lane][j];
+        for (int k = j + 1; k <= lane; ++k) M[lane][k] -= lj * M[k][j];
+      }
+      __syncwarp();
+    }
+    if (!ok) {
+      if (lane == 0) atomicExch(bad, 1);
+      continue;
+    }
+    // C C^T g = e_last: forward gives y = e_last / C[m-1][m-1]; backward
+    // C^T g = y from the last row up, one warp reduction per row
+    const double cl = M[m - 1][m - 1];
+    double g_mine = (lane == m - 1) ? 1.0 / (cl * cl) : 0.0;
+    for (int r = m - 2; r >= 0; --r) {
+      double t = (lane > r && lane < m) ? M[lane][r] * g_mine : 0.0;
+      t = warp_sum(t);
+      if (lane == r) g_mine = -t / M[r][r];
+    }
+    // G row = g / sqrt(g_last), sqrt(g_last) = 1 / C[m-1][m-1]
+    if (lane < m) {
+      g_col[o + lane] = (int32_t)P[lane];
+      g_val[o + lane] = g_mine * cl;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void gather_rows_vals(int64_t nnz, const int64_t* idx, const int32_t* rows,
+                                 const double* vals, int32_t* rows_out, double* vals_out) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += st) {
+    rows_out[e] = rows[idx[e]];
+    vals_out[e] = vals[idx[e]];
+  }
+}
+
+__global__ void expand_rows(int64_t n, const int64_t* rp, int32_t* row_of) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) row_of[k] = (int32_t)i;
+}
+
+__global__ void iota64(int64_t m, int64_t* v) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += st) v[e] = e;
+}
+
+__global__ void count_cols(int64_t m, const int32_t* col, unsigned long long* cnt) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += st)
+    atomicAdd(cnt + col[e] + 1, 1ull);
+}
+
+int grid_of(int64_t work, int per) {
+  const int64_t g = (work + per - 1) / per;
+  const int64_t cap = (int64_t)dev_info().sm_count * 32;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+}  // namespace
+
+// A plain-format n x n matrix over device arrays (taken over: freed with the
+// handle); the schedule is built from the row pointers copied to the host.
+static int plain_from_device(int64_t n, int64_t* rp, int32_t* col, double* val, int64_t nnz,
+                             lg_csr** out) {
+  std::vector<int64_t> hrp((size_t)n + 1);
+  LG_CUDA(cudaMemcpy(hrp.data(), rp, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost));
+  std::vector<SpmvBlock> blocks;
+  std::vector<int32_t> lnp;
+  std::vector<int64_t> lfirst;
+  lg_csr* a = new lg_csr();
+  a->n = n;
+  a->nnz = nnz;
+  a->cta = pick_cta(nnz);
+  build_schedule(n, hrp.data(), a->cta, blocks, lnp, lfirst);
+  a->row_ptr = rp;
+  a->col = col;
+  a->val = val;
+  a->nblocks = (int64_t)blocks.size();
+  set_chunks(a, blocks);
+  a->nlong = (int64_t)lnp.size();
+  for (int32_t v : lnp) a->nparts += v;
+  if ((a->nblocks &&
+       cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess) ||
+      (a->nlong && (cudaMalloc(&a->long_nparts, 4 * (size_t)a->nlong) != cudaSuccess ||
+                    cudaMalloc(&a->long_first, 8 * (size_t)a->nlong) != cudaSuccess))) {
+    lg_csr_destroy(a);
+    return fail(LG_ENOMEM, "fsai: schedule alloc");
+  }
+  if (a->nblocks)
+    cudaMemcpy(a->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
+  if (a->nlong) {
+    cudaMemcpy(a->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(a->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
+  }
+  *out = a;
+  return LG_OK;
+}
+
+extern "C" int lg_fsai_device(const lg_csr* a, int kmax, lg_csr** g_out, lg_csr** gt_out) {
+  if (!a || !g_out || !gt_out || kmax < 1 || kmax > kFsaiMax)
+    return fail(LG_EINVAL, "lg_fsai_device: bad argument (1 <= kmax <= 32)");
+  if (!a->packed || a->nvals != 1)
+    return fail(LG_EINVAL, "lg_fsai_device: needs a packed matrix with one off-diagonal value "
+                           "(use the host setup, lg_fsai_factorize, otherwise)");
+  const int64_t n = a->n;
+  const uint32_t cmask = (a->cbits >= 32) ? 0xffffffffu : ((1u << a->cbits) - 1u);
+  double offv = 0.0;
+  LG_CUDA(cudaMemcpy(&offv, a->table, 8, cudaMemcpyDeviceToHost));
+  int64_t *cnt = nullptr, *grp = nullptr, *idx = nullptr, *idx2 = nullptr, *trp = nullptr;
+  int32_t *gcol = nullptr, *grow = nullptr, *tcol_keys = nullptr, *trow = nullptr;
+  double *gval = nullptr, *tval = nullptr;
+  unsigned long long* ccount = nullptr;
+  int* bad = nullptr;
+  void* tmp = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(cnt);
+    cudaFree(idx);
+    cudaFree(idx2);
+    cudaFree(grow);
+    cudaFree(tcol_keys);
+    cudaFree(ccount);
+    cudaFree(bad);
+    cudaFree(tmp);
+  };
+  auto oom = [&](const char* what) {
+    cleanup();
+    cudaFree(grp);
+    cudaFree(gcol);
+    cudaFree(gval);
+    cudaFree(trp);
+    cudaFree(trow);
+    cudaFree(tval);
+    return fail(LG_ENOMEM, std::string("lg_fsai_device: ") + what);
+  };
+  if (cudaMalloc(&cnt, 8 * (size_t)n) != cudaSuccess ||
+      cudaMalloc(&grp, 8 * (size_t)(n + 1)) != cudaSuccess ||
+      cudaMalloc(&bad, sizeof(int)) != cudaSuccess)
+    return oom("allocation");
+  cudaMemset(bad, 0, sizeof(int));
+  fsai_count<<<grid_of(n, 256), 256>>>(n, a->prp, a->pcol, cmask, kmax, cnt);
+  size_t tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, cnt, grp + 1, n);
+  if (cudaMalloc(&tmp, std::max<size_t>(tb, 16)) != cudaSuccess) return oom("scan scratch");
+  cudaMemset(grp, 0, 8);
+  cub::DeviceScan::InclusiveSum(tmp, tb, cnt, grp + 1, n);
+  cudaFree(tmp);
+  tmp = nullptr;
+  int64_t nnz = 0;
+  LG_CUDA(cudaMemcpy(&nnz, grp + n, 8, cudaMemcpyDeviceToHost));
+  if (cudaMalloc(&gcol, 4 * (size_t)nnz) != cudaSuccess ||
+      cudaMalloc(&gval, 8 * (size_t)nnz) != cudaSuccess)
+    return oom("G arrays");
+  {
+    const int64_t blocks = std::min<int64_t>((n + kFsaiWarps - 1) / kFsaiWarps,
+                                             (int64_t)dev_info().sm_count * 64);
+    fsai_rows<<<(unsigned)std::max<int64_t>(blocks, 1), 32 * kFsaiWarps>>>(
+        n, a->prp, a->pcol, cmask, a->pdiag, offv, grp, gcol, gval, bad);
+  }
+  int hbad = 0;
+  LG_CUDA(cudaMemcpy(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost));
+  if (hbad) {
+    cleanup();
+    cudaFree(grp);
+    cudaFree(gcol);
+    cudaFree(gval);
+    return fail(LG_EBREAKDOWN, "lg_fsai_device: a row's pattern submatrix is not positive "
+                               "definite");
+  }
+  // G^T: entries sorted (stably) by column; row indices and values follow
+  if (cudaMalloc(&grow, 4 * (size_t)nnz) != cudaSuccess ||
+      cudaMalloc(&idx, 8 * (size_t)nnz) != cudaSuccess ||
+      cudaMalloc(&idx2, 8 * (size_t)nnz) != cudaSuccess ||
+      cudaMalloc(&tcol_keys, 4 * (size_t)nnz) != cudaSuccess ||
+      cudaMalloc(&trow, 4 * (size_t)nnz) != cudaSuccess ||
+      cudaMalloc(&tval, 8 * (size_t)nnz) != cudaSuccess ||
+      cudaMalloc(&trp, 8 * (size_t)(n + 1)) != cudaSuccess ||
+      cudaMalloc(&ccount, 8 * (size_t)(n + 1)) != cudaSuccess)
+    return oom("G^T arrays");
+  expand_rows<<<grid_of(n, 256), 256>>>(n, grp, grow);
+  iota64<<<grid_of(nnz, 256), 256>>>(nnz, idx);
+  int cbits = 1;
+  while (((int64_t)1 << cbits) < n) ++cbits;
+  tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, gcol, tcol_keys, idx, idx2, nnz, 0, cbits);
+  if (cudaMalloc(&tmp, std::max<size_t>(tb, 16)) != cudaSuccess) return oom("sort scratch");
+  cub::DeviceRadixSort::SortPairs(tmp, tb, gcol, tcol_keys, idx, idx2, nnz, 0, cbits);
+  gather_rows_vals<<<grid_of(nnz, 256), 256>>>(nnz, idx2, grow, gval, trow, tval);
+  cudaMemset(ccount, 0, 8 * (size_t)(n + 1));
+  count_cols<<<grid_of(nnz, 256), 256>>>(nnz, gcol, ccount);
+  cudaFree(tmp);
+  tmp = nullptr;
+  tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, ccount, (unsigned long long*)trp, n + 1);
+  if (cudaMalloc(&tmp, std::max<size_t>(tb, 16)) != cudaSuccess) return oom("scan scratch");
+  cub::DeviceScan::InclusiveSum(tmp, tb, ccount, (unsigned long long*)trp, n + 1);
+  cudaError_t e = cudaDeviceSynchronize();
+  cleanup();
+  if (e != cudaSuccess) {
+    cudaFree(grp);
+    cudaFree(gcol);
+    cudaFree(gval);
+    cudaFree(trp);
+    cudaFree(trow);
+    cudaFree(tval);
+    return fail(LG_ECUDA, std::string("lg_fsai_device: ") + cudaGetErrorString(e));
+  }
+  lg_csr *g = nullptr, *gt = nullptr;
+  int rc = plain_from_device(n, grp, gcol, gval, nnz, &g);
+  if (rc) return rc;
+  rc = plain_from_device(n, trp, trow, tval, nnz, &gt);
+  if (rc) {
+    lg_csr_destroy(g);
+    return rc;
+  }
+  *g_out = g;
+  *gt_out = gt;
+  return LG_OK;
+}

@@ -395,6 +395,9 @@ class DistFsai:
 
     def __init__(self, f, comm):
         from . import _device as dev
+        if f.g is None:
+            raise ValueError("row-partitioned FSAI needs the factor on the host "
+                             "(a device-built FsaiFactor is single-GPU only)")
         self.f = f
         self.comm = comm
         self.g = local_operator(f.g, comm.part, comm.rank)

@@ -121,6 +121,33 @@ class FsaiFactor:
         self._dev_ready = False
         self._DeviceCsr = DeviceCsr
 
+    @classmethod
+    def from_device(cls, a, kmax=32):
+        """The FSAI of a device-only packed matrix with one off-diagonal
+        value (a unit-weight Laplacian such as rmat_laplacian_device's),
+        built on the device (lg_fsai_device).  Single-GPU only (no host
+        copy of G for row-partitioned solves)."""
+        import ctypes
+
+        from .sparse import DeviceCsr
+        d = a.device()
+        hg, hgt = ctypes.c_void_p(), ctypes.c_void_p()
+        nat.call("lg_fsai_device", d.handle, int(kmax), ctypes.byref(hg), ctypes.byref(hgt))
+        self = cls.__new__(cls)
+        self.n = int(a.n)
+        self.kmax = int(kmax)
+        self.shift = 0.0
+        self.attempts = 0
+        self.g = self.gt = None
+        self._DeviceCsr = DeviceCsr
+        info = [ctypes.c_int64() for _ in range(4)] + [ctypes.c_int(), ctypes.c_int64()]
+        nat.call("lg_csr_info", hg, *[ctypes.byref(v) for v in info])
+        self._dg = DeviceCsr.from_handle(hg, self.n, info[1].value)
+        self._dgt = DeviceCsr.from_handle(hgt, self.n, info[1].value)
+        self._tmp = dev.empty(self.n)
+        self._dev_ready = True
+        return self
+
     def _ensure(self):
         if not self._dev_ready:
             self._dg = self._DeviceCsr(self.n, self.g.row_ptr, self.g.col_idx, self.g.values)

@@ -10,7 +10,7 @@ residual-certified: every returned pair is re-verified with fresh products
 the constant kernel vector are measured, and the smallest pairs are
 cross-checked against JD when --jd is given.
 
-usage: python scripts/c5_dacg.py [scale=26] [edge_factor=16] [neig=5] [--jd]
+usage: python scripts/c5_dacg.py [scale=26] [edge_factor=16] [neig=5] [--jd] [--fsai]
 Prints one JSON line (profiles/ keeps the round's copy).
 """
 import json
@@ -40,11 +40,21 @@ def main():
     A = rmat_laplacian_device(scale, ef, seed=0)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
-    f = JacobiFactor(A)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if "--fsai" in sys.argv:
+        from paper_1311_1695_b200.precond import FsaiFactor
+        f = FsaiFactor.from_device(A, kmax=32)
+        label = "fsai kmax 32, device setup (flagged; reference IC(0) infeasible)"
+    else:
+        f = JacobiFactor(A)
+        label = "jacobi (flagged; reference IC(0) infeasible)"
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
     out = {"workload": f"R-MAT scale {scale} ef {ef} (a,b,c)=(.57,.19,.19), LCC, unit weights, "
                        "device-built", "n": A.n, "m": A.m, "nnz": A.nnz, "neig": neig,
-           "delta": delta, "preconditioner": "jacobi (flagged; reference IC(0) infeasible)",
-           "build_s": t_build}
+           "delta": delta, "preconditioner": label, "build_s": t_build,
+           "preconditioner_setup_s": t_setup}
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     pairs, rep = L.dacg_smallest(A, neig, delta=delta, f=f, seed=0)

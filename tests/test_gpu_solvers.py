@@ -218,3 +218,25 @@ def test_fsai_variant_converges_to_same_pairs(L, cfg):
     for sv in ("dacg", "jd"):
         pairs, rep = solver(L, sv)(a, ref["neig"], delta=ref["delta"], f=f)
         check_pairs(L, a, pairs, np.asarray(ref["solvers"][sv]["eigenvalues"]), ref["delta"])
+
+
+def test_fsai_device_setup_matches_host(L):
+    """lg_fsai_device (one warp per row, for packed single-valued matrices)
+    builds the same preconditioner as the host setup: the applies agree to
+    roundoff on C2 (unit weights); on a device-only R-MAT Laplacian DACG with
+    it returns the Jacobi-preconditioned solve's pairs."""
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.precond import FsaiFactor, JacobiFactor
+    a = L.build_laplacian(L.config_graph("C2"))
+    fh = FsaiFactor(a, kmax=32)
+    fd = FsaiFactor.from_device(a, kmax=32)
+    r = np.random.default_rng(6).standard_normal(a.n)
+    zh, zd = fh.apply(r), fd.apply(r)
+    assert np.max(np.abs(zh - zd)) <= 1e-12 * np.max(np.abs(zh))
+    A = rmat_laplacian_device(14, 8, seed=3)
+    fj = JacobiFactor(A)
+    ff = FsaiFactor.from_device(A, kmax=32)
+    pj, rj = L.dacg_smallest(A, 3, delta=1e-8, f=fj, seed=0)
+    pf, rf = L.dacg_smallest(A, 3, delta=1e-8, f=ff, seed=0)
+    assert np.max(np.abs(pf.values - pj.values) / pj.values) <= 1e-8
+    assert rf.mvp < rj.mvp
