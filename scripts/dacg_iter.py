@@ -7,7 +7,7 @@ from paper_1311_1695_b200.dacg import _DacgPlan
 from paper_1311_1695_b200._plan import Fused, Spmv
 name = sys.argv[1] if len(sys.argv) > 1 else "C1"
 a = L.build_laplacian(L.config_graph(name))
-for lab, f in (("ic0", L.ic0_factorize(a)), ("mc", L.ic0_factorize_multicolor(a))):
+for lab, f in (("ic0", L.ic0_factorize(a)), ("mc", L.ic0_factorize_multicolor(a)), ("fsai", L.fsai_factorize(a, 32))):
     with dev.solver_stream() as st:
         pl = _DacgPlan(a, f, a.n, 11)
         pl.C[0] = 1.0 / np.sqrt(a.n)
