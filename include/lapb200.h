@@ -191,11 +191,14 @@ int lg_host_free(void* p);
  * |a_ij|), each row from one dense SPD solve A[P_i, P_i] g = e_last scaled by
  * 1 / sqrt(g_last).  Host setup, OpenMP over rows; the apply is two device
  * SpMVs (lg_csr of G and of G^T).  lg_fsai_nnz gives the size of G. */
-int lg_fsai_nnz(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h, int kmax,
-                int64_t* nnz);
+int lg_fsai_nnz(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
+                const double* val_h, int kmax, int levels, int64_t* nnz);
+/* levels 2 ("FSAI(2)"): the pattern also takes second-level neighbours j < i,
+ * scored by |a_ij| + sum_k |a_ik||a_kj| (k over neighbours of i with at most
+ * 64 entries), the kmax - 1 best kept. */
 int lg_fsai_factorize(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
-                      const double* val_h, int kmax, int64_t* g_row_ptr_h, int64_t* g_col_h,
-                      double* g_val_h);
+                      const double* val_h, int kmax, int levels, int64_t* g_row_ptr_h,
+                      int64_t* g_col_h, double* g_val_h);
 /* The same preconditioner built on the device for a packed matrix with one
  * off-diagonal value (unit-weight Laplacians, e.g. the device-built C5), one
  * warp per row (kmax <= 32); returns G and G^T as plain-format matrices. */

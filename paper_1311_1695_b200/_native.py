@@ -116,10 +116,10 @@ _SIGS = {
     "lg_csr_row_block": (c_int, [c_p, c_i64, c_i64, c_p]),
     "lg_csr_row_ptr": (c_int, [c_p, c_p]),
     "lg_csr_split_cols": (c_int, [c_p, c_i64, c_i64, c_p, c_p]),
-    "lg_fsai_nnz": (c_int, [c_i64, c_p, c_p, c_int, c_p]),
+    "lg_fsai_nnz": (c_int, [c_i64, c_p, c_p, c_p, c_int, c_int, c_p]),
     "lg_graph_parse": (c_int, [c_p, c_i64, c_int, c_int, c_p, c_p, c_p, c_p, c_p, c_p]),
     "lg_host_free": (c_int, [c_p]),
-    "lg_fsai_factorize": (c_int, [c_i64, c_p, c_p, c_p, c_int, c_p, c_p, c_p]),
+    "lg_fsai_factorize": (c_int, [c_i64, c_p, c_p, c_p, c_int, c_int, c_p, c_p, c_p]),
     "lg_fsai_device": (c_int, [c_p, c_int, c_p, c_p]),
     "lg_spmv_acc": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p]),
     "lg_fused_prog": (c_int, [c_p, c_p, c_p, c_p, c_int, c_p, c_int, c_p, c_p]),

@@ -88,7 +88,7 @@ class FsaiFactor:
     stream at a time.
     """
 
-    def __init__(self, a, kmax=64):
+    def __init__(self, a, kmax=32, levels=1):
         import ctypes
 
         from .sparse import CsrMatrix, DeviceCsr
@@ -98,16 +98,18 @@ class FsaiFactor:
         val = np.ascontiguousarray(a.values, dtype=np.float64)
         nnz = ctypes.c_int64()
         nat.call("lg_fsai_nnz", n, rp.ctypes.data, col.ctypes.data if col.size else None,
-                 int(kmax), ctypes.byref(nnz))
+                 val.ctypes.data if val.size else None, int(kmax), int(levels),
+                 ctypes.byref(nnz))
         grp = np.zeros(n + 1, dtype=np.int64)
         gcol = np.zeros(max(nnz.value, 1), dtype=np.int64)
         gval = np.zeros(max(nnz.value, 1), dtype=np.float64)
         nat.call("lg_fsai_factorize", n, rp.ctypes.data, col.ctypes.data if col.size else None,
-                 val.ctypes.data if val.size else None, int(kmax), grp.ctypes.data,
+                 val.ctypes.data if val.size else None, int(kmax), int(levels), grp.ctypes.data,
                  gcol.ctypes.data, gval.ctypes.data)
         gcol, gval = gcol[:nnz.value], gval[:nnz.value]
         self.n = n
         self.kmax = int(kmax)
+        self.levels = int(levels)
         self.shift = 0.0
         self.attempts = 0
         self.g = CsrMatrix(n, grp, gcol, gval)
@@ -179,9 +181,10 @@ class FsaiFactor:
         return out if on_dev else dev.to_host(out)
 
 
-def fsai_factorize(a, kmax=64):
-    """FSAI preconditioner of a (flagged non-reference variant)."""
-    return FsaiFactor(a, kmax)
+def fsai_factorize(a, kmax=32, levels=1):
+    """FSAI preconditioner of a (flagged non-reference variant); levels=2
+    widens each row's pattern to second-level neighbours (FSAI(2))."""
+    return FsaiFactor(a, kmax, levels)
 
 
 class CallablePrec:

@@ -20,13 +20,10 @@ for cfg in sys.argv[1:] or ["C2", "C3", "C4"]:
     t0 = time.perf_counter()
     precs = {"ic0": L.ic0_factorize(a)}
     setup = {"ic0": time.perf_counter() - t0}
-    for k in (32, 64):
+    for k, lv in ((32, 1), (8, 2), (16, 2), (32, 2)):
         t0 = time.perf_counter()
-        precs[f"fsai{k}"] = L.fsai_factorize(a, kmax=k)
-        setup[f"fsai{k}"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    precs["mc"] = L.ic0_factorize_multicolor(a)
-    setup["mc"] = time.perf_counter() - t0
+        precs[f"fsai{k}_l{lv}"] = L.fsai_factorize(a, kmax=k, levels=lv)
+        setup[f"fsai{k}_l{lv}"] = time.perf_counter() - t0
     for p in precs.values():
         p.device()
     for sv, fn in (("dacg", L.dacg_smallest), ("jd", L.jd_smallest)):

@@ -328,3 +328,48 @@ def test_graph_loader_paths_streams_and_round_trip(tmp_path):
     assert count == 3 and labels.tolist() == [0, 0, 0, 1, 1, 2]
     with pytest.raises(ValueError):
         L.load_edge_list(b"", format="csv")
+
+
+def test_fsai2_pattern_and_rows():
+    """FSAI(2) (levels=2): each row's pattern is the kmax - 1 best lower
+    candidates by |a_ij| + sum_k |a_ik||a_kj| (k: neighbours with at most
+    64 entries), ties to the larger column, plus the diagonal; the rows solve
+    A[P, P] g = e_last (diag(G A G^T) = 1)."""
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200.generators import chung_lu_graph
+    from paper_1311_1695_b200.graphs import largest_component
+    from paper_1311_1695_b200.precond import FsaiFactor
+    from paper_1311_1695_b200.sparse import CsrMatrix
+    g, _ = largest_component(chung_lu_graph(400, 2.1, 5.0, max_degree=80, weighted=True, seed=8))
+    rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+    a = CsrMatrix(g.n_nodes, rp, col, val)
+    n, kmax = a.n, 8
+    f = FsaiFactor(a, kmax=kmax, levels=2)
+    A = np.zeros((n, n))
+    for r in range(n):
+        A[r, col[rp[r]:rp[r + 1]]] = val[rp[r]:rp[r + 1]]
+    deg = np.diff(rp)
+    for i in range(n):
+        score = {}
+        for q in range(rp[i], rp[i + 1]):
+            k = col[q]
+            if k == i:
+                continue
+            if k < i:
+                score[k] = score.get(k, 0.0) + abs(val[q])
+            if deg[k] > 64:
+                continue
+            for t in range(rp[k], rp[k + 1]):
+                j = col[t]
+                if j < i and j != k:
+                    score[j] = score.get(j, 0.0) + abs(val[q]) * abs(val[t])
+        best = sorted(score.items(), key=lambda kv: (-kv[1], -kv[0]))[:kmax - 1]
+        P = sorted(j for j, _ in best) + [i]
+        got = f.g.col_idx[f.g.row_ptr[i]:f.g.row_ptr[i + 1]].tolist()
+        assert got == P, (i, got, P)
+        e = np.zeros(len(P))
+        e[-1] = 1.0
+        gw = np.linalg.solve(A[np.ix_(P, P)], e)
+        gw /= np.sqrt(gw[-1])
+        gv = f.g.values[f.g.row_ptr[i]:f.g.row_ptr[i + 1]]
+        assert np.max(np.abs(gv - gw)) <= 1e-10 * np.max(np.abs(gw))
