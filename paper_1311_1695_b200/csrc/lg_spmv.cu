@@ -1213,6 +1213,63 @@ extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
   return LG_OK;
 }
 
+// Rows [r0, r1) of a plain-format matrix (e.g. a device-built FSAI factor)
+// as an n x n plain matrix whose other rows are absent from the schedule.
+static int plain_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** out) {
+  if (!a->row_ptr) return fail(LG_EINVAL, "lg_csr_row_block: matrix has no plain arrays");
+  const int64_t n = a->n, nloc = r1 - r0;
+  std::vector<int64_t> lrp((size_t)nloc + 1);
+  LG_CUDA(cudaMemcpy(lrp.data(), a->row_ptr + r0, 8 * (size_t)(nloc + 1),
+                     cudaMemcpyDeviceToHost));
+  const int64_t off0 = lrp[0], m = lrp[(size_t)nloc] - off0;
+  std::vector<int64_t> rp((size_t)n + 1, 0);
+  for (int64_t i = 0; i < nloc; ++i) rp[(size_t)(r0 + i + 1)] = lrp[(size_t)i + 1] - off0;
+  for (int64_t r = r1 + 1; r <= n; ++r) rp[(size_t)r] = m;
+  std::vector<char> absent((size_t)n, 1);
+  for (int64_t r = r0; r < r1; ++r) absent[(size_t)r] = 0;
+  std::vector<SpmvBlock> blocks;
+  std::vector<int32_t> lnp;
+  std::vector<int64_t> lfirst;
+  build_schedule(n, rp.data(), a->cta, blocks, lnp, lfirst, &absent);
+  lg_csr* b = new lg_csr();
+  b->cta = a->cta;
+  b->n = n;
+  b->nnz = m;
+  b->nblocks = (int64_t)blocks.size();
+  set_chunks(b, blocks);
+  b->nlong = (int64_t)lnp.size();
+  for (int32_t v : lnp) b->nparts += v;
+  bool ok = cudaMalloc(&b->row_ptr, 8 * (size_t)(n + 1)) == cudaSuccess &&
+            cudaMalloc(&b->col, 4 * (size_t)std::max<int64_t>(m, 1)) == cudaSuccess &&
+            cudaMalloc(&b->val, 8 * (size_t)std::max<int64_t>(m, 1)) == cudaSuccess &&
+            (b->nblocks == 0 ||
+             cudaMalloc(&b->blocks, sizeof(SpmvBlock) * (size_t)b->nblocks) == cudaSuccess) &&
+            (b->nlong == 0 || (cudaMalloc(&b->long_nparts, 4 * (size_t)b->nlong) == cudaSuccess &&
+                               cudaMalloc(&b->long_first, 8 * (size_t)b->nlong) == cudaSuccess));
+  if (!ok) {
+    lg_csr_destroy(b);
+    return fail(LG_ENOMEM, "lg_csr_row_block: allocation failed");
+  }
+  cudaMemcpy(b->row_ptr, rp.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice);
+  if (m) {
+    cudaMemcpy(b->col, a->col + off0, 4 * (size_t)m, cudaMemcpyDeviceToDevice);
+    cudaMemcpy(b->val, a->val + off0, 8 * (size_t)m, cudaMemcpyDeviceToDevice);
+  }
+  if (b->nblocks)
+    cudaMemcpy(b->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
+  if (b->nlong) {
+    cudaMemcpy(b->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(b->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
+  }
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    lg_csr_destroy(b);
+    return fail(LG_ECUDA, std::string("lg_csr_row_block: ") + cudaGetErrorString(err));
+  }
+  *out = b;
+  return LG_OK;
+}
+
 // ---- one rank's row block (multi-GPU) --------------------------------------
 // Rows [r0, r1) of a packed matrix as a packed n x n matrix whose other rows
 // are absent from the schedule (lg_spmv leaves y there untouched): the
@@ -1222,7 +1279,7 @@ extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
 extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** out) {
   if (!a || !out || r0 < 0 || r1 < r0 || r1 > a->n)
     return fail(LG_EINVAL, "lg_csr_row_block: bad argument");
-  if (!a->packed) return fail(LG_EINVAL, "lg_csr_row_block: only for packed matrices");
+  if (!a->packed) return plain_row_block(a, r0, r1, out);
   const int64_t n = a->n, nloc = r1 - r0;
   std::vector<int64_t> lrp((size_t)nloc + 1);
   LG_CUDA(cudaMemcpy(lrp.data(), a->prp + r0, 8 * (size_t)(nloc + 1), cudaMemcpyDeviceToHost));

@@ -287,22 +287,26 @@ class RowComm:
         return local_operator_device(a.device(), self.part, self.rank)
 
     def local_preconditioner(self, a, f):
-        """The rank-local preconditioner for the solver seam `f`:
-        JacobiFactor -> its slice; None / 'block_ic0' -> block-Jacobi IC(0)
-        of the diagonal block (Jacobi for device-only matrices); 'jacobi'."""
+        """The rank-local preconditioner for the solver seam `f`: None /
+        'fsai' / an FsaiFactor -> FSAI as row-partitioned SpMVs (the same
+        preconditioner at every N; device-built for device-only matrices);
+        'block_ic0' -> block-Jacobi IC(0) of the diagonal block; 'jacobi' /
+        a JacobiFactor -> its slice."""
         from .precond import FsaiFactor, JacobiFactor
         host = hasattr(a, "row_ptr") and getattr(a, "col_idx", None) is not None
         if f is None:
-            f = "fsai" if host else "jacobi"
+            f = "fsai"
         if isinstance(f, str):
             if f == "jacobi":
                 f = JacobiFactor(a)
-            elif f in ("block_ic0", "fsai") and not host:
-                raise ValueError(f"{f} needs the matrix on the host")
+            elif f == "block_ic0" and not host:
+                raise ValueError("block_ic0 needs the matrix on the host")
             elif f == "block_ic0":
                 return BlockJacobiIc0(a, self)
             elif f == "fsai":
-                f = FsaiFactor(a)
+                # device-only matrices (one off-diagonal value) get the
+                # device-built factor
+                f = FsaiFactor(a) if host else FsaiFactor.from_device(a)
             else:
                 raise ValueError(f"unknown distributed preconditioner {f!r}")
         if isinstance(f, JacobiFactor):
@@ -395,13 +399,15 @@ class DistFsai:
 
     def __init__(self, f, comm):
         from . import _device as dev
-        if f.g is None:
-            raise ValueError("row-partitioned FSAI needs the factor on the host "
-                             "(a device-built FsaiFactor is single-GPU only)")
         self.f = f
         self.comm = comm
-        self.g = local_operator(f.g, comm.part, comm.rank)
-        self.gt = local_operator(f.gt, comm.part, comm.rank)
+        if f.g is not None:
+            self.g = local_operator(f.g, comm.part, comm.rank)
+            self.gt = local_operator(f.gt, comm.part, comm.rank)
+        else:   # built on the device (FsaiFactor.from_device): cut on the device
+            f._ensure()
+            self.g = local_operator_device(f._dg, comm.part, comm.rank)
+            self.gt = local_operator_device(f._dgt, comm.part, comm.rank)
         self.t = dev.zeros(f.n)
         self.n = f.n
 

@@ -265,3 +265,42 @@ def test_nccl_collectives_captured_in_solver_graphs():
         assert rep.mvp == rrep.mvp
     finally:
         dist.destroy_process_group()
+
+
+def test_row_partitioned_dacg_device_fsai():
+    """A device-only matrix with its FSAI built on the device
+    (FsaiFactor.from_device): each rank cuts its rows of G and G^T on the
+    device; the MVP count and pairs equal the single-GPU solve's."""
+    import torch
+
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.dist import RowComm, RowPartition, ThreadWorld, matrix_row_ptr
+    from paper_1311_1695_b200.precond import FsaiFactor
+    A = rmat_laplacian_device(14, 8, seed=3)
+    f = FsaiFactor.from_device(A, kmax=32)
+    ref, rrep = L.dacg_smallest(A, 3, delta=1e-8, f=f, seed=0)
+    world = 2
+    tw = ThreadWorld(world)
+    part = RowPartition(matrix_row_ptr(A), world)
+    out, errs = [None] * world, []
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = L.dacg_smallest(A, 3, delta=1e-8, f=f, seed=0, comm=RowComm(part, r, tw))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            tw.bar.abort()
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    if errs:
+        raise errs[0]
+    pairs, rep = out[0]
+    assert np.array_equal(pairs.values, out[1][0].values)
+    assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-8
+    assert abs(rep.mvp - rrep.mvp) <= 0.03 * rrep.mvp + 3
