@@ -10,7 +10,7 @@ MODELLED: per iteration the slice exchanges (1 for the SpMV, +2 for FSAI)
 move (N-1)/N x 8n bytes into each rank at the measured 770 GB/s NVLink peer
 rate plus 10 us, and every dot-product pass costs one 15 us all-reduce.
 As with NCCL, the N > 1 iteration is captured into CUDA graphs (collectives
-included; tests/test_gpu_dist.py::test_nccl_collectives_captured_in_solver_graphs).  usage: python scripts/scaling_projection.py C4|C5"""
+included; tests/test_gpu_dist.py::test_nccl_collectives_captured_in_solver_graphs).  usage: python scripts/scaling_projection.py C4|C5 [--jacobi]"""
 import json
 import os
 import sys
@@ -94,8 +94,11 @@ def main():
     if cfg == "C5":
         from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
         a = rmat_laplacian_device(26, 16, seed=0)
-        f = JacobiFactor(a)
-        prec = "jacobi"
+        if "--jacobi" in sys.argv:
+            f, prec = JacobiFactor(a), "jacobi"
+        else:
+            from paper_1311_1695_b200.precond import FsaiFactor
+            f, prec = FsaiFactor.from_device(a, kmax=32), "fsai"
         worlds = (1, 2, 4, 8)
     else:
         a = L.build_laplacian(L.config_graph(cfg))
