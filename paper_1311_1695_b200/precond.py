@@ -84,8 +84,8 @@ class FsaiFactor:
     most kmax entries per row (hub rows keep their kmax - 1 largest |a_ij|);
     the apply is two SpMVs -- no triangular dependency chain, and across GPUs
     two row-partitioned SpMVs without the block-Jacobi loss.  Same .apply
-    seam as Ic0Factor.  The scratch vector makes one factor usable by one
-    stream at a time.
+    seam as Ic0Factor.  Scratch is per thread, so a factor can be shared by
+    solves on different threads.
     """
 
     def __init__(self, a, kmax=32, levels=1):
@@ -158,12 +158,22 @@ class FsaiFactor:
             self._tmp = dev.empty(self.n)
             self._dev_ready = True
 
+    def _scratch(self):
+        """G r of the apply: one scratch vector per thread, so solves on
+        different threads (streams) can share the factor."""
+        import threading
+        tls = self.__dict__.setdefault("_tls", threading.local())
+        t = getattr(tls, "t", None)
+        if t is None:
+            t = tls.t = dev.empty(self.n)
+        return t
+
     def apply_raw(self, r, z, skip, stream):
         self._ensure()
         ws = dev.workspace().handle
         lib = nat.load()
-        for m, src, dst in ((self._dg, r, self._tmp.data_ptr()),
-                            (self._dgt, self._tmp.data_ptr(), z)):
+        tmp = self._scratch().data_ptr()
+        for m, src, dst in ((self._dg, r, tmp), (self._dgt, tmp, z)):
             nat.check(lib.lg_spmv(m.handle, src, dst, 0.0, None, 0, 0, None, None, 0, 0, None,
                                   ws, skip, stream), "lg_spmv")
 
