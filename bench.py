@@ -344,8 +344,9 @@ def solve_dist_block(a, dist=None, world=1, rank=0, neig=10, delta=1e-8):
     excluded, as in the reference harness bench.py:123-125)."""
     import torch
     import paper_1311_1695_b200 as L
-    from paper_1311_1695_b200.dist import RowComm, RowPartition, TorchBackend
-    part = RowPartition(a.row_ptr, world)
+    from paper_1311_1695_b200.dist import (SOLVER_ROW_WEIGHT, RowComm, RowPartition,
+                                           TorchBackend)
+    part = RowPartition(a.row_ptr, world, SOLVER_ROW_WEIGHT)
     comm = RowComm(part, rank, TorchBackend(dist) if dist else None)
     f = L.fsai_factorize(a, kmax=32)
     f.device()

@@ -12,25 +12,42 @@ order (deterministic).
 import numpy as np
 
 
-def partition_rows(row_ptr, nparts):
+def partition_rows(row_ptr, nparts, row_weight=0.0):
     """Split points (len nparts + 1) of contiguous row blocks with nearly
-    equal nonzeros: binary search on row_ptr at r * nnz / P."""
+    equal cost: binary search on the cumulative cost at r * total / P, the
+    cost of rows [0, i) being row_ptr[i] + row_weight * i (nonzeros, plus
+    row_weight nonzero-equivalents per row for the per-row vector work of a
+    solver iteration; 0: the SpMV alone, equal nonzeros)."""
     row_ptr = np.asarray(row_ptr)
-    nnz = int(row_ptr[-1])
+    n = len(row_ptr) - 1
+    cost = row_ptr.astype(np.float64)
+    if row_weight:
+        cost = cost + float(row_weight) * np.arange(n + 1, dtype=np.float64)
+    total = float(cost[-1])
     cuts = [0]
     for r in range(1, nparts):
-        cuts.append(int(np.searchsorted(row_ptr, r * nnz / nparts)))
-    cuts.append(len(row_ptr) - 1)
+        cuts.append(int(np.searchsorted(cost, r * total / nparts)))
+    cuts.append(n)
     return cuts
 
 
-class RowPartition:
-    """Contiguous row blocks of nearly equal nonzeros (split points by binary
-    search on the row pointers at r * nnz / P)."""
+# Nonzero-equivalents of one row's vector work in a DACG / JD iteration on
+# B200: the SpMV costs ~6 ps per nonzero (C5: 12.9 ms / 2.14e9), the fused
+# passes ~113 ps per row (C5: 3.7 ms / 32.8 M rows), so a rank's iteration is
+# balanced when nnz + 19 * rows is.  An nnz-balanced split leaves the ranks
+# that own the many low-degree rows of a power-law graph with ~3x the vector
+# work (C5 at 8 ranks: 11 M rows against 0.3 M).
+SOLVER_ROW_WEIGHT = 19.0
 
-    def __init__(self, row_ptr, world):
+
+class RowPartition:
+    """Contiguous row blocks of nearly equal cost (split points by binary
+    search on the row pointers; row_weight as in partition_rows)."""
+
+    def __init__(self, row_ptr, world, row_weight=0.0):
         self.world = int(world)
-        self.cuts = partition_rows(row_ptr, world)
+        self.row_weight = float(row_weight)
+        self.cuts = partition_rows(row_ptr, world, row_weight)
         self.counts = [self.cuts[i + 1] - self.cuts[i] for i in range(world)]
 
     def rows(self, rank):
@@ -236,9 +253,11 @@ class RowComm:
         return bool(getattr(self.backend, "graph_safe", False))
 
     @classmethod
-    def from_torch(cls, a, dist):
-        return cls(RowPartition(matrix_row_ptr(a), dist.get_world_size()), dist.get_rank(),
-                   TorchBackend(dist))
+    def from_torch(cls, a, dist, row_weight=SOLVER_ROW_WEIGHT):
+        """Rank of a row-partitioned solve over torch.distributed; the rows
+        are split for a balanced solver iteration (SOLVER_ROW_WEIGHT)."""
+        return cls(RowPartition(matrix_row_ptr(a), dist.get_world_size(), row_weight),
+                   dist.get_rank(), TorchBackend(dist))
 
     @property
     def nl(self):

@@ -10,7 +10,7 @@ MODELLED: per iteration the slice exchanges (1 for the SpMV, +2 for FSAI)
 move (N-1)/N x 8n bytes into each rank at the measured 770 GB/s NVLink peer
 rate plus 10 us, and every dot-product pass costs one 15 us all-reduce.
 As with NCCL, the N > 1 iteration is captured into CUDA graphs (collectives
-included; tests/test_gpu_dist.py::test_nccl_collectives_captured_in_solver_graphs).  usage: python scripts/scaling_projection.py C4|C5 [--jacobi]"""
+included; tests/test_gpu_dist.py::test_nccl_collectives_captured_in_solver_graphs).  usage: python scripts/scaling_projection.py C4|C5 [--jacobi] [--nnz-split]"""
 import json
 import os
 import sys
@@ -108,9 +108,11 @@ def main():
     rp = matrix_row_ptr(a)
     n = a.n
     base = None
+    from paper_1311_1695_b200.dist import SOLVER_ROW_WEIGHT
+    rw = 0.0 if "--nnz-split" in sys.argv else SOLVER_ROW_WEIGHT
     for world in worlds:
-        part = RowPartition(rp, world)
-        ranks = range(world) if (cfg != "C5" or world <= 2) else (0, world - 1)
+        part = RowPartition(rp, world, rw)
+        ranks = range(world) if (cfg != "C5" or world <= 2) else (0, world // 2, world - 1)
         worst, ex, ar = 0.0, 0, 0
         for r in ranks:
             comm = RowComm(part, r, NullBackend())
@@ -123,6 +125,7 @@ def main():
         total = worst + comm_us
         base = base or total
         print(json.dumps({"config": cfg, "preconditioner": prec, "ranks": world,
+                          "row_weight": rw,
                           "local_us_measured": worst, "exchanges": ex, "allreduces": ar,
                           "comm_us_modelled": comm_us, "iteration_us_projected": total,
                           "speedup_projected": base / total,
