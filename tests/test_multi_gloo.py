@@ -208,3 +208,22 @@ def test_block_jacobi_ic0_block_and_factor():
         lrp, lcol, lval, shift, att = O.ic0_factorize(O.Csr(b.n, b.row_ptr, b.col_idx, b.values),
                                                      use_c=False)
         assert np.array_equal(bj.factor.l.values.view(np.int64), lval.view(np.int64))
+
+
+def test_partition_rows_cost_weighted():
+    """row_weight > 0 balances nnz + row_weight * rows: on a power-law graph
+    every block's cost is within one row of the mean, and the low-degree
+    tail is no longer handed to one rank."""
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200.dist import SOLVER_ROW_WEIGHT, partition_rows
+    from paper_1311_1695_b200.generators import chung_lu_graph
+    g = chung_lu_graph(20000, 2.1, 8.0, max_degree=3000, seed=2)
+    rp, _, _ = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+    for world in (2, 3, 8):
+        cuts = partition_rows(rp, world, SOLVER_ROW_WEIGHT)
+        cost = [int(rp[cuts[i + 1]] - rp[cuts[i]]) + SOLVER_ROW_WEIGHT * (cuts[i + 1] - cuts[i])
+                for i in range(world)]
+        maxrow = int(np.diff(rp).max()) + SOLVER_ROW_WEIGHT
+        assert max(cost) - min(cost) <= 2 * maxrow
+        assert cuts[0] == 0 and cuts[-1] == len(rp) - 1 and cuts == sorted(cuts)
+    assert partition_rows(rp, 4) == partition_rows(rp, 4, 0.0)
