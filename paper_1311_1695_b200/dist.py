@@ -148,16 +148,33 @@ class TorchBackend:
         except Exception:
             self.graph_safe = False
 
+    def _host_staged(self, t):
+        """gloo moves host memory only: CUDA tensors go through the host."""
+        return not self.graph_safe and getattr(t, "is_cuda", False)
+
     def allreduce_(self, t, comm):
+        if self._host_staged(t):
+            h = t.cpu()
+            self.dist.all_reduce(h)
+            t.copy_(h)
+            return
         self.dist.all_reduce(t)
 
     def exchange_(self, x, comm):
+        if self._host_staged(x):
+            h = x.cpu()
+            SliceExchange(self.dist, comm.part, comm.rank)(h)
+            x.copy_(h)
+            return
         SliceExchange(self.dist, comm.part, comm.rank)(x)
 
     def exchange_start(self, x, comm):
         """Issue the slice exchange; returns the requests to wait on (NCCL
         runs it on its own stream, after the work already queued on the
         current stream)."""
+        if self._host_staged(x):
+            self.exchange_(x, comm)
+            return []
         d, part, me = self.dist, comm.part, comm.rank
         r0, r1 = part.rows(me)
         ops = []
