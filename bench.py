@@ -499,11 +499,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only knobs: LG_BENCH_BACKEND=gloo with LG_BENCH_SAME_GPU=1 runs the
+    # N > 1 code with every rank on cuda:0 (two processes sharing one GPU)
+    if os.environ.get("LG_BENCH_SAME_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_1311_1695_b200 as L
     from paper_1311_1695_b200 import _device as dev
