@@ -43,7 +43,12 @@ def device():
 
 
 def stream_ptr():
-    """cudaStream_t of torch's current stream (as an int for ctypes)."""
+    """cudaStream_t of torch's current stream (as an int for ctypes).  Inside
+    solver_stream() the pointer is cached per thread: torch's
+    current_stream() costs ~10 us a call, and a solve makes thousands."""
+    s = getattr(_state, "stream", None)
+    if s is not None:
+        return s
     return torch().cuda.current_stream().cuda_stream
 
 
@@ -237,8 +242,11 @@ class _StreamCtx:
     def __enter__(self):
         self.cm = self.t.cuda.stream(self.s)
         self.cm.__enter__()
+        self.prev = getattr(_state, "stream", None)
+        _state.stream = self.s.cuda_stream
         return self.s
 
     def __exit__(self, *exc):
+        _state.stream = self.prev
         self.cm.__exit__(*exc)
         self.t.cuda.current_stream().wait_stream(self.s)
