@@ -110,6 +110,11 @@ int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h,
                  double* x_dev_scratch, double* y_dev_scratch, void* stream);
 /* Batched SpMM: Y[:, j] = A X[:, j] for j < k (column-major, ld = n). */
 int lg_spmm(const lg_csr* a, const double* x, double* y, int k, void* stream);
+/* Y = A X with X, Y row-major n x k (ld k), 1 <= k <= 16, packed matrices:
+ * one gather of a contiguous k-vector per nonzero serves all k products
+ * (results.py:90-105's k fresh products as one pass). */
+int lg_spmm_rowmajor(const lg_csr* a, const double* x, double* y, int k, lg_ws* ws,
+                     void* stream);
 
 /* ---- Laplacian assembly (graphs.py:250-263), bit-exact ----------------- */
 /* Canonical edge list (i < j, lexicographically sorted, w > 0) -> CSR of

@@ -93,6 +93,7 @@ _SIGS = {
                         c_i64, c_int, c_p, c_p, c_p, c_p]),
     "lg_spmv_host": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p]),
     "lg_spmm": (c_int, [c_p, c_p, c_p, c_int, c_p]),
+    "lg_spmm_rowmajor": (c_int, [c_p, c_p, c_p, c_int, c_p, c_p]),
     "lg_rmat_device": (c_int, [c_int, c_int, c_dbl, c_dbl, c_dbl, ctypes.c_uint64, c_p, c_p,
                                c_p]),
     "lg_lcc_device": (c_int, [c_i64, c_i64, c_p, c_p, c_p, c_p]),

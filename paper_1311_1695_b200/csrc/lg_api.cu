@@ -118,6 +118,7 @@ int lg_ws_destroy(lg_ws* ws) {
   cudaFree(ws->long_dots);
   cudaFree(ws->long_ticket);
   cudaFree(ws->long_part);
+  cudaFree(ws->mm_part);
   delete ws;
   return LG_OK;
 }

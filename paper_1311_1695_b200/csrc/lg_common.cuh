@@ -61,6 +61,8 @@ struct lg_ws {
   int64_t long_cap = 0;           // capacity in long rows
   double* long_part = nullptr;    // [part_cap] partial sum of each part
   int64_t part_cap = 0;
+  double* mm_part = nullptr;      // [mm_cap] long-row part partials of the SpMM
+  int64_t mm_cap = 0;
 };
 
 namespace lg {

@@ -1036,12 +1036,199 @@ int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h, double* xd,
 
 int lg_spmm(const lg_csr* a, const double* x, double* y, int k, void* stream) {
   if (!a || !x || !y || k < 0) return fail(LG_EINVAL, "lg_spmm: bad argument");
+  if (!g_host_ws.ready()) return fail(LG_ECUDA, "lg_spmm: setup");
+  if (!g_host_ws.ws) {
+    int rc0 = lg_ws_create(&g_host_ws.ws);
+    if (rc0) return rc0;
+  }
   for (int j = 0; j < k; ++j) {
     int rc = lg_spmv(a, x + (int64_t)j * a->n, y + (int64_t)j * a->n, 0.0,
-                     nullptr, 0, 0, nullptr, nullptr, 0, 0, nullptr, nullptr,
+                     nullptr, 0, 0, nullptr, nullptr, 0, 0, nullptr, g_host_ws.ws,
                      nullptr, stream);
     if (rc) return rc;
   }
+  return LG_OK;
+}
+
+}  // extern "C"
+
+// ---- row-major SpMM: Y = A X for k <= 16 vectors at once --------------------
+// With X stored row-major (n x k), the k values a nonzero needs are one
+// contiguous k * 8-byte run: one gather serves all k products, where k
+// separate SpMVs make k random gathers (the L1TEX line rate bounds the
+// SpMV, section 3 of DESIGN.md).  Lanes form G = 32 / K groups of K (K = k
+// rounded up to a power of two), lane j of a group owning column j.  A row
+// of at most kMmGroupRow nonzeros is one group's (G rows per warp in
+// flight); a longer row of a block is the whole warp's, group g taking
+// nonzeros g, g + G, ..., the groups summed by a butterfly.  A long-row part (>= one block) is split over the
+// CTA's warps and its K partials go through the long-row part slots and
+// ticket, summed in part order by the last part to finish (deterministic).
+// Packed format only (lg_spmm falls back to k SpMVs otherwise).
+namespace {
+constexpr int kMmThreads = 256;
+constexpr int kMmGroupRow = 48;   // rows up to this long: one K-lane group each
+
+template <int K>
+__global__ void __launch_bounds__(kMmThreads) spmm_rm_kernel(
+    const int64_t* prp, const uint32_t* pcol, const double* pdiag, const double* table, int nvals,
+    int cbits, const SpmvBlock* blocks, int64_t nblocks, const int32_t* long_nparts,
+    const int64_t* long_first, const double* x, double* y, int k, double* part_sum,
+    unsigned* ticket) {
+  constexpr int G = 32 / K;
+  constexpr int W = kMmThreads / 32;
+  __shared__ double tab[kMaxTable];
+  __shared__ double red[W][K];
+  extern __shared__ uint32_t scol[];   // one block's column words (cta * kPer)
+  __shared__ int fin;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane / K, j = lane % K;
+  const uint32_t cmask = (1u << cbits) - 1u;
+  for (int i = threadIdx.x; i < nvals; i += kMmThreads) tab[i] = table[i];
+  __syncthreads();
+  for (int64_t b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    const SpmvBlock blk = blocks[b];
+    if (blk.lshift >= 0) {
+      // the block's column words, coalesced into shared memory once; the
+      // gathers below then depend on nothing but shared memory
+      const int cnt = (int)(blk.nz1 - blk.nz0);
+      for (int e = threadIdx.x; e < cnt; e += kMmThreads) scol[e] = pcol[blk.nz0 + e];
+      __syncthreads();
+      // short rows: one group of K lanes per row, W * G rows in flight per
+      // CTA, the row's nonzeros walked four at a time
+      for (int rr = warp * G + g; rr < blk.nrows; rr += W * G) {
+        const int64_t r = blk.row0 + rr;
+        const int e1 = (int)(prp[r + 1] - blk.nz0);
+        int e = (int)(prp[r] - blk.nz0);
+        if (e1 - e > kMmGroupRow) continue;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (j < k) {
+          for (; e + 3 < e1; e += 4) {
+            const uint32_t w0 = scol[e], w1 = scol[e + 1], w2 = scol[e + 2], w3 = scol[e + 3];
+            a0 += tab[w0 >> cbits] * x[(int64_t)(w0 & cmask) * k + j];
+            a1 += tab[w1 >> cbits] * x[(int64_t)(w1 & cmask) * k + j];
+            a2 += tab[w2 >> cbits] * x[(int64_t)(w2 & cmask) * k + j];
+            a3 += tab[w3 >> cbits] * x[(int64_t)(w3 & cmask) * k + j];
+          }
+          for (; e < e1; ++e) {
+            const uint32_t w0 = scol[e];
+            a0 += tab[w0 >> cbits] * x[(int64_t)(w0 & cmask) * k + j];
+          }
+          y[r * k + j] = ((a0 + a1) + (a2 + a3)) + pdiag[r] * x[r * k + j];
+        }
+      }
+      // longer rows of the block: the whole warp, groups summed by butterfly
+      for (int rr = warp; rr < blk.nrows; rr += W) {
+        const int64_t r = blk.row0 + rr;
+        const int e0 = (int)(prp[r] - blk.nz0), e1 = (int)(prp[r + 1] - blk.nz0);
+        if (e1 - e0 <= kMmGroupRow) continue;
+        double acc = 0.0;
+        for (int e = e0 + g; e < e1; e += G) {
+          const uint32_t w = scol[e];
+          if (j < k) acc += tab[w >> cbits] * x[(int64_t)(w & cmask) * k + j];
+        }
+#pragma unroll
+        for (int o = K; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (g == 0 && j < k) y[r * k + j] = acc + pdiag[r] * x[r * k + j];
+      }
+      __syncthreads();   // scol reused by the next block
+    } else {
+      // part of a long row: the CTA's warps split the part, K partials
+      const int cnt = (int)(blk.nz1 - blk.nz0);
+      for (int e = threadIdx.x; e < cnt; e += kMmThreads) scol[e] = pcol[blk.nz0 + e];
+      __syncthreads();
+      double acc = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (j < k) {
+        constexpr int S = W * G;
+        int e = warp * G + g;
+        for (; e + 3 * S < cnt; e += 4 * S) {
+          const uint32_t w0 = scol[e], w1 = scol[e + S], w2 = scol[e + 2 * S],
+                         w3 = scol[e + 3 * S];
+          acc += tab[w0 >> cbits] * x[(int64_t)(w0 & cmask) * k + j];
+          a1 += tab[w1 >> cbits] * x[(int64_t)(w1 & cmask) * k + j];
+          a2 += tab[w2 >> cbits] * x[(int64_t)(w2 & cmask) * k + j];
+          a3 += tab[w3 >> cbits] * x[(int64_t)(w3 & cmask) * k + j];
+        }
+        for (; e < cnt; e += S) {
+          const uint32_t w0 = scol[e];
+          acc += tab[w0 >> cbits] * x[(int64_t)(w0 & cmask) * k + j];
+        }
+        acc = (acc + a1) + (a2 + a3);
+      }
+#pragma unroll
+      for (int o = K; o < 32; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (g == 0) red[warp][j] = acc;
+      __syncthreads();
+      if (threadIdx.x < K) {
+        double t = 0.0;
+        for (int w2 = 0; w2 < W; ++w2) t += red[w2][threadIdx.x];
+        part_sum[(int64_t)blk.part * K + threadIdx.x] = t;
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned arrived = atomicAdd(ticket + blk.nrows, 1u);
+        fin = arrived == (unsigned)long_nparts[blk.nrows] - 1u;
+      }
+      __syncthreads();
+      if (fin && threadIdx.x < K) {
+        __threadfence();
+        const int lr = blk.nrows;
+        const int64_t first = long_first[lr];
+        const int np = long_nparts[lr];
+        double t = 0.0;
+        for (int p = 0; p < np; ++p) t += ld_cg(part_sum + (first + p) * K + threadIdx.x);
+        const int64_t r = blk.row0;
+        if ((int)threadIdx.x < k) y[r * k + threadIdx.x] = t + pdiag[r] * x[r * k + threadIdx.x];
+        if (threadIdx.x == 0) ticket[lr] = 0u;
+      }
+      __syncthreads();
+    }
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int lg_spmm_rowmajor(const lg_csr* a, const double* x, double* y, int k, lg_ws* ws,
+                     void* stream) {
+  if (!a || !x || !y || k < 1 || k > 16 || !ws)
+    return fail(LG_EINVAL, "lg_spmm_rowmajor: bad argument (1 <= k <= 16, workspace)");
+  if (!a->packed) return fail(LG_EINVAL, "lg_spmm_rowmajor: needs the packed format");
+  if (a->n == 0 || a->nblocks == 0) return LG_OK;
+  const int K = k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
+  if (a->nlong) {
+    int rc = ensure_long_ws(ws, a);
+    if (rc) return rc;
+    if (ws->mm_cap < a->nparts * K) {
+      cudaFree(ws->mm_part);
+      ws->mm_part = nullptr;
+      ws->mm_cap = 0;
+      LG_CUDA(cudaMalloc(&ws->mm_part, 8 * (size_t)(a->nparts * K)));
+      ws->mm_cap = a->nparts * K;
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t smem = sizeof(uint32_t) * (size_t)a->cta * kPer;
+  static thread_local int occ = 0;
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_rm_kernel<16>, kMmThreads,
+                                                      sizeof(uint32_t) * 256 * kPer) !=
+            cudaSuccess || occ < 1)
+      occ = 1;
+  }
+  const unsigned g = (unsigned)std::max<int64_t>(
+      1, std::min<int64_t>(a->nblocks, (int64_t)occ * dev_info().sm_count));
+#define LG_MM(KK)                                                                               \
+  spmm_rm_kernel<KK><<<g, kMmThreads, smem, s>>>(a->prp, a->pcol, a->pdiag, a->table, a->nvals,  \
+                                              a->cbits, a->blocks, a->nblocks,                 \
+                                              a->long_nparts, a->long_first, x, y, k,          \
+                                              ws->mm_part, ws->long_ticket)
+  if (K == 2) LG_MM(2);
+  else if (K == 4) LG_MM(4);
+  else if (K == 8) LG_MM(8);
+  else LG_MM(16);
+#undef LG_MM
+  LG_LAUNCH_CHECK("spmm_rm_kernel");
   return LG_OK;
 }
 
