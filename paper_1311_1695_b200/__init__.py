@@ -39,6 +39,10 @@ from .pcg import DeflationBasis, PcgOutcome, jd_correction_solve, kernel_basis, 
 from .precond import FsaiFactor, JacobiFactor, fsai_factorize
 from .results import EigenPairSet, SolverError, SolverReport, rayleigh_residuals
 from .sparse import CsrMatrix, MvpCounter, spmv
+from . import spectral
+from .spectral import (PinvApprox, cut_weight, estimate_lambda_max, fiedler, fiedler_order,
+                       gap_ratios, make_pinv, partition_relaxed, pinv_apply, pinv_dense,
+                       sign_partition)
 
 __version__ = "0.1.0"
 
@@ -51,5 +55,7 @@ __all__ = [
     "grid_graph", "ic0_factorize", "identity_factor", "irlm_smallest", "jd_correction_solve",
     "jd_smallest", "kernel_basis", "largest_component", "mgs_orthonormalize", "ncv_for",
     "path_graph", "pcg_solve", "rayleigh_residuals", "rmat_graph", "spmv", "star_graph",
-    "tridiag_eig",
+    "tridiag_eig", "spectral", "PinvApprox", "cut_weight", "estimate_lambda_max", "fiedler",
+    "fiedler_order", "gap_ratios", "make_pinv", "partition_relaxed", "pinv_apply", "pinv_dense",
+    "sign_partition",
 ]
