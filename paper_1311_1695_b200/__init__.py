@@ -36,7 +36,8 @@ from .irlm import irlm_smallest, ncv_for
 from .jd import jd_smallest
 from .kernels import GramSchmidtBreakdown, dense_sym_eig, mgs_orthonormalize, tridiag_eig
 from .pcg import DeflationBasis, PcgOutcome, jd_correction_solve, kernel_basis, pcg_solve
-from .precond import FsaiFactor, JacobiFactor, fsai_factorize
+from .precond import (FsaiFactor, Ic0JacobiFactor, JacobiFactor, fsai_factorize,
+                      ic0_jacobi_sweeps)
 from .results import EigenPairSet, SolverError, SolverReport, rayleigh_residuals
 from .sparse import CsrMatrix, MvpCounter, spmv
 from . import spectral
@@ -48,7 +49,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CsrMatrix", "DeflationBasis", "EdgeList", "EigenPairSet", "GramSchmidtBreakdown",
-    "FsaiFactor", "fsai_factorize", "GraphFormatError", "GraphStats", "load_edge_list",
+    "FsaiFactor", "fsai_factorize", "Ic0JacobiFactor", "ic0_jacobi_sweeps", "GraphFormatError", "GraphStats", "load_edge_list",
     "stats", "csr_connected_components", "write_matrix_market", "Ic0Error", "Ic0Factor", "JacobiFactor", "MulticolorIc0Factor", "ic0_factorize_multicolor", "MvpCounter", "PcgOutcome", "SolverError",
     "SolverReport", "ba_graph", "build_laplacian", "chung_lu_graph", "complete_graph",
     "config_graph", "connected_components", "cycle_graph", "dacg_smallest", "dense_sym_eig",

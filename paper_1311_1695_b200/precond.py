@@ -197,6 +197,115 @@ def fsai_factorize(a, kmax=32, levels=1):
     return FsaiFactor(a, kmax, levels)
 
 
+class Ic0JacobiFactor:
+    """IC(0) with its triangular solves replaced by s Jacobi sweeps each
+    (flagged NON-reference variant: "Jacobi-sweep
+    approximate triangular solves").
+
+    With L = D + N the reference's IC(0) factor (ic0.py:48-116, D its
+    diagonal), L^{-1} = sum_i (-D^{-1} N)^i D^{-1} (N D^{-1} nilpotent), and
+    s sweeps y <- D^{-1} r - D^{-1} N y from y = D^{-1} r keep the first
+    s + 1 terms, G_s.  The backward sweeps on L^T keep exactly the terms of
+    G_s^T, so z = G_s^T G_s r: symmetric positive definite for every s, and
+    the exact IC(0) apply once s reaches the factor's level count.  Each
+    sweep is two launches: y' = D^{-1} r (a diagonal lg_spmv) and y' += B y
+    (lg_spmv_acc, B = -D^{-1} N or -D^{-1} N^T): no dependency chain, about
+    (s + 1) half-Laplacian products per triangle.  Same .apply seam.
+    """
+
+    def __init__(self, f, sweeps=2):
+        from .sparse import DeviceCsr
+        l = f.l if hasattr(f, "l") else f
+        sweeps = int(sweeps)
+        if sweeps < 0:
+            raise ValueError("sweeps must be >= 0")
+        n = int(l.n)
+        rp = np.asarray(l.row_ptr, dtype=np.int64)
+        col = np.asarray(l.col_idx, dtype=np.int64)
+        val = np.asarray(l.values, dtype=np.float64)
+        rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+        on_diag = col == rows
+        if np.count_nonzero(on_diag) != n:
+            raise ValueError("factor needs a stored diagonal in every row")
+        d = np.empty(n)
+        d[rows[on_diag]] = val[on_diag]
+        off = ~on_diag
+        if np.any(col[off] > rows[off]):
+            raise ValueError("factor must be lower triangular")
+        orow, ocol = rows[off], col[off]
+        bval = -val[off] / d[orow]                     # -D^{-1} N, row-scaled
+        frp = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(frp, orow + 1, 1)
+        frp = np.cumsum(frp)
+        # -D^{-1} N^T: entry (j, i) = -n_ij / d_j, rows of N^T by a stable sort
+        order = np.argsort(ocol, kind="stable")
+        brp = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(brp, ocol + 1, 1)
+        brp = np.cumsum(brp)
+        tval = -val[off][order] / d[ocol[order]]
+        self.n = n
+        self.sweeps = sweeps
+        self.shift = getattr(f, "shift", 0.0)
+        self.attempts = getattr(f, "attempts", 0)
+        idx = np.arange(n + 1, dtype=np.int64)
+        self._dinv = DeviceCsr(n, idx, np.arange(n, dtype=np.int64), 1.0 / d)
+        self._bf = DeviceCsr(n, frp, ocol, bval)
+        self._bb = DeviceCsr(n, brp, orow[order], tval)
+
+    def _scratch(self):
+        import threading
+        tls = self.__dict__.setdefault("_tls", threading.local())
+        t = getattr(tls, "t", None)
+        if t is None:
+            t = tls.t = [dev.empty(self.n) for _ in range(3)]
+        return t
+
+    def apply_raw(self, r, z, skip, stream):
+        ws = dev.workspace().handle
+        lib = nat.load()
+        t1, t2, p = [t.data_ptr() for t in self._scratch()]
+        s = self.sweeps
+
+        def diag(src, dst):
+            nat.check(lib.lg_spmv(self._dinv.handle, src, dst, 0.0, None, 0, 0, None, None, 0,
+                                  0, None, ws, skip, stream), "lg_spmv")
+
+        def acc(m, src, dst):
+            nat.check(lib.lg_spmv_acc(m.handle, src, dst, ws, skip, stream), "lg_spmv_acc")
+
+        # forward: y_0 = D^-1 r, y_i = D^-1 r + B_f y_{i-1}   (t1 / t2)
+        fw = [t1, t2]
+        diag(r, fw[0])
+        for i in range(1, s + 1):
+            diag(r, fw[i % 2])
+            acc(self._bf, fw[(i - 1) % 2], fw[i % 2])
+        y = fw[s % 2]
+        # backward on L^T, the last write landing in z   (z / p)
+        bw = lambda i: z if (s - i) % 2 == 0 else p       # noqa: E731
+        diag(y, bw(0))
+        for i in range(1, s + 1):
+            diag(y, bw(i))
+            acc(self._bb, bw(i - 1), bw(i))
+
+    def device(self):
+        return self
+
+    def apply(self, r, z=None):
+        on_dev = dev.is_device_array(r)
+        rd = dev.to_device(r)
+        if tuple(rd.shape) != (self.n,):
+            raise ValueError("vector length does not match factor dimension")
+        out = dev.empty(self.n) if z is None else z
+        self.apply_raw(rd.data_ptr(), out.data_ptr(), None, dev.stream_ptr())
+        return out if on_dev else dev.to_host(out)
+
+
+def ic0_jacobi_sweeps(f, sweeps=2):
+    """IC(0) factor f (or its L) applied by `sweeps` Jacobi sweeps per
+    triangle (flagged non-reference variant)."""
+    return Ic0JacobiFactor(f, sweeps)
+
+
 class CallablePrec:
     """Wraps a user callable / object with .apply (not graph-capturable)."""
 
@@ -223,7 +332,7 @@ def device_preconditioner(f, n):
         return IdentityPrec(n)
     if isinstance(f, (Ic0Factor, MulticolorIc0Factor)):
         return f.device()
-    if isinstance(f, (JacobiFactor, FsaiFactor)):
+    if isinstance(f, (JacobiFactor, FsaiFactor, Ic0JacobiFactor)):
         return f.device()
     if hasattr(f, "l") and hasattr(f.l, "row_ptr"):
         hit = _cache.get(id(f))

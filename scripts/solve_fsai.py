@@ -1,5 +1,5 @@
 """Time to solution with the reference IC(0) vs the flagged FSAI and
-multicolour-IC(0) variants on the BASELINE configs (dev aid; one JSON line
+multicolour-IC(0) / Jacobi-sweep IC(0) variants on the BASELINE configs (dev aid; one JSON line
 per run).  usage: python scripts/solve_fsai.py C2 C3 C4"""
 import json
 import os
@@ -24,6 +24,14 @@ for cfg in sys.argv[1:] or ["C2", "C3", "C4"]:
         t0 = time.perf_counter()
         precs[f"fsai{k}_l{lv}"] = L.fsai_factorize(a, kmax=k, levels=lv)
         setup[f"fsai{k}_l{lv}"] = time.perf_counter() - t0
+    f0 = precs["ic0"]
+    for sw in (1, 2, 3):
+        t0 = time.perf_counter()
+        precs[f"ic0_jacobi{sw}"] = L.ic0_jacobi_sweeps(f0, sw)
+        setup[f"ic0_jacobi{sw}"] = setup["ic0"] + time.perf_counter() - t0
+    only = os.environ.get("PRECS")
+    if only:
+        precs = {k: v for k, v in precs.items() if k in only.split(",")}
     for p in precs.values():
         p.device()
     for sv, fn in (("dacg", L.dacg_smallest), ("jd", L.jd_smallest)):

@@ -240,3 +240,40 @@ def test_fsai_device_setup_matches_host(L):
     pf, rf = L.dacg_smallest(A, 3, delta=1e-8, f=ff, seed=0)
     assert np.max(np.abs(pf.values - pj.values) / pj.values) <= 1e-8
     assert rf.mvp < rj.mvp
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+def test_ic0_jacobi_sweeps_variant(L, cfg):
+    """IC(0) with Jacobi-sweep triangular solves (flagged non-reference
+    variant): the apply is G_s^T G_s r with G_s = sum_{i<=s} (-D^-1 N)^i D^-1
+    (checked against scipy on the host factor), equals the exact IC(0) apply
+    once s reaches the factor's level count, and DACG / JD with s = 2 return
+    the reference's eigenvalues with fresh residuals <= delta."""
+    import scipy.sparse as sp
+    ref = golden_config(cfg)
+    a = L.build_laplacian(L.config_graph(cfg))
+    f = L.ic0_factorize(a)
+    Lm = sp.csr_matrix((f.l.values, f.l.col_idx, f.l.row_ptr), shape=(a.n, a.n))
+    dinv = sp.diags(1.0 / Lm.diagonal())
+    B = -(dinv @ sp.tril(Lm, k=-1))
+    r = np.random.default_rng(3).standard_normal(a.n)
+    for s in (0, 1, 3):
+        y = dinv @ r
+        g = y.copy()
+        for _ in range(s):
+            g = y + B @ g
+        zt = dinv @ g
+        w = zt.copy()
+        Bt = -(dinv @ sp.tril(Lm, k=-1).T)
+        for _ in range(s):
+            w = zt + Bt @ w
+        z = L.ic0_jacobi_sweeps(f, s).apply(r)
+        assert np.max(np.abs(z - w)) <= 1e-12 * np.max(np.abs(w))
+    lev = f.device().levels
+    exact = f.apply(r)
+    z = L.ic0_jacobi_sweeps(f, lev).apply(r)
+    assert np.max(np.abs(z - exact)) <= 1e-10 * np.max(np.abs(exact))
+    fj = L.ic0_jacobi_sweeps(f, 2)
+    for sv in ("dacg", "jd"):
+        pairs, rep = solver(L, sv)(a, ref["neig"], delta=ref["delta"], f=fj)
+        check_pairs(L, a, pairs, np.asarray(ref["solvers"][sv]["eigenvalues"]), ref["delta"])
