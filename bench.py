@@ -285,6 +285,8 @@ def solve_configs_block(prebuilt=None):
             ff = L.fsai_factorize(a, kmax=32)
             ff.device()
             variants.append(("_fsai", ff, "fsai kmax 32 (flagged variant)"))
+            variants.append(("_ic0j3", L.ic0_jacobi_sweeps(f, 3),
+                             "ic0, 3 Jacobi sweeps per triangle (flagged variant)"))
         for name in solvers:
             for suffix, prec, label in variants:
                 walls = []
