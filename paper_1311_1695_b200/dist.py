@@ -328,7 +328,7 @@ class RowComm:
         preconditioner at every N; device-built for device-only matrices);
         'block_ic0' -> block-Jacobi IC(0) of the diagonal block; 'jacobi' /
         a JacobiFactor -> its slice."""
-        from .precond import FsaiFactor, JacobiFactor
+        from .precond import FsaiFactor, Ic0JacobiFactor, JacobiFactor
         host = hasattr(a, "row_ptr") and getattr(a, "col_idx", None) is not None
         if f is None:
             f = "fsai"
@@ -349,11 +349,13 @@ class RowComm:
             return LocalJacobi(f, self.r0, self.r1)
         if isinstance(f, FsaiFactor):
             return DistFsai(f, self)
-        if isinstance(f, (BlockJacobiIc0, DistFsai)):
+        if isinstance(f, Ic0JacobiFactor):
+            return DistIc0Jacobi(f, self)
+        if isinstance(f, (BlockJacobiIc0, DistFsai, DistIc0Jacobi)):
             return f
-        raise ValueError("row-partitioned solves take an FsaiFactor, a JacobiFactor, 'fsai', "
-                         "'jacobi' or 'block_ic0' as preconditioner (the natural-order IC(0) "
-                         "sweeps do not shard, SURVEY 8(e))")
+        raise ValueError("row-partitioned solves take an FsaiFactor, an Ic0JacobiFactor, a "
+                         "JacobiFactor, 'fsai', 'jacobi' or 'block_ic0' as preconditioner (the "
+                         "natural-order IC(0) sweeps do not shard, SURVEY 8(e))")
 
 
 def split_cols(dmat, r0, r1):
@@ -425,6 +427,47 @@ class BlockJacobiIc0:
 
     def apply_raw(self, r, z, skip, stream):
         self.factor.device().apply_raw(r, z, skip, stream)
+
+
+class DistIc0Jacobi:
+    """The reference IC(0) factor applied by s Jacobi sweeps per triangle
+    (precond.Ic0JacobiFactor) across ranks: every sweep is a row-partitioned
+    product after the in-place slice exchange of its input, the D^{-1}
+    scalings are rank-local -- the same preconditioner at every rank count,
+    so the iteration counts do not depend on N (unlike block-Jacobi IC(0))."""
+
+    def __init__(self, f, comm):
+        from . import _device as dev
+        self.f = f
+        self.comm = comm
+        self.s = f.sweeps
+        self.dinv = local_operator(f.dinv, comm.part, comm.rank)
+        self.bf = local_operator(f.bf, comm.part, comm.rank)
+        self.bb = local_operator(f.bb, comm.part, comm.rank)
+        self.t = [dev.zeros(f.n) for _ in range(3)]
+        self.n = f.n
+
+    def dist_steps(self, r, z, skip=None):
+        from ._plan import Exchange, Spmv, SpmvAcc
+        s = self.s
+        t1, t2, p = self.t
+        fw = [t1, t2]
+        steps = [Spmv(self.dinv, r, fw[0], skip=skip)]
+        for i in range(1, s + 1):
+            steps += [Exchange(self.comm, fw[(i - 1) % 2]),
+                      Spmv(self.dinv, r, fw[i % 2], skip=skip),
+                      SpmvAcc(self.bf, fw[(i - 1) % 2], fw[i % 2], skip=skip)]
+        y = fw[s % 2]
+
+        def bw(i):
+            return z if (s - i) % 2 == 0 else p
+
+        steps.append(Spmv(self.dinv, y, bw(0), skip=skip))
+        for i in range(1, s + 1):
+            steps += [Exchange(self.comm, bw(i - 1)),
+                      Spmv(self.dinv, y, bw(i), skip=skip),
+                      SpmvAcc(self.bb, bw(i - 1), bw(i), skip=skip)]
+        return steps
 
 
 class DistFsai:

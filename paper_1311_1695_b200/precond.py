@@ -247,10 +247,14 @@ class Ic0JacobiFactor:
         self.sweeps = sweeps
         self.shift = getattr(f, "shift", 0.0)
         self.attempts = getattr(f, "attempts", 0)
+        from types import SimpleNamespace as _M
         idx = np.arange(n + 1, dtype=np.int64)
-        self._dinv = DeviceCsr(n, idx, np.arange(n, dtype=np.int64), 1.0 / d)
-        self._bf = DeviceCsr(n, frp, ocol, bval)
-        self._bb = DeviceCsr(n, brp, orow[order], tval)
+        # host triples (row-partitioned solves cut their row blocks from these)
+        self.dinv = _M(n=n, row_ptr=idx, col_idx=np.arange(n, dtype=np.int64), values=1.0 / d)
+        self.bf = _M(n=n, row_ptr=frp, col_idx=ocol, values=bval)
+        self.bb = _M(n=n, row_ptr=brp, col_idx=orow[order], values=tval)
+        self._dinv, self._bf, self._bb = (DeviceCsr(n, m.row_ptr, m.col_idx, m.values)
+                                          for m in (self.dinv, self.bf, self.bb))
 
     def _scratch(self):
         import threading

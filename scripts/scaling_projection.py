@@ -6,11 +6,12 @@ of the SpMV as interior + exterior halves, its preconditioner share, every
 fused pass over its slice, the scalar programs) is built with the real
 row-partitioned plan and timed alone on one GPU with the collectives
 replaced by no-ops; the max over ranks is taken.  The collectives are
-MODELLED: per iteration the slice exchanges (1 for the SpMV, +2 for FSAI)
+MODELLED: per iteration the slice exchanges (1 for the SpMV, +2 for FSAI, +2S for
+S-sweep IC(0))
 move (N-1)/N x 8n bytes into each rank at the measured 770 GB/s NVLink peer
 rate plus 10 us, and every dot-product pass costs one 15 us all-reduce.
 As with NCCL, the N > 1 iteration is captured into CUDA graphs (collectives
-included; tests/test_gpu_dist.py::test_nccl_collectives_captured_in_solver_graphs).  usage: python scripts/scaling_projection.py C4|C5 [--jacobi] [--nnz-split]"""
+included; tests/test_gpu_dist.py::test_nccl_collectives_captured_in_solver_graphs).  usage: python scripts/scaling_projection.py C4|C5 [--jacobi] [--ic0j S] [--nnz-split]"""
 import json
 import os
 import sys
@@ -102,8 +103,13 @@ def main():
         worlds = (1, 2, 4, 8)
     else:
         a = L.build_laplacian(L.config_graph(cfg))
-        f = L.fsai_factorize(a, 32)
-        prec = "fsai"
+        if "--ic0j" in sys.argv:
+            sw = int(sys.argv[sys.argv.index("--ic0j") + 1])
+            f = L.ic0_jacobi_sweeps(L.ic0_factorize(a), sw)
+            prec = f"ic0_jacobi{sw} (reference IC(0) factor)"
+        else:
+            f = L.fsai_factorize(a, 32)
+            prec = "fsai"
         worlds = (1, 2, 4, 8)
     rp = matrix_row_ptr(a)
     n = a.n

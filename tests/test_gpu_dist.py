@@ -188,6 +188,29 @@ def test_row_partitioned_fsai_same_iterations(world):
         assert np.max(res) <= 1.5 * delta
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_partitioned_ic0_jacobi_sweeps(world):
+    """The reference IC(0) factor with Jacobi-sweep triangular solves
+    (dist.DistIc0Jacobi: every sweep a row-partitioned product after an
+    exchange) is the same preconditioner at every rank count: DACG and JD
+    take the single-GPU solve's MVP counts and eigenvalues."""
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200.results import rayleigh_residuals
+    a = _graph()
+    f = L.ic0_jacobi_sweeps(L.ic0_factorize(a), 2)
+    delta = 1e-8
+    for fn, run in ((L.dacg_smallest, _run_ranks), (L.jd_smallest, _run_ranks_jd)):
+        ref, rrep = fn(a, 4, delta=delta, f=f, seed=0)
+        out = run(a, world, f, 4, delta)
+        pairs, rep = out[0]
+        for p, _ in out:
+            assert np.array_equal(p.values, pairs.values)
+        assert np.max(np.abs(pairs.values - ref.values) / ref.values) <= 1e-8
+        assert abs(rep.mvp - rrep.mvp) <= 0.03 * rrep.mvp + 3
+        _, res = rayleigh_residuals(a, pairs.vectors)
+        assert np.max(res) <= 1.5 * delta
+
+
 @pytest.mark.parametrize("world,prec", [(2, "fsai"), (3, "jacobi")])
 def test_row_partitioned_irlm(world, prec):
     """IRLM (inverse Lanczos, deflated PCG inner solves) row-partitioned:
