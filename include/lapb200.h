@@ -150,6 +150,12 @@ int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** out);
  * counterpart.) */
 int lg_csr_split_cols(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** inner,
                       lg_csr** outer);
+/* Column panel [c0, c1) of a packed operator: every row, only the columns in
+ * the range (and the diagonal when with_diag).  The product of a graph whose
+ * x exceeds L2 splits into panels (y = P_0 x, y += P_k x with lg_spmv_acc) so
+ * each panel's gathers hit an L2-resident slice of x.  (SURVEY 8(f) SpMV
+ * locality; no reference counterpart.) */
+int lg_csr_col_panel(const lg_csr* a, int64_t c0, int64_t c1, int with_diag, lg_csr** out);
 /* y += A x, no epilogue (the exterior half of a split row block). */
 int lg_spmv_acc(const lg_csr* a, const double* x, double* y, lg_ws* ws, const int* skip,
                 void* stream);

@@ -1534,30 +1534,30 @@ extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr*
 // product runs while the slices of x are exchanged; the exterior product
 // then accumulates into y (lg_spmv_acc).  Both stay in the packed format.
 namespace {
-__global__ void split_count(int64_t r0, int64_t r1, const int64_t* prp, const uint32_t* pcol,
-                            uint32_t cmask, int64_t* cin, int64_t* cout) {
+__global__ void split_count(int64_t r0, int64_t r1, int64_t c0, int64_t c1, const int64_t* prp,
+                            const uint32_t* pcol, uint32_t cmask, int64_t* cin, int64_t* cout) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += st) {
     int64_t ni = 0;
     for (int64_t k = prp[r]; k < prp[r + 1]; ++k) {
       const int64_t c = pcol[k] & cmask;
-      ni += (c >= r0 && c < r1);
+      ni += (c >= c0 && c < c1);
     }
     cin[r - r0] = ni;
-    cout[r - r0] = (prp[r + 1] - prp[r]) - ni;
+    if (cout) cout[r - r0] = (prp[r + 1] - prp[r]) - ni;
   }
 }
-__global__ void split_scatter(int64_t r0, int64_t r1, const int64_t* prp, const uint32_t* pcol,
-                              uint32_t cmask, const int64_t* oin, const int64_t* oout,
-                              uint32_t* win, uint32_t* wout) {
+__global__ void split_scatter(int64_t r0, int64_t r1, int64_t c0, int64_t c1, const int64_t* prp,
+                              const uint32_t* pcol, uint32_t cmask, const int64_t* oin,
+                              const int64_t* oout, uint32_t* win, uint32_t* wout) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < r1; r += st) {
-    int64_t pi = oin[r - r0], po = oout[r - r0];
+    int64_t pi = oin[r - r0], po = wout ? oout[r - r0] : 0;
     for (int64_t k = prp[r]; k < prp[r + 1]; ++k) {
       const uint32_t w = pcol[k];
       const int64_t c = w & cmask;
-      if (c >= r0 && c < r1) win[pi++] = w;
-      else wout[po++] = w;
+      if (c >= c0 && c < c1) win[pi++] = w;
+      else if (wout) wout[po++] = w;
     }
   }
 }
@@ -1641,7 +1641,7 @@ extern "C" int lg_csr_split_cols(const lg_csr* a, int64_t r0, int64_t r1, lg_csr
   }
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>((nloc + 255) / 256,
                                                              (int64_t)dev_info().sm_count * 16));
-  if (nloc) split_count<<<g, 256>>>(r0, r1, a->prp, a->pcol, cmask, cin, cout);
+  if (nloc) split_count<<<g, 256>>>(r0, r1, r0, r1, a->prp, a->pcol, cmask, cin, cout);
   size_t tb = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tb, cin, oin, std::max<int64_t>(nloc, 1));
   if (cudaMalloc(&tmp, std::max<size_t>(tb, 16)) != cudaSuccess) {
@@ -1666,7 +1666,7 @@ extern "C" int lg_csr_split_cols(const lg_csr* a, int64_t r0, int64_t r1, lg_csr
     cleanup();
     return fail(LG_ENOMEM, "lg_csr_split_cols: allocation failed");
   }
-  if (nloc) split_scatter<<<g, 256>>>(r0, r1, a->prp, a->pcol, cmask, oin, oout, win, wout);
+  if (nloc) split_scatter<<<g, 256>>>(r0, r1, r0, r1, a->prp, a->pcol, cmask, oin, oout, win, wout);
   cudaError_t e = cudaDeviceSynchronize();
   cleanup();
   if (e != cudaSuccess) {
@@ -1695,6 +1695,71 @@ extern "C" int lg_csr_split_cols(const lg_csr* a, int64_t r0, int64_t r1, lg_csr
   }
   *inner = bi;
   *outer = bo;
+  return LG_OK;
+}
+
+// Column panel [c0, c1) of the whole operator (every row, only the columns in
+// the range; the diagonal when with_diag).  A product split into panels whose
+// slice of x fits in L2 gathers x from L2 instead of DRAM: y = P_0 x, then
+// y += P_k x (lg_spmv_acc) — for graphs whose x exceeds L2 (C5).
+extern "C" int lg_csr_col_panel(const lg_csr* a, int64_t c0, int64_t c1, int with_diag,
+                                lg_csr** out) {
+  if (!a || !out || c0 < 0 || c1 < c0 || c1 > a->n)
+    return fail(LG_EINVAL, "lg_csr_col_panel: bad argument");
+  if (!a->packed) return fail(LG_EINVAL, "lg_csr_col_panel: only for packed matrices");
+  const int64_t n = a->n;
+  const uint32_t cmask = (a->cbits >= 32) ? 0xffffffffu : ((1u << a->cbits) - 1u);
+  int64_t *cin = nullptr, *oin = nullptr;
+  void* tmp = nullptr;
+  uint32_t* win = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(cin);
+    cudaFree(oin);
+    cudaFree(tmp);
+  };
+  const size_t nb = 8 * (size_t)std::max<int64_t>(n, 1);
+  if (cudaMalloc(&cin, nb) != cudaSuccess || cudaMalloc(&oin, nb) != cudaSuccess) {
+    cleanup();
+    return fail(LG_ENOMEM, "lg_csr_col_panel: allocation failed");
+  }
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256,
+                                                             (int64_t)dev_info().sm_count * 16));
+  if (n) split_count<<<g, 256>>>(0, n, c0, c1, a->prp, a->pcol, cmask, cin, nullptr);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, cin, oin, std::max<int64_t>(n, 1));
+  if (cudaMalloc(&tmp, std::max<size_t>(tb, 16)) != cudaSuccess) {
+    cleanup();
+    return fail(LG_ENOMEM, "lg_csr_col_panel: scan scratch");
+  }
+  std::vector<int64_t> hin((size_t)n);
+  int64_t mi = 0;
+  if (n) {
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cin, oin, n);
+    cudaMemcpy(hin.data(), cin, nb, cudaMemcpyDeviceToHost);
+    for (int64_t i = 0; i < n; ++i) mi += hin[(size_t)i];
+  }
+  if (cudaMalloc(&win, 4 * (size_t)std::max<int64_t>(mi, 1)) != cudaSuccess) {
+    cleanup();
+    return fail(LG_ENOMEM, "lg_csr_col_panel: allocation failed");
+  }
+  if (n) split_scatter<<<g, 256>>>(0, n, c0, c1, a->prp, a->pcol, cmask, oin, nullptr, win, nullptr);
+  cudaError_t e = cudaDeviceSynchronize();
+  cleanup();
+  if (e != cudaSuccess) {
+    cudaFree(win);
+    return fail(LG_ECUDA, std::string("lg_csr_col_panel: ") + cudaGetErrorString(e));
+  }
+  int rc = make_part(a, 0, n, hin, win, mi, with_diag != 0, out);
+  if (rc) {
+    cudaFree(win);
+    return rc;
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    lg_csr_destroy(*out);
+    *out = nullptr;
+    return fail(LG_ECUDA, std::string("lg_csr_col_panel: ") + cudaGetErrorString(e));
+  }
   return LG_OK;
 }
 

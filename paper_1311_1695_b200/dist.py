@@ -375,6 +375,20 @@ def split_cols(dmat, r0, r1):
     return tuple(out)
 
 
+def col_panel(dmat, c0, c1, with_diag):
+    """Columns [c0, c1) of a packed operator, every row (lg_csr_col_panel)."""
+    import ctypes
+
+    from . import _native as nat
+    from .sparse import DeviceCsr
+    h = ctypes.c_void_p()
+    nat.call("lg_csr_col_panel", dmat.handle, int(c0), int(c1), int(bool(with_diag)),
+             ctypes.byref(h))
+    info = [ctypes.c_int64() for _ in range(4)] + [ctypes.c_int(), ctypes.c_int64()]
+    nat.call("lg_csr_info", h, *[ctypes.byref(v) for v in info])
+    return DeviceCsr.from_handle(h, dmat.n, info[1].value)
+
+
 def matrix_row_ptr(a):
     """Row pointers to balance on: host CSR arrays, or the device matrix's."""
     if hasattr(a, "row_ptr") and getattr(a, "col_idx", None) is not None:

@@ -537,6 +537,38 @@ def test_split_row_block_interior_exterior(world):
             assert err <= 1e-12 * max(1.0, want.abs().max().item())
 
 
+@pytest.mark.parametrize("panels", [2, 5])
+def test_col_panels_sum_to_full_product(panels):
+    """lg_csr_col_panel: the column panels of an operator (diagonal in the
+    first) partition its nonzeros, and y = P_0 x, y += P_k x (lg_spmv_acc)
+    equals the one-pass product to roundoff.  Host-built weighted and
+    device-built R-MAT matrices."""
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200._plan import SpmvAcc
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.dist import col_panel
+    g, _ = L.largest_component(L.generators.chung_lu_graph(20000, 2.1, 8.0, max_degree=4000,
+                                                           weighted=True, seed=11))
+    for A in (L.build_laplacian(g), rmat_laplacian_device(13, 8, seed=2)):
+        full = A.device()
+        if not full.packed:
+            continue
+        n = A.n
+        x = dev.to_device(np.random.default_rng(5).standard_normal(n))
+        want = dev.empty(n)
+        full.matvec(x, want)
+        cuts = [n * k // panels for k in range(panels + 1)]
+        parts = [col_panel(full, cuts[k], cuts[k + 1], k == 0) for k in range(panels)]
+        assert sum(p.nnz for p in parts) == full.nnz
+        y = dev.empty(n)
+        parts[0].matvec(x, y)
+        for p in parts[1:]:
+            SpmvAcc(p, x, y)()
+        err = (y - want).abs().max().item()
+        assert err <= 1e-12 * max(1.0, want.abs().max().item())
+
+
 def test_spmv_256_thread_schedule_parity():
     """The 256-thread schedule (chosen for matrices with >= 2^27
     off-diagonals, forced here with LG_SPMV_CTA=256 in a child process) gives
