@@ -118,6 +118,7 @@ _SIGS = {
     "lg_csr_row_ptr": (c_int, [c_p, c_p]),
     "lg_csr_split_cols": (c_int, [c_p, c_i64, c_i64, c_p, c_p]),
     "lg_csr_col_panel": (c_int, [c_p, c_i64, c_i64, c_int, c_p]),
+    "lg_csr_set_panels": (c_int, [c_p, c_int]),
     "lg_fsai_nnz": (c_int, [c_i64, c_p, c_p, c_p, c_int, c_int, c_p]),
     "lg_graph_parse": (c_int, [c_p, c_i64, c_int, c_int, c_p, c_p, c_p, c_p, c_p, c_p]),
     "lg_host_free": (c_int, [c_p]),

@@ -86,6 +86,10 @@ struct lg_csr {
   int nchunks = 0;
   int64_t chunk_b[9] = {};
   int64_t chunk_row[9] = {};
+  // column panels of a full operator (lg_csr_set_panels): when set, lg_spmv
+  // runs y = P_0 x - theta x, y += P_k x instead of the one-pass product
+  int npanels = 0;
+  lg_csr* panel[16] = {};
 };
 
 namespace lg {
@@ -739,6 +743,7 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
 
 int lg_csr_destroy(lg_csr* a) {
   if (!a) return LG_OK;
+  for (int k = 0; k < a->npanels; ++k) lg_csr_destroy(a->panel[k]);
   cudaFree(a->row_ptr);
   cudaFree(a->col);
   cudaFree(a->val);
@@ -787,6 +792,10 @@ int lg_csr_download(const lg_csr* a, int64_t* rp, int64_t* col, double* val) {
                        cudaMemcpyDeviceToHost));
   return LG_OK;
 }
+
+int lg_spmv_panels_(const lg_csr* a, const double* x, double* y, double theta_h,
+                    const double* theta_d, int theta_neg, const int* skip, lg_ws* ws,
+                    void* stream);
 
 int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
             const double* theta_d, int theta_neg, int ndots,
@@ -839,17 +848,24 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
   cudaStream_t s = (cudaStream_t)stream;
   int na = ndots + nq;
   const bool pk = a->packed != 0;
-  if (na == 0) return launch<0>(args, ws, s, pk, a->cta);
+  if (a->npanels > 1 && ws == &local)
+    return fail(LG_EINVAL, "lg_spmv: panelled matrix; pass a workspace");
+  auto product = [&]() {
+    return a->npanels > 1
+               ? lg_spmv_panels_(a, x, y, theta_h, theta_d, theta_neg, skip, ws, stream)
+               : launch<0>(args, ws, s, pk, a->cta);
+  };
+  if (na == 0) return product();
   static const bool fused_epilogue = [] {
     const char* e = getenv("LG_SPMV_EPILOGUE");
     return e && atoi(e) == 1;
   }();
-  if (!fused_epilogue || a->cta != 128) {
+  if (!fused_epilogue || a->cta != 128 || a->npanels > 1) {
     // The gather loop is latency-bound and wants every register for
     // occupancy: the dot / Q^T y epilogue costs less as one streaming pass
     // over y right behind the SpMV (measured on C4: +4-9 us instead of
     // +18-60 us inside the kernel).  Same result layout: dots, then Q^T y.
-    int rc = launch<0>(args, ws, s, pk, a->cta);
+    int rc = product();
     if (rc) return rc;
     lg_fused_args f{};
     f.n = a->n;
@@ -1759,6 +1775,70 @@ extern "C" int lg_csr_col_panel(const lg_csr* a, int64_t c0, int64_t c1, int wit
     lg_csr_destroy(*out);
     *out = nullptr;
     return fail(LG_ECUDA, std::string("lg_csr_col_panel: ") + cudaGetErrorString(e));
+  }
+  return LG_OK;
+}
+
+// Attach p equal-width column panels to a FULL operator (every row present;
+// not a row block): lg_spmv then runs the panel chain.  p <= 1 detaches.
+extern "C" int lg_csr_set_panels(lg_csr* a, int p) {
+  if (!a || p < 0 || p > 16) return fail(LG_EINVAL, "lg_csr_set_panels: bad argument");
+  if (p > 1 && !a->packed) return fail(LG_EINVAL, "lg_csr_set_panels: only for packed matrices");
+  cudaDeviceSynchronize();
+  for (int k = 0; k < a->npanels; ++k) lg_csr_destroy(a->panel[k]);
+  a->npanels = 0;
+  if (p <= 1) return LG_OK;
+  lg_csr* parts[16] = {};
+  for (int k = 0; k < p; ++k) {
+    int rc = lg_csr_col_panel(a, a->n * k / p, a->n * (k + 1) / p, k == 0, &parts[k]);
+    if (rc) {
+      for (int j = 0; j < k; ++j) lg_csr_destroy(parts[j]);
+      return rc;
+    }
+  }
+  for (int k = 0; k < p; ++k) a->panel[k] = parts[k];
+  a->npanels = p;
+  return LG_OK;
+}
+
+// The panel chain behind lg_spmv: P_0 carries the diagonal and the theta
+// shift; the rest accumulate.  Same stream, same workspace, in order.
+extern "C" int lg_spmv_panels_(const lg_csr* a, const double* x, double* y, double theta_h,
+                               const double* theta_d, int theta_neg, const int* skip,
+                               lg_ws* ws, void* stream) {
+  for (int k = 0; k < a->npanels; ++k) {
+    const lg_csr* m = a->panel[k];
+    if (m->nblocks == 0) continue;
+    if (m->nlong) {
+      int rc = ensure_long_ws(ws, m);
+      if (rc) return rc;
+    }
+    SpmvArgs args{};
+    args.accum = k > 0;
+    args.n = m->n;
+    args.row_ptr = m->prp;
+    args.pcol = m->pcol;
+    args.pdiag = m->pdiag;
+    args.table = m->table;
+    args.nvals = m->nvals;
+    args.cbits = m->cbits;
+    args.blocks = m->blocks;
+    args.nblocks = m->nblocks;
+    args.long_nparts = m->long_nparts;
+    args.long_first = m->long_first;
+    args.x = x;
+    args.y = y;
+    if (k == 0) {
+      args.theta_h = theta_h;
+      args.theta_d = theta_d;
+      args.theta_neg = theta_neg;
+    }
+    args.skip = skip;
+    args.long_part = ws->long_part;
+    args.long_ticket = ws->long_ticket;
+    args.nlong = m->nlong;
+    int rc = launch<0>(args, ws, (cudaStream_t)stream, true, m->cta);
+    if (rc) return rc;
   }
   return LG_OK;
 }

@@ -29,7 +29,7 @@ class DeviceLaplacian:
         self.n = int(n)
         self.m = int(m)
         self.symmetric = True
-        self._dev = DeviceCsr.from_handle(handle, self.n, self.n + 2 * self.m)
+        self._dev = DeviceCsr.from_handle(handle, self.n, self.n + 2 * self.m).auto_panels()
 
     @property
     def nnz(self):

@@ -569,6 +569,37 @@ def test_col_panels_sum_to_full_product(panels):
         assert err <= 1e-12 * max(1.0, want.abs().max().item())
 
 
+def test_panelled_operator_solves_match():
+    """lg_csr_set_panels: the panelled product (theta shift and epilogue
+    dots included, as the solvers call it) gives the one-pass product to
+    roundoff, and DACG / JD on a panelled operator return the same
+    eigenvalues; detaching restores the one-pass product bitwise."""
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.precond import JacobiFactor
+    A = rmat_laplacian_device(14, 8, seed=3)
+    d = A.device()
+    x = dev.to_device(np.random.default_rng(1).standard_normal(A.n))
+    want, y, y2 = dev.empty(A.n), dev.empty(A.n), dev.empty(A.n)
+    d.matvec(x, want, theta=0.37)
+    f = JacobiFactor(A)
+    ref_d, _ = L.dacg_smallest(A, 3, delta=1e-9, f=f, seed=0)
+    ref_j, _ = L.jd_smallest(A, 3, delta=1e-9, f=f, seed=0)
+    d.set_panels(3)
+    try:
+        d.matvec(x, y, theta=0.37)
+        assert (y - want).abs().max().item() <= 1e-12 * want.abs().max().item()
+        got_d, _ = L.dacg_smallest(A, 3, delta=1e-9, f=f, seed=0)
+        got_j, _ = L.jd_smallest(A, 3, delta=1e-9, f=f, seed=0)
+    finally:
+        d.set_panels(0)
+    assert np.max(np.abs(got_d.values - ref_d.values) / ref_d.values) <= 1e-8
+    assert np.max(np.abs(got_j.values - ref_j.values) / ref_j.values) <= 1e-8
+    d.matvec(x, y2, theta=0.37)
+    assert bool((y2 == want).all())
+
+
 def test_spmv_256_thread_schedule_parity():
     """The 256-thread schedule (chosen for matrices with >= 2^27
     off-diagonals, forced here with LG_SPMV_CTA=256 in a child process) gives
