@@ -187,7 +187,9 @@ __device__ __forceinline__ double product(const SpmvArgs& a, const Staged<PACKED
 template <bool PACKED>
 __device__ __forceinline__ double finish_row(const SpmvArgs& a, int64_t r, double s,
                                              double theta) {
-  if constexpr (PACKED) s += a.pdiag[r] * __ldg(a.x + r);
+  if constexpr (PACKED) {
+    if (a.pdiag) s += a.pdiag[r] * __ldg(a.x + r);  // NULL: accumulating column panel
+  }
   if (theta != 0.0) s -= theta * __ldg(a.x + r);
   if (a.accum) s = a.y[r] + s;
   return s;
@@ -1818,7 +1820,7 @@ extern "C" int lg_spmv_panels_(const lg_csr* a, const double* x, double* y, doub
     args.n = m->n;
     args.row_ptr = m->prp;
     args.pcol = m->pcol;
-    args.pdiag = m->pdiag;
+    args.pdiag = k == 0 ? m->pdiag : nullptr;  // later panels: no diagonal to stream
     args.table = m->table;
     args.nvals = m->nvals;
     args.cbits = m->cbits;
