@@ -22,6 +22,8 @@ scale = int(sys.argv[1]) if len(sys.argv) > 1 else 26
 plist = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 4, 8, 16]
 A = rmat_laplacian_device(scale, 16, seed=0)
 d = A.device()
+auto_p = d.npanels
+d.set_panels(0)  # the one-pass baseline (DeviceLaplacian auto-panels x > 96 MiB)
 n = A.n
 x = dev.to_device(np.random.default_rng(0).standard_normal(n))
 want = dev.empty(n)
@@ -42,7 +44,7 @@ def timed(fn, reps=10, warm=3):
     return e0.elapsed_time(e1) / reps
 
 
-out = {"workload": f"R-MAT scale {scale} ef 16 LCC device-built", "n": n, "nnz": A.nnz,
+out = {"auto_panels": auto_p, "workload": f"R-MAT scale {scale} ef 16 LCC device-built", "n": n, "nnz": A.nnz,
        "x_mb": n * 8 / 2**20}
 out["one_pass_ms"] = timed(lambda: d.matvec(x, want))
 scale_ref = want.abs().max().item()
