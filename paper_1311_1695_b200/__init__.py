@@ -16,8 +16,10 @@ from .generators import (
     complete_graph,
     config_graph,
     cycle_graph,
+    geometric_graph,
     grid_graph,
     path_graph,
+    random_connected_graph,
     rmat_graph,
     star_graph,
 )
@@ -58,5 +60,5 @@ __all__ = [
     "path_graph", "pcg_solve", "rayleigh_residuals", "rmat_graph", "spmv", "star_graph",
     "tridiag_eig", "spectral", "PinvApprox", "cut_weight", "estimate_lambda_max", "fiedler",
     "fiedler_order", "gap_ratios", "make_pinv", "partition_relaxed", "pinv_apply", "pinv_dense",
-    "sign_partition",
+    "sign_partition", "geometric_graph", "random_connected_graph",
 ]

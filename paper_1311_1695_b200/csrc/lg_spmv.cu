@@ -90,6 +90,9 @@ struct lg_csr {
   // runs y = P_0 x - theta x, y += P_k x instead of the one-pass product
   int npanels = 0;
   lg_csr* panel[16] = {};
+  // rows absent from the schedule (SKIP_EMPTY, row blocks, split halves):
+  // such an operator is not a full operator and cannot be panelled
+  int is_block = 0;
 };
 
 namespace lg {
@@ -686,6 +689,7 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
   a->cbits = cbits;
   a->nvals = (int)table.size();
   a->noff = packed ? (int64_t)pcol.size() : 0;
+  a->is_block = (flags & LG_CSR_SKIP_EMPTY) ? 1 : 0;
   for (int32_t v : lnp) a->nparts += v;
   auto cleanup = [&](const char* what) {
     lg_csr_destroy(a);
@@ -1211,7 +1215,8 @@ int lg_spmm_rowmajor(const lg_csr* a, const double* x, double* y, int k, lg_ws* 
                      void* stream) {
   if (!a || !x || !y || k < 1 || k > 16 || !ws)
     return fail(LG_EINVAL, "lg_spmm_rowmajor: bad argument (1 <= k <= 16, workspace)");
-  if (!a->packed) return fail(LG_EINVAL, "lg_spmm_rowmajor: needs the packed format");
+  if (!a->packed || !a->pdiag)
+    return fail(LG_EINVAL, "lg_spmm_rowmajor: needs the packed format with its diagonal");
   if (a->n == 0 || a->nblocks == 0) return LG_OK;
   const int K = k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
   if (a->nlong) {
@@ -1500,6 +1505,7 @@ extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr*
   build_schedule(n, prp.data(), a->cta, blocks, lnp, lfirst, &absent);
 
   lg_csr* b = new lg_csr();
+  b->is_block = 1;
   b->cta = a->cta;
   b->n = n;
   b->nnz = m + nloc;
@@ -1603,26 +1609,28 @@ static int make_part(const lg_csr* a, int64_t r0, int64_t r1, const std::vector<
   b->cbits = a->cbits;
   b->nvals = a->nvals;
   b->noff = m;
-  b->pcol = words;
+  b->is_block = (r0 > 0 || r1 < n) ? 1 : 0;
   b->nblocks = (int64_t)blocks.size();
   set_chunks(b, blocks);
   b->nlong = (int64_t)lnp.size();
   for (int32_t v : lnp) b->nparts += v;
   bool ok = cudaMalloc(&b->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
-            cudaMalloc(&b->pdiag, 8 * (size_t)n) == cudaSuccess &&
+            (!with_diag || cudaMalloc(&b->pdiag, 8 * (size_t)n) == cudaSuccess) &&
             (b->nvals == 0 || cudaMalloc(&b->table, 8 * (size_t)b->nvals) == cudaSuccess) &&
             (b->nblocks == 0 ||
              cudaMalloc(&b->blocks, sizeof(SpmvBlock) * (size_t)b->nblocks) == cudaSuccess) &&
             (b->nlong == 0 || (cudaMalloc(&b->long_nparts, 4 * (size_t)b->nlong) == cudaSuccess &&
                                cudaMalloc(&b->long_first, 8 * (size_t)b->nlong) == cudaSuccess));
   if (!ok) {
-    lg_csr_destroy(b);
+    lg_csr_destroy(b);  // words stay the caller's on failure
     return fail(LG_ENOMEM, "lg_csr_split_cols: allocation failed");
   }
+  b->pcol = words;
   cudaMemcpy(b->prp, prp.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice);
-  cudaMemset(b->pdiag, 0, 8 * (size_t)n);
-  if (with_diag)
+  if (with_diag) {  // parts without the diagonal keep pdiag NULL (nothing to stream)
+    cudaMemset(b->pdiag, 0, 8 * (size_t)n);
     cudaMemcpy(b->pdiag + r0, a->pdiag + r0, 8 * (size_t)nloc, cudaMemcpyDeviceToDevice);
+  }
   if (b->nvals) cudaMemcpy(b->table, a->table, 8 * (size_t)b->nvals, cudaMemcpyDeviceToDevice);
   if (b->nblocks)
     cudaMemcpy(b->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
@@ -1786,6 +1794,8 @@ extern "C" int lg_csr_col_panel(const lg_csr* a, int64_t c0, int64_t c1, int wit
 extern "C" int lg_csr_set_panels(lg_csr* a, int p) {
   if (!a || p < 0 || p > 16) return fail(LG_EINVAL, "lg_csr_set_panels: bad argument");
   if (p > 1 && !a->packed) return fail(LG_EINVAL, "lg_csr_set_panels: only for packed matrices");
+  if (p > 1 && a->is_block)
+    return fail(LG_EINVAL, "lg_csr_set_panels: only for full operators (this one has absent rows)");
   cudaDeviceSynchronize();
   for (int k = 0; k < a->npanels; ++k) lg_csr_destroy(a->panel[k]);
   a->npanels = 0;
@@ -1895,6 +1905,10 @@ extern "C" int lg_csr_row_ptr(const lg_csr* a, int64_t* host_out) {
 extern "C" int lg_csr_diagonal(const lg_csr* a, double* d_out) {
   if (!a || !d_out) return fail(LG_EINVAL, "lg_csr_diagonal: bad argument");
   if (!a->packed) return fail(LG_EINVAL, "lg_csr_diagonal: only for packed matrices");
+  if (!a->pdiag) {  // a part without the diagonal
+    LG_CUDA(cudaMemset(d_out, 0, 8 * (size_t)a->n));
+    return LG_OK;
+  }
   LG_CUDA(cudaMemcpy(d_out, a->pdiag, 8 * (size_t)a->n, cudaMemcpyDeviceToDevice));
   return LG_OK;
 }
@@ -2092,7 +2106,7 @@ static int plain_from_device(int64_t n, int64_t* rp, int32_t* col, double* val, 
 extern "C" int lg_fsai_device(const lg_csr* a, int kmax, lg_csr** g_out, lg_csr** gt_out) {
   if (!a || !g_out || !gt_out || kmax < 1 || kmax > kFsaiMax)
     return fail(LG_EINVAL, "lg_fsai_device: bad argument (1 <= kmax <= 32)");
-  if (!a->packed || a->nvals != 1)
+  if (!a->packed || a->nvals != 1 || !a->pdiag)
     return fail(LG_EINVAL, "lg_fsai_device: needs a packed matrix with one off-diagonal value "
                            "(use the host setup, lg_fsai_factorize, otherwise)");
   const int64_t n = a->n;

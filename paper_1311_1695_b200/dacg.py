@@ -410,9 +410,11 @@ def dacg_smallest(a, neig, delta=1e-6, f=None, null_basis=None,
     maxit_per_pair.
 
     comm (extension, not in the reference): a dist.RowComm -- this process is
-    one rank of a row-partitioned solve; f is then a
-    JacobiFactor, 'jacobi' or 'block_ic0' (default: block-Jacobi IC(0)), and
-    every rank returns the same pairs."""
+    one rank of a row-partitioned solve; f is then None or
+    'fsai' (the default: FSAI as two row-partitioned products, the same
+    preconditioner at every rank count), an FsaiFactor, an Ic0JacobiFactor,
+    a JacobiFactor, 'jacobi' or 'block_ic0' (dist.RowComm.local_preconditioner),
+    and every rank returns the same pairs."""
     with dev.solver_stream():
         return _dacg(a, neig, delta, f, null_basis, maxit_per_pair, seed, counter, x0, comm)
 

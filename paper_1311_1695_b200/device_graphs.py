@@ -25,11 +25,13 @@ from .sparse import DeviceCsr
 class DeviceLaplacian:
     """Unit-weight graph Laplacian held only on the device."""
 
-    def __init__(self, n, m, handle):
+    def __init__(self, n, m, handle, panels=True):
         self.n = int(n)
         self.m = int(m)
         self.symmetric = True
-        self._dev = DeviceCsr.from_handle(handle, self.n, self.n + 2 * self.m).auto_panels()
+        self._dev = DeviceCsr.from_handle(handle, self.n, self.n + 2 * self.m)
+        if panels:  # off when only row blocks of it are multiplied (N > 1)
+            self._dev.auto_panels()
 
     @property
     def nnz(self):
@@ -44,9 +46,12 @@ class DeviceLaplacian:
         return dev.to_host(d)
 
 
-def rmat_laplacian_device(scale, edge_factor, a=0.57, b=0.19, c=0.19, seed=0, lcc=True):
+def rmat_laplacian_device(scale, edge_factor, a=0.57, b=0.19, c=0.19, seed=0, lcc=True,
+                          panels=True):
     """Sample an R-MAT graph on the device, keep its largest component and
-    assemble its Laplacian in the packed SpMV format."""
+    assemble its Laplacian in the packed SpMV format.  panels=False skips the
+    column panels of the full product (for row-partitioned use, where only
+    row blocks of the operator are multiplied)."""
     dev.require_cuda()
     di, dj = ctypes.c_void_p(), ctypes.c_void_p()
     m = ctypes.c_int64()
@@ -65,4 +70,4 @@ def rmat_laplacian_device(scale, edge_factor, a=0.57, b=0.19, c=0.19, seed=0, lc
     finally:
         nat.load().lg_free(di)
         nat.load().lg_free(dj)
-    return DeviceLaplacian(n, mm, h)
+    return DeviceLaplacian(n, mm, h, panels=panels)

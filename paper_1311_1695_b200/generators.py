@@ -13,8 +13,11 @@ every graph is reproducible on any host with the same numpy.
     rmat_graph          C3 / C5  R-MAT (a, b, c, d) edge sampling
     config_graph(name)  the BASELINE configurations, LCC applied
 
-plus the small deterministic families the tests use (path, cycle, complete,
-star, grid).
+plus the reference's own fixture families (generators.py:8-107: path,
+cycle, complete, star, grid, and the seeded random_connected_graph /
+geometric_graph that its test suite draws from), restated so the same seeds
+give the same edge lists (pinned against kat_graphs.npz,
+tests/test_oracle_golden.py).
 """
 
 import numpy as np
@@ -52,6 +55,52 @@ def grid_graph(rows, cols, weight=1.0):
     i = np.concatenate([ids[:, :-1].ravel(), ids[:-1, :].ravel()])
     j = np.concatenate([ids[:, 1:].ravel(), ids[1:, :].ravel()])
     return EdgeList(rows * cols, i, j, np.full(i.size, float(weight)))
+
+
+def random_connected_graph(n, extra_edges=0, seed=0, weighted=True):
+    """A random tree (each node v > 0 hangs off a uniform earlier node) plus
+    up to extra_edges distinct random chords, drawn with at most
+    50 (extra_edges + 1) attempts; weights U(0.5, 1.5) drawn after the edges
+    (reference generators.py:47-68, same default_rng call sequence)."""
+    rng = np.random.default_rng(seed)
+    edges = {(int(rng.integers(0, v)), v) for v in range(1, n)}
+    target, tries = n - 1 + extra_edges, 0
+    while len(edges) < target and tries < 50 * (extra_edges + 1):
+        u, v = (int(t) for t in rng.integers(0, n, size=2))
+        tries += 1
+        if u != v:
+            edges.add((u, v) if u < v else (v, u))
+    ij = np.array(sorted(edges), dtype=np.int64).reshape(-1, 2)
+    m = ij.shape[0]
+    w = rng.uniform(0.5, 1.5, size=m) if weighted else np.ones(m)
+    return EdgeList(n, ij[:, 0], ij[:, 1], w)
+
+
+def geometric_graph(n, radius, seed=0, weighted=False):
+    """Uniform points in the unit square, joined when closer than radius
+    (weight 1 / (1 + distance) when weighted); while disconnected, the
+    component of node 0 is joined to its nearest outside node (reference
+    generators.py:71-107)."""
+    from .graphs import connected_components
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, 2))
+    d2 = ((pts[:, None, :] - pts[None, :, :]) ** 2).sum(axis=2)
+    iu, ju = np.triu_indices(n, k=1)
+    near = d2[iu, ju] < radius * radius
+    i, j = iu[near], ju[near]
+    w = 1.0 / (1.0 + np.sqrt(d2[i, j])) if weighted else np.ones(i.size)
+    g = EdgeList(n, i, j, w)
+    while True:
+        count, labels = connected_components(g)
+        if count == 1:
+            return g
+        inside = np.flatnonzero(labels == labels[0])
+        outside = np.flatnonzero(labels != labels[0])
+        k = int(np.argmin(d2[np.ix_(inside, outside)]))
+        u, v = int(inside[k // outside.size]), int(outside[k % outside.size])
+        wt = 1.0 / (1.0 + np.sqrt(d2[u, v])) if weighted else 1.0
+        g = EdgeList(n, np.append(g.i, min(u, v)), np.append(g.j, max(u, v)),
+                     np.append(g.w, wt))
 
 
 # --------------------------------------------------------- canonicalisation

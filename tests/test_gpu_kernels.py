@@ -254,6 +254,10 @@ def test_ic0_configs(L, cfg):
     assert abs(np.linalg.norm(z) - ref["ic0_apply_x_seed0"]["norm"]) <= \
         1e-12 * ref["ic0_apply_x_seed0"]["norm"]
     assert np.allclose(z[:8], ref["ic0_apply_x_seed0"]["head"], rtol=1e-11, atol=0)
+    # elementwise against the oracle's SuperLU apply of the same factor
+    # (ic0.py:40-45 restated), relative to the largest entry
+    zr = O.Ic0(a.n, f.l.row_ptr, f.l.col_idx, f.l.values).apply(x)
+    assert np.max(np.abs(z - zr)) <= 1e-12 * np.max(np.abs(zr))
     # L L^T z = x (inverse property, size independent)
     Lm = O.Csr(a.n, f.l.row_ptr, f.l.col_idx, f.l.values)
     import scipy.sparse as sp
@@ -598,6 +602,38 @@ def test_panelled_operator_solves_match():
     assert np.max(np.abs(got_j.values - ref_j.values) / ref_j.values) <= 1e-8
     d.matvec(x, y2, theta=0.37)
     assert bool((y2 == want).all())
+
+
+def test_set_panels_rejects_row_blocks():
+    """Column panels need a full operator: lg_csr_set_panels refuses a row
+    block (host-built SKIP_EMPTY, or cut on the device), and LG_SPMV_PANELS
+    never reaches a row block, so absent rows are still left untouched."""
+    import os
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.dist import (RowPartition, device_row_ptr, local_operator,
+                                           local_operator_device)
+    import paper_1311_1695_b200 as L
+    a = L.build_laplacian(L.config_graph("C1"))
+    part = RowPartition(a.row_ptr, 2)
+    blk = local_operator(a, part, 1)
+    with pytest.raises(ValueError, match="full operators"):
+        blk.set_panels(2)
+    A = rmat_laplacian_device(12, 8, seed=3)
+    dblk = local_operator_device(A.device(), RowPartition(device_row_ptr(A.device()), 2), 0)
+    with pytest.raises(ValueError, match="full operators"):
+        dblk.set_panels(3)
+    os.environ["LG_SPMV_PANELS"] = "3"
+    try:
+        blk2 = local_operator(a, part, 0)
+    finally:
+        del os.environ["LG_SPMV_PANELS"]
+    assert blk2.npanels == 0
+    r0, r1 = part.rows(0)
+    x = dev.to_device(np.random.default_rng(2).standard_normal(a.n))
+    y = dev.to_device(np.full(a.n, 7.0))
+    blk2.matvec(x, y)
+    assert bool((y[r1:] == 7.0).all())
 
 
 def test_spmv_256_thread_schedule_parity():
