@@ -328,7 +328,9 @@ int lg_fused_prog(const lg_fused_args* args, double* slots, int* flags, const ui
                   int nops, const double* imm, int nimm, lg_ws* ws, void* stream);
 
 /* Out[:, 0:p] = In[:, 0:m] * Y  (Y is m x p column-major, host, copied by
- * value into the launch; m <= 64, p <= 32; In/Out column-major ld = n). */
+ * value into the launches; any m, p: tiles of <= 32 output columns and
+ * <= 1024 / width input columns, later input tiles accumulating in order;
+ * In/Out column-major ld = n). */
 int lg_gemm_small(int64_t n, const double* in, int64_t ldi, int m,
                   const double* y_h, int p, double* out, int64_t ldo,
                   void* stream);

@@ -282,6 +282,7 @@ struct GemmArgs {
   int p;
   double* out;
   int64_t ldo;
+  int acc;  // add into out (a later row panel of Y)
   double y[kGemmMaxY];
 };
 
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(kThreads) gemm_small_kernel(const __grid_const
        i += stride) {
     double acc[P];
 #pragma unroll
-    for (int c = 0; c < P; ++c) acc[c] = 0.0;
+    for (int c = 0; c < P; ++c) acc[c] = (a.acc && c < a.p) ? a.out[i + (int64_t)c * a.ldo] : 0.0;
     for (int j = 0; j < a.m; ++j) {
       double v = a.in[i + (int64_t)j * a.ldi];
 #pragma unroll
@@ -415,27 +416,38 @@ int lg_fused_prog(const lg_fused_args* args, double* slots, int* flags, const ui
 int lg_gemm_small(int64_t n, const double* in, int64_t ldi, int m,
                   const double* y_h, int p, double* out, int64_t ldo,
                   void* stream) {
-  if (n < 0 || m < 0 || p < 0 || m > kGemmMaxM || p > kGemmMaxP || m * p > kGemmMaxY)
-    return fail(LG_EINVAL, "lg_gemm_small: bad shape (m <= 64, p <= 32, m*p <= 1024)");
+  if (n < 0 || m < 0 || p < 0) return fail(LG_EINVAL, "lg_gemm_small: bad shape");
   if (n == 0 || p == 0) return LG_OK;
   if (!out || ldo < n || (m > 0 && (!in || !y_h || ldi < n)))
     return fail(LG_EINVAL, "lg_gemm_small: bad pointer / leading dimension");
+  // Tiles of <= 32 output columns x <= 1024 / width input columns, each one
+  // launch with its Y tile by value; later input tiles accumulate into out,
+  // so every output keeps the sequential j order of a single pass.
   static thread_local GemmArgs a;  // large by-value launch parameter (host staging)
-  a.n = n;
-  a.in = in;
-  a.ldi = ldi;
-  a.m = m;
-  a.p = p;
-  a.out = out;
-  a.ldo = ldo;
-  std::memcpy(a.y, y_h, sizeof(double) * (size_t)(m * p));
-  int g = vec_grid(n);
   cudaStream_t s = (cudaStream_t)stream;
-  if (p <= 4) gemm_small_kernel<4><<<g, kThreads, 0, s>>>(a);
-  else if (p <= 8) gemm_small_kernel<8><<<g, kThreads, 0, s>>>(a);
-  else if (p <= 16) gemm_small_kernel<16><<<g, kThreads, 0, s>>>(a);
-  else gemm_small_kernel<32><<<g, kThreads, 0, s>>>(a);
-  LG_LAUNCH_CHECK("gemm_small_kernel");
+  const int g = vec_grid(n);
+  for (int c0 = 0; c0 < p; c0 += kGemmMaxP) {
+    const int pw = std::min(kGemmMaxP, p - c0);
+    const int mt = std::min(kGemmMaxM, kGemmMaxY / pw);
+    for (int j0 = 0; j0 < std::max(m, 1); j0 += mt) {
+      const int mw = std::min(mt, m - j0);
+      a.n = n;
+      a.in = in + (int64_t)j0 * ldi;
+      a.ldi = ldi;
+      a.m = std::max(mw, 0);
+      a.p = pw;
+      a.out = out + (int64_t)c0 * ldo;
+      a.ldo = ldo;
+      a.acc = j0 > 0;
+      for (int c = 0; c < pw; ++c)
+        for (int j = 0; j < a.m; ++j) a.y[j + c * a.m] = y_h[(j0 + j) + (int64_t)(c0 + c) * m];
+      if (pw <= 4) gemm_small_kernel<4><<<g, kThreads, 0, s>>>(a);
+      else if (pw <= 8) gemm_small_kernel<8><<<g, kThreads, 0, s>>>(a);
+      else if (pw <= 16) gemm_small_kernel<16><<<g, kThreads, 0, s>>>(a);
+      else gemm_small_kernel<32><<<g, kThreads, 0, s>>>(a);
+      LG_LAUNCH_CHECK("gemm_small_kernel");
+    }
+  }
   return LG_OK;
 }
 

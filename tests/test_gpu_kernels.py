@@ -708,3 +708,23 @@ def test_spmm_rowmajor_matches_spmv(k):
     oa = O.Csr(a.n, a.row_ptr, a.col_idx, a.values)
     th_o, res_o = O.rayleigh_residuals(oa, V)
     assert np.allclose(th, th_o, rtol=1e-12) and np.allclose(res, res_o, rtol=1e-10)
+
+
+@pytest.mark.parametrize("m,p", [(0, 3), (5, 1), (60, 20), (120, 51), (64, 32), (7, 70)])
+def test_gemm_small_any_shape(m, p):
+    """lg_gemm_small tiles any (m, p): IRLM's Ritz vectors at neig 20
+    (ncv 60) and 50 (ncv 120) exceed one 64 x 32 / 1024-entry tile (the
+    reference's acceptance criterion 1 runs neig 20, test_acceptance.py:102)."""
+    import ctypes
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200 import _native as nat
+    n = 1000
+    rng = np.random.default_rng(m * 100 + p)
+    src = rng.standard_normal((max(m, 1), n))
+    y = np.asfortranarray(rng.standard_normal((m, p)))
+    sd, out = dev.to_device(src), dev.to_device(np.full((p, n), 3.0))
+    nat.call("lg_gemm_small", n, sd.data_ptr(), n, m, y.ctypes.data if m else None, p,
+             out.data_ptr(), n, ctypes.c_void_p(dev.stream_ptr()))
+    want = (src[:m].T @ y).T
+    got = dev.to_host(out)
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
