@@ -134,6 +134,16 @@ def cpu_spmv_threads(rp, col, val, x, nthreads, chunks):
     return y
 
 
+def bench_config(config, n, nnz, world):
+    """The `config` object both arms print (identical, so the driver can pair
+    the lines)."""
+    return {"workload": f"{config}: one SpMV of the weighted Laplacian (BASELINE configs[3], LCC)"
+                        if config == "C4" else f"{config}: one SpMV of the graph Laplacian",
+            "n": n, "nnz": nnz,
+            "l2": "flushed between steps (256 MiB write, untimed)",
+            "parallelism": f"rows{world}" if world > 1 else "single"}
+
+
 def reference_arm(args):
     """CPU reference arm: the oracle restatement of the reference SpMV."""
     rank = int(os.environ.get("RANK", "0"))
@@ -165,8 +175,7 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: SpMV of the weighted Laplacian",
-                   "n": n, "nnz": nnz},
+        "config": bench_config(args.config, n, nnz, int(os.environ.get("WORLD_SIZE", "1"))),
         "effective_gbs": algo / (ms * 1e-3) / 1e9,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
                          "sample": f"{args.steps} full {args.config} matvecs, oracle reduceat "
@@ -193,6 +202,71 @@ def cpu_baseline_sample(g, seconds=10.0):
     return {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
             "sample": f"{reps} oracle matvecs (np.add.reduceat, sparse.py:128-139) in "
                       f"{reps * dt:.1f} s on one host core"}
+
+
+def _event_timer(fn, flush=None, reps=20):
+    """Median CUDA-event time of fn() in microseconds on the current stream,
+    L2 flushed before every rep (untimed) when a flush buffer is given."""
+    import torch
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    s = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
+    for i in range(reps):
+        if flush is not None:
+            flush.fill_(i & 0xff)
+        s[i].record(st)
+        fn()
+        e[i].record(st)
+    torch.cuda.synchronize()
+    return 1e3 * float(np.median([a.elapsed_time(b) for a, b in zip(s, e)]))
+
+
+def cpu_solvers_block(budget_s=25.0):
+    """The reference solvers timed on THIS box's host cores in this run: the
+    oracle's restatements of dacg_smallest / jd_smallest / irlm_smallest
+    (pinned to the reference's golden eigenvalues and MVP counts,
+    tests/test_oracle_golden.py), each with a shared precomputed IC(0) factor
+    exactly as the reference harness does (bench.py:123-158 of the reference:
+    factorisation outside the timed solve).  Runs longer than budget_s stop at
+    the deadline; their wall time is projected as (time per MVP so far) x (the
+    reference's MVP count), and says so.  Rank 0, N = 1 only."""
+    from oracle import lapeig_oracle as O
+    runs = {"C1": ("dacg", "jd", "irlm"), "C2": ("dacg", "jd"), "C3": ("jd",),
+            "C4": ("dacg", "jd")}
+    fns = {"dacg": O.dacg, "jd": O.jd, "irlm": O.irlm}
+    out = {"cores": os.cpu_count(),
+           "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS", "default"),
+           "kind": "port", "note": "oracle restatement of the reference solvers; SpMV and "
+           "SuperLU-equivalent triangular solves single-threaded like the reference"}
+    for cfg, solvers in runs.items():
+        gold = json.loads((ROOT / "tests" / "golden" / f"config_{cfg}.json").read_text())
+        g = build_graph(cfg)
+        rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+        a = O.Csr(g.n_nodes, rp, col, val)
+        lrp, lcol, lval, _, _ = O.ic0_factorize(a)
+        f = O.Ic0(a.n, lrp, lcol, lval)
+        for name in solvers:
+            r = gold["solvers"][name]
+            t0 = time.perf_counter()
+            rec = {"neig": gold["neig"], "delta": gold["delta"], "reference_mvp": r["mvp"]}
+            try:
+                res = fns[name](a, gold["neig"], delta=gold["delta"], f=f,
+                                deadline=t0 + budget_s)
+                rec.update(wall_s=time.perf_counter() - t0, mvp=res.mvp, projected=False,
+                           eig_relerr_vs_golden=float(np.max(
+                               np.abs(res.values - r["eigenvalues"]) /
+                               np.abs(r["eigenvalues"]))))
+            except TimeoutError:
+                dt = time.perf_counter() - t0
+                done = max(1, a.count)
+                rec.update(wall_s=dt / done * r["mvp"], projected=True,
+                           sample=f"{done} MVPs in {dt:.1f} s, projected to the reference's "
+                                  f"{r['mvp']} MVPs")
+            out[f"{cfg}_{name}"] = rec
+    return out
 
 
 def _ncu_traffic(config, world):
@@ -492,6 +566,7 @@ def main():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-vendor", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -582,6 +657,8 @@ def main():
             + 16 * local_rows + 8 * (n - local_rows)
     else:
         local_stream = local_algo
+    if world == 1:
+        local_stream = d.stream_bytes   # exactly what the launch streams (lg_csr_info)
     peaks, peak_kind = _peaks()
     # e2e through the public API with host buffers (rank 0 replica path)
     xh = np.random.default_rng(1).standard_normal(n)
@@ -620,10 +697,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: one SpMV of the weighted Laplacian "
-                               f"(BASELINE configs[3], LCC)", "n": n, "nnz": nnz,
-                   "l2": "flushed between steps (256 MiB write, untimed)",
-                   "parallelism": f"rows{world}" if world > 1 else "single"},
+        "config": bench_config(args.config, n, nnz, world),
         "effective_gbs": algo / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": local_stream / (ms * 1e-3) / 1e9,
                      "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -632,8 +706,9 @@ def main():
                      "bytes_per_launch": local_stream,
                      "format": "packed Laplacian (4 B / off-diagonal + diag vector)"
                                if d.packed else "CSR f64 / int32",
-                     "bytes_model": ("4 (nnz - n) + 8 (n+1) + 8 n + 16 n (packed)" if d.packed
-                                     else "12 nnz + 8 (n+1) + 16 n (SURVEY 8(d))"),
+                     "bytes_model": ("4 (nnz - n) + 96 B per warp block (row structure) + 8 n "
+                                     "(diagonal) + 16 n (x, y) (packed)" if d.packed
+                                     else "12 nnz + 96 B per warp block + 16 n"),
                      "effective_bytes_model": "12 nnz + 8 (n+1) + 16 n (SURVEY 8(d))",
                      # the kernel is bound by the L1TEX sector rate of the
                      # random x gathers, not by HBM: one gather per
@@ -649,8 +724,10 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    line_factor = {}
     if rank == 0 and world == 1 and not args.no_solve:
         f = L.ic0_factorize(a)
+        line_factor["f"] = f
         f_mc = L.ic0_factorize_multicolor(a)
         f.device()
         f_mc.device()   # device factor upload = setup, like the reference's splu
@@ -666,6 +743,28 @@ def main():
             line["c5"] = c5
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(g)
+        if not args.no_solve:
+            cs = cpu_solvers_block()
+            line["cpu_solvers"] = cs
+            # time-to-solution speed-up against the reference solvers timed on
+            # this box in this run (same graph, neig, delta, preconditioner)
+            for blk, key_of in (("solve_configs", lambda k: k),
+                                ("solve", lambda k: "C4_" + k)):
+                for k, v in line.get(blk, {}).items():
+                    if "preconditioner" in v and "reference" not in v["preconditioner"]:
+                        base = k.rsplit("_", 1)[0] if blk == "solve_configs" else k.split("_")[0]
+                    else:
+                        base = k
+                    c = cs.get(key_of(base))
+                    if c and v.get("wall_s"):
+                        v["reference_wall_s_same_box"] = c["wall_s"]
+                        v["reference_wall_projected"] = c["projected"]
+                        v["speedup_vs_reference_same_box"] = c["wall_s"] / v["wall_s"]
+    if rank == 0 and world == 1 and not args.no_vendor:
+        sys.path.insert(0, str(ROOT / "scripts"))
+        from vendor_cusparse import vendor_block
+        fv = line_factor.get("f")
+        line["vendor"] = vendor_block(a, fv, x, _event_timer)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -28,6 +28,7 @@
 //     int32 column): the SpMV streams 2.2x fewer bytes on C4 and the value
 //     actually multiplied is bit-identical to the stored one.
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -37,25 +38,54 @@
 
 namespace lg {
 
-// The CTA size T is chosen per matrix (128 or 256 threads, lg_csr.cta); a
-// row block holds at most T * kPer nonzeros, so the schedule depends on it.
-// 256 pays on very large matrices (C5: rows of 1-2 K nonzeros stay in one
-// block instead of becoming ticketed long-row parts; 15.1 -> 13.0 ms), 128
-// on the rest (C3: 32.8 vs 34.8 us, C4 equal).
-constexpr int kPer = 8;        // stream words per thread per block
-constexpr int kST = 128;       // default CTA size (and of the build kernels)
-constexpr int kRowCap = 1024;  // rows per normal block
-constexpr int kShortRow = 32;  // rows up to this length: one thread each
+// Warp-block schedule (built once per operator on the host, O(n + nnz/8)).
+// A normal block is at most kWin stream positions of whole rows; its window
+// starts at the 16-byte-aligned position at or below its first nonzero, so a
+// lane's eight words are two aligned 128-bit loads.  A row longer than
+// kLongPart (power-law hubs: 107,553 nonzeros in C4's largest row) is cut into
+// parts of kLongPart from its first nonzero.  Every block therefore streams
+// about the same bytes, which is what balances degree-skewed graphs.
+constexpr int kWPer = 8;                 // stream words per lane
+constexpr int kWin = 32 * kWPer;         // window of one warp block (positions)
+constexpr int kLongPart = kWin - 4;      // part length of a long row
+constexpr int kWRows = 256;              // rows per normal block (8-bit offsets)
+constexpr int kWThreads = 256;           // CTA size of the SpMV (8 warps)
 #ifndef LG_SPMV_MINB
-#define LG_SPMV_MINB 12   // resident 128-thread CTAs per SM (register bound)
+#define LG_SPMV_MINB 4                   // resident CTAs per SM (register cap 64)
+#endif
+#ifndef LG_SPMV_PIPE
+#define LG_SPMV_PIPE 1                   // next block's loads before this block's work
+#endif
+constexpr int kST = 128;                 // CTA size of the build kernels
+// every stream array (pcol / col / val) is allocated with this many slack
+// entries, so a lane's two 128-bit loads never leave the allocation
+constexpr int64_t kStreamPad = 8;
+
+enum : int32_t { kBlkLong = -1, kBlkSeg = 0, kBlkRows = 1 };
+
+// -DLG_SPMV_CHECK: bounds-check every index the SpMV kernel uses (debug)
+#ifdef LG_SPMV_CHECK
+#define LG_CK(c, what)                                                                 \
+  do {                                                                                 \
+    if (!(c)) {                                                                        \
+      printf("lg_spmv check failed: %s (block %d thread %d)\n", what, blockIdx.x,      \
+             threadIdx.x);                                                             \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define LG_CK(c, what) do { } while (0)
 #endif
 
 struct SpmvBlock {
   int64_t nz0, nz1;  // nonzero range
   int32_t row0;      // first row
   int32_t nrows;     // rows (normal) / long-row id (long)
-  int32_t lshift;    // log2(lanes per row) (normal); -1 marks a long-row part
+  int32_t lshift;    // kind: kBlkLong part, kBlkSeg segmented, kBlkRows row-serial
   int32_t part;      // compact long-part slot (long)
+  // kBlkSeg: per lane, bits 0-7 flag the window positions where a row starts,
+  // bits 8-15 the row (relative to row0) of the lane's first valid position
+  uint16_t meta[32];
 };
 
 }  // namespace lg
@@ -82,7 +112,6 @@ struct lg_csr {
   int64_t* long_first = nullptr;   // device [nlong] slot of part 0
   // row chunks of the schedule for the host-buffer path (lg_spmv_host):
   // blocks [chunk_b[c], chunk_b[c+1]) cover rows [chunk_row[c], chunk_row[c+1])
-  int cta = 128;                   // CTA size the schedule was cut for
   int nchunks = 0;
   int64_t chunk_b[9] = {};
   int64_t chunk_row[9] = {};
@@ -93,6 +122,11 @@ struct lg_csr {
   // rows absent from the schedule (SKIP_EMPTY, row blocks, split halves):
   // such an operator is not a full operator and cannot be panelled
   int is_block = 0;
+  // compacted schedule (an operator whose rows with entries are scattered,
+  // e.g. a column panel): schedule row i is matrix row rowmap[i]
+  int32_t* rowmap = nullptr;       // device [rows with entries] or NULL
+  // columns a column panel reads (x[pf_c0:pf_c1] is what it prefetches)
+  int64_t pf_c0 = 0, pf_c1 = 0;
 };
 
 namespace lg {
@@ -109,6 +143,7 @@ struct SpmvArgs {
   const double* table;
   int nvals;
   int cbits;
+  int64_t nzs;              // stream length (bounds the 128-bit loads)
   const SpmvBlock* blocks;
   int64_t nblocks;
   const int32_t* long_nparts;
@@ -119,323 +154,362 @@ struct SpmvArgs {
   double theta_h;
   const double* theta_d;
   int theta_neg;
-  int ndots;
-  const double* dvec[LG_MAXD];
-  const double* q;
-  int64_t ldq;
-  int nq;
-  double* out;
   const int* skip;
+  const int32_t* rowmap;   // schedule row -> matrix row (NULL: identity)
+  // L2 prefetch regions issued at kernel start (x, diagonal): the gathers of
+  // a cold x then hit L2 instead of paying DRAM latency one sector at a time
+  const void* pf[2];
+  int64_t pf_bytes[2];
+  int64_t nparts, nlong;    // bounds (LG_SPMV_CHECK builds)
   double* long_part;   // [nparts] partial of each long-row part
   unsigned* long_ticket;  // [nlong]
-  int64_t nlong;
 };
 
-template <int NA, int M>
-__device__ __forceinline__ void epilogue_row(const SpmvArgs& a, int64_t r,
-                                             double yr, double (&acc)[M]) {
-  if constexpr (NA > 0) {
+// One lane's eight stream positions [p, p + 8): two aligned 128-bit loads
+// (the window may start up to 3 positions before the block and run past its
+// end -- those positions are masked -- and the arrays carry kStreamPad slack
+// entries, so the loads never leave the allocation).
+template <bool PACKED>
+struct WWords {
+  uint32_t w[kWPer];
+  double v[PACKED ? 1 : kWPer];
+};
+
+template <bool PACKED>
+__device__ __forceinline__ void wload(const SpmvArgs& a, int64_t p, WWords<PACKED>& L) {
+  LG_CK(p >= 0 && p + kWPer <= a.nzs + kStreamPad, "stream window");
 #pragma unroll
-    for (int d = 0; d < NA; ++d) {
-      if (d < a.ndots) {
-        const double* v = a.dvec[d];
-        acc[d] += yr * (v ? v[r] : yr);
-      } else if (d < a.ndots + a.nq) {
-        acc[d] += yr * a.q[r + (int64_t)(d - a.ndots) * a.ldq];
-      }
+  for (int h = 0; h < 2; ++h) {
+    const int64_t q = p + 4 * h;
+    uint4 u;
+    if constexpr (PACKED) u = __ldcs(reinterpret_cast<const uint4*>(a.pcol + q));
+    else u = __ldcs(reinterpret_cast<const uint4*>(a.col + q));
+    L.w[4 * h] = u.x; L.w[4 * h + 1] = u.y; L.w[4 * h + 2] = u.z; L.w[4 * h + 3] = u.w;
+    if constexpr (!PACKED) {
+      const double2 v0 = __ldcs(reinterpret_cast<const double2*>(a.val + q));
+      const double2 v1 = __ldcs(reinterpret_cast<const double2*>(a.val + q + 2));
+      L.v[4 * h] = v0.x; L.v[4 * h + 1] = v0.y; L.v[4 * h + 2] = v1.x; L.v[4 * h + 3] = v1.y;
     }
   }
 }
 
-
-// Stream words of one block held in registers: issued one block ahead so the
-// DRAM latency of the column / value stream overlaps the current block's
-// gathers and row reductions (software pipelining across blocks).
+// products of the valid positions (vm bit j) of one lane's window; the eight
+// gathers are issued before any multiply
 template <bool PACKED>
-struct Staged {
-  uint32_t w[kPer];                 // packed: col | vidx << cbits; plain: col
-  double v[PACKED ? 1 : kPer];      // plain: values
-};
-
-template <bool PACKED, int T>
-__device__ __forceinline__ void stage(const SpmvArgs& a, const SpmvBlock& blk, int tid,
-                                      Staged<PACKED>& st) {
-  const int cnt = (int)(blk.nz1 - blk.nz0);
+__device__ __forceinline__ void wproducts(const SpmvArgs& a, const WWords<PACKED>& L,
+                                          unsigned vm, const double* tab, uint32_t cmask,
+                                          double (&p)[kWPer]) {
+  double xv[kWPer];
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int e = tid + j * T;
-    if (e < cnt) {
-      const int64_t k = blk.nz0 + e;
-      if constexpr (PACKED) {
-        st.w[j] = __ldcs(a.pcol + k);
-      } else {
-        st.w[j] = (uint32_t)__ldcs(a.col + k);
-        st.v[j] = __ldcs(a.val + k);
-      }
-    }
+  for (int j = 0; j < kWPer; ++j) {
+    const uint32_t c = PACKED ? (L.w[j] & cmask) : L.w[j];
+    if ((vm >> j) & 1u) LG_CK(c < (uint32_t)a.n, "gather column");
+    xv[j] = ((vm >> j) & 1u) ? __ldg(a.x + c) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < kWPer; ++j) {
+    if constexpr (PACKED) p[j] = xv[j] * tab[((vm >> j) & 1u) ? (L.w[j] >> a.cbits) : 0u];
+    else p[j] = ((vm >> j) & 1u) ? L.v[j] * xv[j] : 0.0;
   }
 }
 
 template <bool PACKED>
-__device__ __forceinline__ double product(const SpmvArgs& a, const Staged<PACKED>& st, int j,
-                                          const double* tab, uint32_t cmask) {
-  if constexpr (PACKED) {
-    const uint32_t w = st.w[j];
-    return tab[w >> a.cbits] * __ldg(a.x + (w & cmask));
-  } else {
-    return st.v[j] * __ldg(a.x + st.w[j]);
-  }
-}
-
-template <bool PACKED>
-__device__ __forceinline__ double finish_row(const SpmvArgs& a, int64_t r, double s,
-                                             double theta) {
+__device__ __forceinline__ void finish_row(const SpmvArgs& a, int64_t r, double s,
+                                           double theta) {
+  if (a.rowmap) r = a.rowmap[r];
+  LG_CK(r >= 0 && r < a.n, "row");
   if constexpr (PACKED) {
     if (a.pdiag) s += a.pdiag[r] * __ldg(a.x + r);  // NULL: accumulating column panel
   }
   if (theta != 0.0) s -= theta * __ldg(a.x + r);
   if (a.accum) s = a.y[r] + s;
-  return s;
+  a.y[r] = s;
 }
 
-template <int NA, bool PACKED, int T>
-__global__ void __launch_bounds__(T, (NA <= 4 ? LG_SPMV_MINB * 128 / T
-                                              : (NA <= 16 ? 1024 / T : 256 / T)))
-spmv_kernel(SpmvArgs a, lg_ws ws) {
-  constexpr int kST = T;
-  constexpr int kSW = T / 32;
-  constexpr int kChunk = T * kPer;
+// y = A x - theta x (y += ... when accum).  Persistent grid; warp w of the
+// grid takes blocks w, w + W, ... (W warps in the grid).  A segmented block:
+// each lane multiplies its eight positions, folds them into row segments in
+// registers (left to right), and the warp joins segments that cross lanes
+// with a segmented inclusive scan over shuffles; the lane holding a row's
+// last position writes it.  No shared memory, no barrier.  Summation order is
+// fixed by the schedule, so y is bitwise reproducible.
+//
+// Software pipeline (the loop is latency-bound: descriptor -> stream words ->
+// gathers -> row writes is a chain of dependent memory round trips): while a
+// block's gathers are in flight the warp decodes the next block's descriptor,
+// issues that block's stream loads, and loads the descriptor after it.  A
+// descriptor is read with one coalesced 96-byte load (a word per lane) and
+// decoded by shuffles.
+struct WDesc {
+  int64_t nz0, nz1;
+  int32_t row0, nrows, kind, part;
+  uint32_t meta;
+};
+
+__device__ __forceinline__ uint32_t desc_word(const SpmvArgs& a, int64_t b, int lane) {
+  constexpr int kWords = (int)(sizeof(SpmvBlock) / 4);
+  return (b < a.nblocks && lane < kWords)
+             ? __ldcs(reinterpret_cast<const unsigned int*>(a.blocks + b) + lane)
+             : 0u;
+}
+
+__device__ __forceinline__ WDesc desc_decode(uint32_t w, int lane) {
+  WDesc d;
+  const unsigned m = 0xffffffffu;
+  d.nz0 = (int64_t)(((uint64_t)__shfl_sync(m, w, 1) << 32) | __shfl_sync(m, w, 0));
+  d.nz1 = (int64_t)(((uint64_t)__shfl_sync(m, w, 3) << 32) | __shfl_sync(m, w, 2));
+  d.row0 = (int32_t)__shfl_sync(m, w, 4);
+  d.nrows = (int32_t)__shfl_sync(m, w, 5);
+  d.kind = (int32_t)__shfl_sync(m, w, 6);
+  d.part = (int32_t)__shfl_sync(m, w, 7);
+  const uint32_t mw = __shfl_sync(m, w, 8 + (lane >> 1));
+  d.meta = (lane & 1) ? (mw >> 16) : (mw & 0xffffu);
+  return d;
+}
+
+__device__ __forceinline__ unsigned valid_mask(const WDesc& d, int lane) {
+  if (d.kind == kBlkRows || d.nz1 <= d.nz0) return 0u;
+  // the block's positions relative to its window: [lo, hi), lo <= 3, hi <= kWin
+  const int lo = (int)(d.nz0 & 3) - kWPer * lane;
+  const int hi = (int)(d.nz1 - (d.nz0 & ~(int64_t)3)) - kWPer * lane;
+  const int a = min(max(lo, 0), kWPer), b = min(max(hi, 0), kWPer);
+  return ((1u << b) - 1u) & ~((1u << a) - 1u);
+}
+
+template <bool PACKED>
+__global__ void __launch_bounds__(kWThreads, PACKED ? LG_SPMV_MINB : 3) wspmv_kernel(SpmvArgs a) {
   if (a.skip && *a.skip) return;
-  __shared__ double sm[kChunk];
-  extern __shared__ double tab_sm[];   // packed value table (nvals)
-  __shared__ double red_sm[kSW * (NA > 0 ? NA : 1)];
-  __shared__ int fin_flag;
-  __shared__ int wcnt_sm[kSW];
-  __shared__ int list_sm[kRowCap];
-  double acc[NA > 0 ? NA : 1];
+  // each CTA prefetches its share of the prefetch regions into L2 (bulk
+  // copy engine, 16-byte granules, one instruction per 32 KB piece)
 #pragma unroll
-  for (int d = 0; d < (NA > 0 ? NA : 1); ++d) acc[d] = 0.0;
-  double theta = a.theta_h;
-  if (a.theta_d) theta += a.theta_neg ? -*a.theta_d : *a.theta_d;
-  const int tid = threadIdx.x;
-  const uint32_t cmask = PACKED ? ((1u << a.cbits) - 1u) : 0u;
+  for (int r = 0; r < 2; ++r) {
+    if (a.pf_bytes[r] <= 0) continue;
+    const int64_t g16 = (a.pf_bytes[r] + 15) >> 4;
+    const int64_t per = (g16 + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = per * blockIdx.x, hi = g16 < lo + per ? g16 : lo + per;
+    for (int64_t q = lo + (int64_t)threadIdx.x * 2048; q < hi; q += (int64_t)kWThreads * 2048) {
+      const uint32_t bytes = (uint32_t)(16 * (hi - q < 2048 ? hi - q : (int64_t)2048));
+      const char* src = static_cast<const char*>(a.pf[r]) + 16 * q;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    }
+  }
+  extern __shared__ double tab_sm[];   // packed value table (max(nvals, 1) entries)
   if constexpr (PACKED) {
-    for (int i = tid; i < a.nvals; i += kST) tab_sm[i] = a.table[i];
+    // entry 0 always exists: masked positions read it (branch-free products)
+    for (int i = threadIdx.x; i < max(a.nvals, 1); i += kWThreads)
+      tab_sm[i] = i < a.nvals ? a.table[i] : 0.0;
     __syncthreads();
   }
-  int64_t b = blockIdx.x;
-  if (b >= a.nblocks) {
-    if constexpr (NA > 0)
-      grid_reduce<NA>(acc, a.ndots + a.nq, ws, a.out, red_sm, ws.long_dots, a.nlong);
-    return;
-  }
-  SpmvBlock blk = a.blocks[b];
-  Staged<PACKED> cur;
-  stage<PACKED, T>(a, blk, tid, cur);
-
-  while (b < a.nblocks) {
-    const int64_t bn = b + gridDim.x;
-    SpmvBlock nblk;
-    if (bn < a.nblocks) nblk = a.blocks[bn];
-    const int cnt = (int)(blk.nz1 - blk.nz0);
-    if (blk.lshift >= 0) {
-      // ---- normal block: products into shared memory
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        const int e = tid + j * kST;
-        if (e < cnt) sm[e] = product<PACKED>(a, cur, j, tab_sm, cmask);
-      }
-      // row bounds of this thread's first row (independent of the products)
-      int lo0 = 0, hi0 = 0;
-      if (tid < blk.nrows) {
-        lo0 = (int)(a.row_ptr[blk.row0 + tid] - blk.nz0);
-        hi0 = (int)(a.row_ptr[blk.row0 + tid + 1] - blk.nz0);
-      }
-      Staged<PACKED> nxt;
-      if (bn < a.nblocks) stage<PACKED, T>(a, nblk, tid, nxt);
-      __syncthreads();
-      // phase A: one thread per row for rows of at most kShortRow entries;
-      // longer rows are compacted (in row order, via ballots) into a list
-      int nlist = 0;
-      for (int base = 0; base < blk.nrows; base += kST) {
-        const int rr = base + tid;
-        bool is_long = false;
-        if (rr < blk.nrows) {
-          const int64_t r = blk.row0 + rr;
-          int lo = lo0, hi = hi0;
-          if (base) {
-            lo = (int)(a.row_ptr[r] - blk.nz0);
-            hi = (int)(a.row_ptr[r + 1] - blk.nz0);
-          }
-          if (hi - lo <= kShortRow) {
-            double sacc = 0.0;
-            for (int e = lo; e < hi; ++e) sacc += sm[e];
-            const double yr = finish_row<PACKED>(a, r, sacc, theta);
-            a.y[r] = yr;
-            epilogue_row<NA>(a, r, yr, acc);
+  double theta = a.theta_h;
+  if (a.theta_d) theta += a.theta_neg ? -*a.theta_d : *a.theta_d;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cmask = PACKED ? ((a.cbits >= 32) ? 0xffffffffu : ((1u << a.cbits) - 1u)) : 0u;
+  const int64_t nw = (int64_t)gridDim.x * (kWThreads / 32);
+  int64_t b = (int64_t)blockIdx.x * (kWThreads / 32) + (threadIdx.x >> 5);
+  __shared__ double rsum[kWThreads / 32][kWRows];   // per warp: row sums of a block
+  double* slot = rsum[threadIdx.x >> 5];
+  if (b >= a.nblocks) return;
+  // pipeline prologue: current descriptor + words, next descriptor word
+  WDesc d = desc_decode(desc_word(a, b, lane), lane);
+  unsigned vm = valid_mask(d, lane);
+  WWords<PACKED> W;
+  if (vm) wload<PACKED>(a, (d.nz0 & ~(int64_t)3) + kWPer * lane, W);
+  uint32_t wnext = desc_word(a, b + nw, lane);
+  while (true) {
+    // gathers of the current block
+    double p[kWPer];
+    wproducts<PACKED>(a, W, vm, tab_sm, cmask, p);
+    // next block: decode, issue its stream words; load the descriptor after
+    // (LG_SPMV_PIPE=0 builds issue them after this block instead)
+    const int64_t bn = b + nw;
+    WDesc dn;
+    unsigned vmn = 0u;
+    WWords<PACKED> Wn;
+    auto next_loads = [&]() {
+      dn = desc_decode(wnext, lane);
+      vmn = bn < a.nblocks ? valid_mask(dn, lane) : 0u;
+      if (vmn) wload<PACKED>(a, (dn.nz0 & ~(int64_t)3) + kWPer * lane, Wn);
+      wnext = desc_word(a, bn + nw, lane);
+    };
+    if constexpr (LG_SPMV_PIPE) next_loads();
+    const int64_t row0 = d.row0;
+    if (d.kind == kBlkRows) {
+      // rows with no stored entry (or other irregular blocks): lane per row
+      for (int i = lane; i < d.nrows; i += 32) {
+        const int64_t r = row0 + i;
+        double s = 0.0;
+        for (int64_t k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) {
+          if constexpr (PACKED) {
+            const uint32_t w = a.pcol[k];
+            s += tab_sm[w >> a.cbits] * __ldg(a.x + (w & cmask));
           } else {
-            is_long = true;
+            s += a.val[k] * __ldg(a.x + a.col[k]);
           }
         }
-        const unsigned ball = __ballot_sync(0xffffffffu, is_long);
-        const int lane = tid & 31, warp = tid >> 5;
-        if (lane == 0) wcnt_sm[warp] = __popc(ball);
-        __syncthreads();
-        int off = nlist;
-        for (int w = 0; w < warp; ++w) off += wcnt_sm[w];
-        if (is_long) list_sm[off + __popc(ball & ((1u << lane) - 1u))] = rr;
-        for (int w = 0; w < kSW; ++w) nlist += wcnt_sm[w];
-        __syncthreads();
+        finish_row<PACKED>(a, r, s, theta);
       }
-      // phase B: one warp per long row (lane-strided, then butterfly)
-      {
-        const int lane = tid & 31, warp = tid >> 5;
-        for (int i = warp; i < nlist; i += kSW) {
-          const int rr = list_sm[i];
-          const int64_t r = blk.row0 + rr;
-          const int lo = (int)(a.row_ptr[r] - blk.nz0);
-          const int hi = (int)(a.row_ptr[r + 1] - blk.nz0);
-          double sacc = 0.0;
-          for (int e = lo + lane; e < hi; e += 32) sacc += sm[e];
-          sacc = warp_sum(sacc);
-          if (lane == 0) {
-            const double yr = finish_row<PACKED>(a, r, sacc, theta);
-            a.y[r] = yr;
-            epilogue_row<NA>(a, r, yr, acc);
-          }
-        }
-      }
-      __syncthreads();  // sm reused by the next block
-      cur = nxt;
-    } else {
-      // ---- part of a long row: register partial, ticket, ordered finish
+    } else if (d.kind == kBlkLong) {
+      // part of a long row: lane sums left to right, butterfly, ordered finish
       double s = 0.0;
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        const int e = tid + j * kST;
-        if (e < cnt) s += product<PACKED>(a, cur, j, tab_sm, cmask);
-      }
-      Staged<PACKED> nxt;
-      if (bn < a.nblocks) stage<PACKED, T>(a, nblk, tid, nxt);
+      for (int j = 0; j < kWPer; ++j) s += p[j];
       s = warp_sum(s);
-      if ((tid & 31) == 0) sm[tid >> 5] = s;
-      __syncthreads();
-      if (tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < kSW; ++w) t += sm[w];
-        a.long_part[blk.part] = t;
-        __threadfence();
-        const int lr = blk.nrows;
-        unsigned arrived = atomicAdd(a.long_ticket + lr, 1u);
-        fin_flag = (arrived == (unsigned)a.long_nparts[lr] - 1u);
+      unsigned last = 0u;
+      const int lr = d.nrows;
+      if (lane == 0) {
+        LG_CK(d.part >= 0 && d.part < a.nparts && lr >= 0 && lr < a.nlong, "long part");
+        a.long_part[d.part] = s;
+        // release: the partial is visible before the ticket moves
+        unsigned arrived;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;"
+                     : "=r"(arrived) : "l"(a.long_ticket + lr) : "memory");
+        last = arrived == (unsigned)a.long_nparts[lr] - 1u;
       }
-      __syncthreads();
-      if (fin_flag && tid < 32) {
-        // the finishing CTA's first warp sums the parts lane-strided and
-        // then by butterfly: fixed order, independent of arrival order
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        // the last part to arrive sums every part lane-strided, then by
+        // butterfly: fixed order whatever the arrival order
         __threadfence();
-        const int lr = blk.nrows;
         const int64_t first = a.long_first[lr];
         const int np = a.long_nparts[lr];
         double t = 0.0;
-        for (int p0 = tid; p0 < np; p0 += 32 * 8) {
-          double v[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            v[j] = p0 + 32 * j < np ? ld_cg(a.long_part + first + p0 + 32 * j) : 0.0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (p0 + 32 * j < np) t += v[j];
-        }
+        for (int q = lane; q < np; q += 32) t += ld_cg(a.long_part + first + q);
         t = warp_sum(t);
-        if (tid == 0) {
-          const int64_t r = blk.row0;
-          const double yr = finish_row<PACKED>(a, r, t, theta);
-          a.y[r] = yr;
+        if (lane == 0) {
+          finish_row<PACKED>(a, row0, t, theta);
           a.long_ticket[lr] = 0u;
-          if constexpr (NA > 0) {
-            // long-row epilogue goes to its own slot: order stays fixed no
-            // matter which CTA finishes the row
-            double la[NA];
-#pragma unroll
-            for (int d = 0; d < NA; ++d) la[d] = 0.0;
-            epilogue_row<NA>(a, r, yr, la);
-            for (int d = 0; d < a.ndots + a.nq; ++d)
-              ws.long_dots[(int64_t)lr * kMaxRedVals + d] = la[d];
-          }
         }
       }
-      __syncthreads();
-      cur = nxt;
+    } else {
+      // ---- segmented block: each completed row's sum goes to the warp's slot
+      // array (by row offset); one coalesced pass then finishes the rows
+      // (diagonal, shift, accumulation, store).  Branch-free: running sums
+      // c_j restart at every row start (flag F_j), the warp joins the lanes'
+      // open tails with a segmented scan, and a row ends at position j when
+      // j is valid and position j + 1 starts a row or ends the block.
+      const unsigned F = d.meta & vm & 0xffu;
+      double c[kWPer];
+      double run = 0.0;
+#pragma unroll
+      for (int j = 0; j < kWPer; ++j) {
+        run = (((F >> j) & 1u) ? 0.0 : run) + p[j];
+        c[j] = run;
+      }
+      // segmented inclusive scan of the lanes' open tails
+      double v = run;
+      bool f = F != 0u;
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const double vu = __shfl_up_sync(0xffffffffu, v, dd);
+        const bool fu = __shfl_up_sync(0xffffffffu, (int)f, dd) != 0;
+        if (lane >= dd && !f) {
+          v = vu + v;
+          f = fu;
+        }
+      }
+      double cprev = __shfl_up_sync(0xffffffffu, v, 1);
+      if (lane == 0) cprev = 0.0;
+      // row ends: the next position (next lane's first for j = 7) starts a
+      // row, or j is the block's last position
+      const unsigned nf = __shfl_down_sync(0xffffffffu, F & 1u, 1);
+      const int last = (int)(d.nz1 - 1 - (d.nz0 & ~(int64_t)3)) - kWPer * lane;
+      unsigned E = vm & ((F >> 1) | ((lane < 31 ? nf : 0u) << (kWPer - 1)));
+      if (last >= 0 && last < kWPer) E |= 1u << last;
+      // positions before the lane's first row start continue a row from the
+      // lanes before: add their carry
+      const unsigned before = F ? ((F & (0u - F)) - 1u) : 0xffu;
+      const int rfirst = (int)(d.meta >> 8);
+      const int fv = __ffs(vm) - 1;
+      // row of position j: rfirst + (row starts in (fv, j])
+      const unsigned fcount = F & ~(1u << fv);
+#pragma unroll
+      for (int j = 0; j < kWPer; ++j) {
+        if ((E >> j) & 1u) {
+          const int r = rfirst + __popc(fcount & ((2u << j) - 1u));
+          LG_CK(r >= 0 && r < d.nrows, "slot");
+          slot[r] = ((before >> j) & 1u) ? cprev + c[j] : c[j];
+        }
+      }
+      __syncwarp();
+      for (int i = lane; i < d.nrows; i += 32) finish_row<PACKED>(a, row0 + i, slot[i], theta);
+      __syncwarp();
     }
-    blk = nblk;
+    if (bn >= a.nblocks) break;
+    if constexpr (!LG_SPMV_PIPE) next_loads();
     b = bn;
-  }
-  if constexpr (NA > 0) {
-    grid_reduce<NA>(acc, a.ndots + a.nq, ws, a.out, red_sm, ws.long_dots, a.nlong);
+    d = dn;
+    vm = vmn;
+    W = Wn;
   }
 }
 
-// Build the row-block schedule on the host (O(n)).
-// absent (optional): rows with no stored entry that are left out of the
-// schedule altogether (y is not written there) -- the row block of one rank
-// in the row-partitioned multi-GPU SpMV, embedded in the global index space.
-static void build_schedule(int64_t n, const int64_t* rp, int cta,
-                           std::vector<SpmvBlock>& blocks,
+// Build the warp-block schedule on the host.
+// absent (optional): rows left out of the schedule altogether (y is not
+// written there) -- the row block of one rank in the row-partitioned
+// multi-GPU SpMV, embedded in the global index space.
+static void build_schedule(int64_t n, const int64_t* rp, std::vector<SpmvBlock>& blocks,
                            std::vector<int32_t>& long_nparts,
                            std::vector<int64_t>& long_first,
                            const std::vector<char>* absent = nullptr) {
-  const int kChunk = cta * kPer;
-  const int kST = cta;
   int64_t r = 0, part_total = 0;
+  blocks.reserve((size_t)(rp[n] / (kWin - 16) + n / kWRows + 16));
   while (r < n) {
     if (absent && (*absent)[(size_t)r]) {
       ++r;
       continue;
     }
-    int64_t len = rp[r + 1] - rp[r];
-    if (len > kChunk) {
-      int32_t np = (int32_t)((len + kChunk - 1) / kChunk);
-      int32_t lr = (int32_t)long_nparts.size();
+    const int64_t len = rp[r + 1] - rp[r];
+    if (len > kLongPart) {
+      const int32_t np = (int32_t)((len + kLongPart - 1) / kLongPart);
+      const int32_t lr = (int32_t)long_nparts.size();
       long_nparts.push_back(np);
       const int64_t slot0 = part_total;
       part_total += np;
       long_first.push_back(slot0);
-      for (int32_t p = 0; p < np; ++p) {
-        SpmvBlock b;
-        b.nz0 = rp[r] + (int64_t)p * kChunk;
-        b.nz1 = std::min(rp[r] + (int64_t)(p + 1) * kChunk, rp[r + 1]);
+      for (int32_t q = 0; q < np; ++q) {
+        SpmvBlock b{};
+        b.nz0 = rp[r] + (int64_t)q * kLongPart;
+        b.nz1 = std::min(rp[r] + (int64_t)(q + 1) * kLongPart, rp[r + 1]);
         b.row0 = (int32_t)r;
         b.nrows = lr;
-        b.lshift = -1;
-        b.part = (int32_t)(slot0 + p);
+        b.lshift = kBlkLong;
+        b.part = (int32_t)(slot0 + q);
         blocks.push_back(b);
       }
       ++r;
       continue;
     }
-    int64_t r0 = r, nz = 0;
-    while (r < n && r - r0 < kRowCap) {
+    const int64_t r0 = r, nz0 = rp[r];
+    const int64_t cap = kWin - (nz0 & 3);
+    bool empty = false;
+    while (r < n && r - r0 < kWRows) {
       if (absent && (*absent)[(size_t)r]) break;
-      int64_t l = rp[r + 1] - rp[r];
-      if (l > kChunk || nz + l > kChunk) break;
-      nz += l;
+      const int64_t l = rp[r + 1] - rp[r];
+      if (l > kLongPart || rp[r + 1] - nz0 > cap) break;
+      empty |= (l == 0);
       ++r;
     }
-    SpmvBlock b;
-    b.nz0 = rp[r0];
+    SpmvBlock b{};
+    b.nz0 = nz0;
     b.nz1 = rp[r];
     b.row0 = (int32_t)r0;
     b.nrows = (int32_t)(r - r0);
-    // lanes per row: one pass over the block's rows with every thread busy
-    // when rows are few (long), one thread per row when they are many --
-    // never more lanes than the mean row length
-    const int64_t nr = r - r0;
-    const double avg = (double)nz / (double)nr;
-    int sh = 0;
-    while (sh < 5 && (nr << (sh + 1)) <= kST && (double)(2 << sh) <= 2.0 * avg) ++sh;
-    b.lshift = sh;
-    b.part = 0;
+    b.lshift = empty ? kBlkRows : kBlkSeg;
+    if (!empty) {
+      const int64_t base = nz0 & ~(int64_t)3;
+      for (int64_t i = 0; i < r - r0; ++i) {
+        const int64_t s = rp[r0 + i] - base;
+        b.meta[s >> 3] |= (uint16_t)(1u << (s & 7));
+      }
+      // row of each lane's first valid position
+      int64_t row = 0;
+      for (int l = 0; l < 32; ++l) {
+        const int64_t fv = std::max<int64_t>(base + kWPer * l, nz0);
+        if (fv >= b.nz1) break;
+        while (rp[r0 + row + 1] <= fv) ++row;
+        b.meta[l] |= (uint16_t)(row << 8);
+      }
+    }
     blocks.push_back(b);
   }
 }
@@ -454,8 +528,8 @@ static void set_chunks(lg_csr* a, const std::vector<SpmvBlock>& blocks) {
   int c = 0;
   for (int k = 1; k < kHostChunks; ++k) {
     int64_t b = k * nb / kHostChunks;
-    while (b < nb && blocks[(size_t)b].lshift < 0 && b > 0 &&
-           blocks[(size_t)b - 1].lshift < 0 &&
+    while (b < nb && blocks[(size_t)b].lshift == kBlkLong && b > 0 &&
+           blocks[(size_t)b - 1].lshift == kBlkLong &&
            blocks[(size_t)b - 1].nrows == blocks[(size_t)b].nrows)
       ++b;   // inside one long row's parts
     if (b <= prev || b >= nb) continue;
@@ -468,6 +542,74 @@ static void set_chunks(lg_csr* a, const std::vector<SpmvBlock>& blocks) {
   a->nchunks = c + 1;
 }
 
+// Build the schedule of `a` from host row pointers and upload it (blocks,
+// long-row part tables); sets nblocks / nlong / nparts / chunks.
+static int attach_schedule(lg_csr* a, const int64_t* rp, const std::vector<char>* absent,
+                           const char* who) {
+  std::vector<SpmvBlock> blocks;
+  std::vector<int32_t> lnp;
+  std::vector<int64_t> lfirst;
+  // Present rows in many separate runs (a column panel leaves every row
+  // without an entry in its columns absent): schedule the present rows as one
+  // compacted sequence and map each back through rowmap, so blocks are not
+  // cut at every gap.  A few runs (a rank's row block) keep the plain form.
+  std::vector<int32_t> map;
+  std::vector<int64_t> crp;
+  if (absent) {
+    int64_t runs = 0;
+    for (int64_t r = 0; r < a->n; ++r)
+      runs += !(*absent)[(size_t)r] && (r == 0 || (*absent)[(size_t)r - 1]);
+    if (runs > 64) {
+      // absent rows hold no entries, so the present rows' entries stay one
+      // contiguous stream: compacted row i starts where matrix row map[i] does
+      for (int64_t r = 0; r < a->n; ++r) {
+        if ((*absent)[(size_t)r]) continue;
+        if (rp[r + 1] == rp[r] || (!map.empty() && rp[map.back() + 1] != rp[r])) {
+          map.clear();   // an empty present row, or entries between present rows:
+                         // keep the plain form
+          crp.clear();
+          break;
+        }
+        map.push_back((int32_t)r);
+        crp.push_back(rp[r]);
+      }
+      if (!map.empty()) crp.push_back(rp[map.back() + 1]);
+    }
+  }
+  if (!map.empty()) {
+    const int64_t nc = (int64_t)map.size();
+    build_schedule(nc, crp.data(), blocks, lnp, lfirst, nullptr);
+    if (cudaMalloc(&a->rowmap, 4 * (size_t)nc) != cudaSuccess)
+      return fail(LG_ENOMEM, std::string(who) + ": row map alloc");
+    LG_CUDA(cudaMemcpy(a->rowmap, map.data(), 4 * (size_t)nc, cudaMemcpyHostToDevice));
+  } else {
+    build_schedule(a->n, rp, blocks, lnp, lfirst, absent);
+  }
+  a->nblocks = (int64_t)blocks.size();
+  set_chunks(a, blocks);
+  if (a->rowmap && a->nchunks > 1) {   // chunk rows are compacted indices: one chunk
+    a->nchunks = 1;
+    a->chunk_b[1] = a->nblocks;
+    a->chunk_row[1] = a->n;
+  }
+  a->nlong = (int64_t)lnp.size();
+  a->nparts = 0;
+  for (int32_t v : lnp) a->nparts += v;
+  if ((a->nblocks &&
+       cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess) ||
+      (a->nlong && (cudaMalloc(&a->long_nparts, 4 * (size_t)a->nlong) != cudaSuccess ||
+                    cudaMalloc(&a->long_first, 8 * (size_t)a->nlong) != cudaSuccess)))
+    return fail(LG_ENOMEM, std::string(who) + ": schedule alloc");
+  if (a->nblocks)
+    LG_CUDA(cudaMemcpy(a->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(),
+                       cudaMemcpyHostToDevice));
+  if (a->nlong) {
+    LG_CUDA(cudaMemcpy(a->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice));
+    LG_CUDA(cudaMemcpy(a->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice));
+  }
+  return LG_OK;
+}
+
 static int ensure_long_ws(lg_ws* ws, const lg_csr* a) {
   if (a->nlong > ws->long_cap) {
     cudaFree(ws->long_dots);
@@ -475,8 +617,6 @@ static int ensure_long_ws(lg_ws* ws, const lg_csr* a) {
     ws->long_dots = nullptr;
     ws->long_ticket = nullptr;
     ws->long_cap = 0;
-    LG_CUDA(cudaMalloc(&ws->long_dots,
-                       sizeof(double) * (size_t)a->nlong * kMaxRedVals));
     LG_CUDA(cudaMalloc(&ws->long_ticket, sizeof(unsigned) * (size_t)a->nlong));
     LG_CUDA(cudaMemset(ws->long_ticket, 0, sizeof(unsigned) * (size_t)a->nlong));
     LG_CUDA(cudaDeviceSynchronize());
@@ -492,77 +632,95 @@ static int ensure_long_ws(lg_ws* ws, const lg_csr* a) {
   return LG_OK;
 }
 
-template <int NA, bool PACKED, int T>
-static int grid_for(size_t dyn) {
-  static thread_local size_t last_dyn = (size_t)-1;
-  static thread_local int occ = 1;
-  if (dyn != last_dyn) {
+// Kernel arguments of a product with `m` (no theta, no accumulation).
+static SpmvArgs spmv_args(const lg_csr* m, const double* x, double* y, lg_ws* ws) {
+  SpmvArgs args{};
+  args.n = m->n;
+  args.row_ptr = m->packed ? m->prp : m->row_ptr;
+  args.col = m->col;
+  args.val = m->val;
+  args.pcol = m->packed ? m->pcol : nullptr;
+  args.pdiag = m->pdiag;
+  args.table = m->table;
+  args.nvals = m->nvals;
+  args.cbits = m->cbits;
+  args.nzs = m->packed ? m->noff : m->nnz;
+  args.blocks = m->blocks;
+  args.nblocks = m->nblocks;
+  args.long_nparts = m->long_nparts;
+  args.long_first = m->long_first;
+  args.x = x;
+  args.y = y;
+  args.long_part = ws ? ws->long_part : nullptr;
+  args.long_ticket = ws ? ws->long_ticket : nullptr;
+  args.rowmap = m->rowmap;
+  args.nparts = m->nparts;
+  args.nlong = m->nlong;
+  // x (and the diagonal) into L2 up front when both fit in a third of it;
+  // a column panel prefetches its slice of x (why panels exist: C5)
+  static const bool pf_on = [] {
+    const char* e = getenv("LG_SPMV_PREFETCH");
+    return !(e && atoi(e) == 0);
+  }();
+  const int64_t l2 = dev_info().l2_bytes > 0 ? dev_info().l2_bytes : (int64_t)126 << 20;
+  if (pf_on && x && ((uintptr_t)x & 15) == 0) {
+    const int64_t c0 = m->pf_c0 & ~(int64_t)1, c1 = m->pf_c1 > 0 ? m->pf_c1 : m->n;
+    const int64_t xb = 8 * (c1 - c0);
+    const int64_t db = (m->packed && m->pdiag) ? 8 * m->n : 0;
+    if (xb + db <= l2 / 3) {
+      args.pf[0] = x + c0;
+      args.pf_bytes[0] = xb;
+      if (db && ((uintptr_t)m->pdiag & 15) == 0) {
+        args.pf[1] = m->pdiag;
+        args.pf_bytes[1] = db;
+      }
+    } else if (xb <= l2 / 3) {
+      args.pf[0] = x + c0;
+      args.pf_bytes[0] = xb;
+    }
+  }
+  return args;
+}
+
+template <bool PACKED>
+static int launch_t(const SpmvArgs& args, cudaStream_t s) {
+  static thread_local int occ = 0;
+  if (!occ) {
     int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, spmv_kernel<NA, PACKED, T>,
-                                                      T, dyn) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, wspmv_kernel<PACKED>, kWThreads,
+                                                      sizeof(double) * kMaxTable) !=
+            cudaSuccess ||
         o < 1)
       o = 1;
     occ = o;
-    last_dyn = dyn;
   }
-  return occ * dev_info().sm_count;
-}
-
-template <int NA, bool PACKED, int T>
-static int launch_t(const SpmvArgs& args, lg_ws* ws, cudaStream_t s) {
-  const size_t dyn = PACKED ? sizeof(double) * (size_t)args.nvals : 0;
-  int64_t g = std::min<int64_t>(args.nblocks, grid_for<NA, PACKED, T>(dyn));
-  if (NA > 0) g = std::min<int64_t>(g, kMaxRedBlocks);
-  if (g < 1) g = 1;
-  spmv_kernel<NA, PACKED, T><<<(unsigned)g, T, dyn, s>>>(args, *ws);
-  LG_LAUNCH_CHECK("spmv_kernel");
+  const int64_t warps = (int64_t)occ * dev_info().sm_count * (kWThreads / 32);
+  const int64_t g = std::max<int64_t>(
+      1, std::min<int64_t>((args.nblocks + kWThreads / 32 - 1) / (kWThreads / 32),
+                           warps / (kWThreads / 32)));
+  const size_t dyn = PACKED ? sizeof(double) * (size_t)std::max(args.nvals, 1) : 0;
+  wspmv_kernel<PACKED><<<(unsigned)g, kWThreads, dyn, s>>>(args);
+  LG_LAUNCH_CHECK("wspmv_kernel");
   return LG_OK;
 }
 
-// NA > 0 (fused epilogue, LG_SPMV_EPILOGUE=1) is instantiated for 128-thread
-// schedules only; lg_spmv routes 256-thread matrices through the separate
-// epilogue pass.
-template <int NA>
-static int launch(const SpmvArgs& args, lg_ws* ws, cudaStream_t s, bool packed, int cta) {
-  if constexpr (NA == 0) {
-    if (cta == 256)
-      return packed ? launch_t<0, true, 256>(args, ws, s) : launch_t<0, false, 256>(args, ws, s);
-  }
-  return packed ? launch_t<NA, true, 128>(args, ws, s) : launch_t<NA, false, 128>(args, ws, s);
-}
-
-// CTA size of a matrix's schedule (LG_SPMV_CTA overrides: 128 or 256).
-static int pick_cta(int64_t noff) {
-  const char* e = getenv("LG_SPMV_CTA");
-  if (e && (atoi(e) == 128 || atoi(e) == 256)) return atoi(e);
-  return noff >= ((int64_t)1 << 27) ? 256 : 128;
+static int launch(const SpmvArgs& args, cudaStream_t s, bool packed) {
+  if (args.nblocks == 0) return LG_OK;
+  if ((packed && ((uintptr_t)args.pcol & 15)) ||
+      (!packed && (((uintptr_t)args.col & 15) || ((uintptr_t)args.val & 15))))
+    return fail(LG_EINVAL, "lg_spmv: stream arrays must be 16-byte aligned");
+  return packed ? launch_t<true>(args, s) : launch_t<false>(args, s);
 }
 
 // y = A x over the schedule blocks [b0, b1) only (a row chunk; no epilogue).
 static int spmv_range(const lg_csr* a, const double* x, double* y, int64_t b0, int64_t b1,
                       lg_ws* ws, cudaStream_t s, int accum = 0) {
   if (b1 <= b0) return LG_OK;
-  SpmvArgs args{};
+  SpmvArgs args = spmv_args(a, x, y, ws);
   args.accum = accum;
-  args.n = a->n;
-  args.row_ptr = a->packed ? a->prp : a->row_ptr;
-  args.col = a->col;
-  args.val = a->val;
-  args.pcol = a->packed ? a->pcol : nullptr;
-  args.pdiag = a->pdiag;
-  args.table = a->table;
-  args.nvals = a->nvals;
-  args.cbits = a->cbits;
   args.blocks = a->blocks + b0;
   args.nblocks = b1 - b0;
-  args.long_nparts = a->long_nparts;
-  args.long_first = a->long_first;
-  args.x = x;
-  args.y = y;
-  args.long_part = ws->long_part;
-  args.long_ticket = ws->long_ticket;
-  args.nlong = a->nlong;
-  return launch<0>(args, ws, s, a->packed != 0, a->cta);
+  return launch(args, s, a->packed != 0);
 }
 
 // Packed Laplacian format eligibility: every row stores its diagonal, the
@@ -666,47 +824,32 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
   std::vector<double> pdiag, table;
   int cbits = 0;
   const bool packed = !(flags & 1) && make_packed(n, rp, col, val, prp, pcol, pdiag, table, cbits);
-  std::vector<SpmvBlock> blocks;
-  std::vector<int32_t> lnp;
-  std::vector<int64_t> lfirst;
   std::vector<char> absent;
   if (flags & LG_CSR_SKIP_EMPTY) {
     absent.resize((size_t)n);
     for (int64_t r = 0; r < n; ++r) absent[(size_t)r] = rp[r + 1] == rp[r];
   }
-  const int cta = pick_cta(packed ? (int64_t)pcol.size() : nnz);
-  build_schedule(n, packed ? prp.data() : rp, cta, blocks, lnp, lfirst,
-                 (flags & LG_CSR_SKIP_EMPTY) ? &absent : nullptr);
-
   lg_csr* a = new lg_csr();
   a->n = n;
   a->nnz = nnz;
-  a->cta = cta;
-  a->nblocks = (int64_t)blocks.size();
-  set_chunks(a, blocks);
-  a->nlong = (int64_t)lnp.size();
   a->packed = packed ? 1 : 0;
   a->cbits = cbits;
   a->nvals = (int)table.size();
   a->noff = packed ? (int64_t)pcol.size() : 0;
   a->is_block = (flags & LG_CSR_SKIP_EMPTY) ? 1 : 0;
-  for (int32_t v : lnp) a->nparts += v;
   auto cleanup = [&](const char* what) {
     lg_csr_destroy(a);
     return fail(LG_ENOMEM, std::string("lg_csr_create: ") + what);
   };
   if (cudaMalloc(&a->row_ptr, sizeof(int64_t) * (size_t)(n + 1)) != cudaSuccess)
     return cleanup("row_ptr alloc");
-  if (nnz && cudaMalloc(&a->col, sizeof(int32_t) * (size_t)nnz) != cudaSuccess)
+  if (nnz && cudaMalloc(&a->col, sizeof(int32_t) * (size_t)(nnz + kStreamPad)) != cudaSuccess)
     return cleanup("col alloc");
-  if (nnz && cudaMalloc(&a->val, sizeof(double) * (size_t)nnz) != cudaSuccess)
+  if (nnz && cudaMalloc(&a->val, sizeof(double) * (size_t)(nnz + kStreamPad)) != cudaSuccess)
     return cleanup("val alloc");
-  if (a->nblocks &&
-      cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess)
-    return cleanup("schedule alloc");
   if (packed) {
     if (cudaMalloc(&a->prp, sizeof(int64_t) * (size_t)(n + 1)) != cudaSuccess ||
-        (a->noff && cudaMalloc(&a->pcol, sizeof(uint32_t) * (size_t)a->noff) != cudaSuccess) ||
+        (a->noff && cudaMalloc(&a->pcol, sizeof(uint32_t) * (size_t)(a->noff + kStreamPad)) != cudaSuccess) ||
         cudaMalloc(&a->pdiag, sizeof(double) * (size_t)n) != cudaSuccess ||
         (a->nvals && cudaMalloc(&a->table, sizeof(double) * (size_t)a->nvals) != cudaSuccess))
       return cleanup("packed alloc");
@@ -719,24 +862,19 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
       cudaMemcpy(a->table, table.data(), sizeof(double) * (size_t)a->nvals,
                  cudaMemcpyHostToDevice);
   }
-  if (a->nlong) {
-    if (cudaMalloc(&a->long_nparts, sizeof(int32_t) * (size_t)a->nlong) != cudaSuccess ||
-        cudaMalloc(&a->long_first, sizeof(int64_t) * (size_t)a->nlong) != cudaSuccess)
-      return cleanup("long-row alloc");
-  }
   cudaMemcpy(a->row_ptr, rp, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice);
   if (nnz) {
     cudaMemcpy(a->col, c32.data(), sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice);
     cudaMemcpy(a->val, val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice);
   }
-  if (a->nblocks)
-    cudaMemcpy(a->blocks, blocks.data(), sizeof(SpmvBlock) * (size_t)a->nblocks,
-               cudaMemcpyHostToDevice);
-  if (a->nlong) {
-    cudaMemcpy(a->long_nparts, lnp.data(), sizeof(int32_t) * (size_t)a->nlong,
-               cudaMemcpyHostToDevice);
-    cudaMemcpy(a->long_first, lfirst.data(), sizeof(int64_t) * (size_t)a->nlong,
-               cudaMemcpyHostToDevice);
+  {
+    const int rc = attach_schedule(a, packed ? prp.data() : rp,
+                                   (flags & LG_CSR_SKIP_EMPTY) ? &absent : nullptr,
+                                   "lg_csr_create");
+    if (rc) {
+      lg_csr_destroy(a);
+      return rc;
+    }
   }
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -760,6 +898,7 @@ int lg_csr_destroy(lg_csr* a) {
   cudaFree(a->pcol);
   cudaFree(a->pdiag);
   cudaFree(a->table);
+  cudaFree(a->rowmap);
   delete a;
   return LG_OK;
 }
@@ -772,12 +911,14 @@ int lg_csr_info(const lg_csr* a, int64_t* n, int64_t* nnz, int64_t* nblocks,
   if (nblocks) *nblocks = a->nblocks;
   if (nlong) *nlong = a->nlong;
   if (packed) *packed = a->packed;
-  // bytes one SpMV streams: plain = f64 values + int32 columns + int64 row
-  // pointers + x read + y written; packed = 32-bit words per off-diagonal +
-  // int64 row pointers + diagonal + x + y
-  if (stream_bytes)
-    *stream_bytes = a->packed ? 4 * a->noff + 8 * (a->n + 1) + 8 * a->n + 16 * a->n
-                              : 12 * a->nnz + 8 * (a->n + 1) + 16 * a->n;
+  // bytes one SpMV streams: plain = f64 values + int32 columns + schedule
+  // descriptors (row structure) + x read + y written; packed = 32-bit words
+  // per off-diagonal + descriptors + diagonal + x + y
+  if (stream_bytes) {
+    const int64_t sched = (int64_t)sizeof(SpmvBlock) * a->nblocks;
+    *stream_bytes = a->packed ? 4 * a->noff + sched + 8 * a->n + 16 * a->n
+                              : 12 * a->nnz + sched + 16 * a->n;
+  }
   return LG_OK;
 }
 
@@ -822,78 +963,38 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
     int rc = ensure_long_ws(ws, a);
     if (rc) return rc;
   }
-  SpmvArgs args{};
-  args.n = a->n;
-  args.row_ptr = a->packed ? a->prp : a->row_ptr;
-  args.col = a->col;
-  args.val = a->val;
-  args.pcol = a->packed ? a->pcol : nullptr;
-  args.pdiag = a->pdiag;
-  args.table = a->table;
-  args.nvals = a->nvals;
-  args.cbits = a->cbits;
-  args.blocks = a->blocks;
-  args.nblocks = a->nblocks;
-  args.long_nparts = a->long_nparts;
-  args.long_first = a->long_first;
-  args.x = x;
-  args.y = y;
+  SpmvArgs args = spmv_args(a, x, y, ws);
   args.theta_h = theta_h;
   args.theta_d = theta_d;
   args.theta_neg = theta_neg;
-  args.ndots = ndots;
-  for (int d = 0; d < ndots; ++d) args.dvec[d] = dvec ? dvec[d] : nullptr;
-  args.q = q;
-  args.ldq = ldq;
-  args.nq = nq;
-  args.out = out;
   args.skip = skip;
-  args.long_part = ws->long_part;
-  args.long_ticket = ws->long_ticket;
-  args.nlong = a->nlong;
   cudaStream_t s = (cudaStream_t)stream;
-  int na = ndots + nq;
-  const bool pk = a->packed != 0;
   if (a->npanels > 1 && ws == &local)
     return fail(LG_EINVAL, "lg_spmv: panelled matrix; pass a workspace");
-  auto product = [&]() {
-    return a->npanels > 1
+  int rc = a->npanels > 1
                ? lg_spmv_panels_(a, x, y, theta_h, theta_d, theta_neg, skip, ws, stream)
-               : launch<0>(args, ws, s, pk, a->cta);
-  };
-  if (na == 0) return product();
-  static const bool fused_epilogue = [] {
-    const char* e = getenv("LG_SPMV_EPILOGUE");
-    return e && atoi(e) == 1;
-  }();
-  if (!fused_epilogue || a->cta != 128 || a->npanels > 1) {
-    // The gather loop is latency-bound and wants every register for
-    // occupancy: the dot / Q^T y epilogue costs less as one streaming pass
-    // over y right behind the SpMV (measured on C4: +4-9 us instead of
-    // +18-60 us inside the kernel).  Same result layout: dots, then Q^T y.
-    int rc = product();
-    if (rc) return rc;
-    lg_fused_args f{};
-    f.n = a->n;
-    f.ndots = ndots;
-    for (int d = 0; d < ndots; ++d) {
-      f.da[d] = y;
-      f.db[d] = (dvec && dvec[d]) ? dvec[d] : nullptr;
-    }
-    if (nq) {
-      f.nblocks = 1;
-      f.b[0].q = q;
-      f.b[0].ld = ldq;
-      f.b[0].k = nq;
-      f.b[0].v = y;
-    }
-    f.result = out;
-    f.skip = skip;
-    return lg_fused(&f, ws, stream);
+               : launch(args, s, a->packed != 0);
+  if (rc || ndots + nq == 0) return rc;
+  // The dots / Q^T y epilogue runs as one streaming pass over y right behind
+  // the product (the gather loop wants every register for occupancy).
+  // Result layout: dots, then Q^T y.
+  lg_fused_args f{};
+  f.n = a->n;
+  f.ndots = ndots;
+  for (int d = 0; d < ndots; ++d) {
+    f.da[d] = y;
+    f.db[d] = (dvec && dvec[d]) ? dvec[d] : nullptr;
   }
-  if (na <= 4) return launch<4>(args, ws, s, pk, 128);
-  if (na <= 16) return launch<16>(args, ws, s, pk, 128);
-  return launch<LG_MAXD + LG_MAXQ>(args, ws, s, pk, 128);
+  if (nq) {
+    f.nblocks = 1;
+    f.b[0].q = q;
+    f.b[0].ld = ldq;
+    f.b[0].k = nq;
+    f.b[0].v = y;
+  }
+  f.result = out;
+  f.skip = skip;
+  return lg_fused(&f, ws, stream);
 }
 
 }  // extern "C"
@@ -1100,7 +1201,7 @@ __global__ void __launch_bounds__(kMmThreads) spmm_rm_kernel(
   constexpr int W = kMmThreads / 32;
   __shared__ double tab[kMaxTable];
   __shared__ double red[W][K];
-  extern __shared__ uint32_t scol[];   // one block's column words (cta * kPer)
+  extern __shared__ uint32_t scol[];   // one block's column words (kWin)
   __shared__ int fin;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / K, j = lane % K;
@@ -1231,11 +1332,11 @@ int lg_spmm_rowmajor(const lg_csr* a, const double* x, double* y, int k, lg_ws* 
     }
   }
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t smem = sizeof(uint32_t) * (size_t)a->cta * kPer;
+  const size_t smem = sizeof(uint32_t) * (size_t)kWin;
   static thread_local int occ = 0;
   if (!occ) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_rm_kernel<16>, kMmThreads,
-                                                      sizeof(uint32_t) * 256 * kPer) !=
+                                                      sizeof(uint32_t) * kWin) !=
             cudaSuccess || occ < 1)
       occ = 1;
   }
@@ -1346,7 +1447,7 @@ extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
             cudaMalloc(&a->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
             cudaMalloc(&a->pdiag, 8 * (size_t)n) == cudaSuccess &&
             cudaMalloc(&a->table, 8) == cudaSuccess &&
-            cudaMalloc(&a->pcol, 4 * (size_t)std::max<int64_t>(2 * m, 1)) == cudaSuccess &&
+            cudaMalloc(&a->pcol, 4 * (size_t)(2 * m + kStreamPad)) == cudaSuccess &&
             (m == 0 || (cudaMalloc(&sj, 4 * (size_t)m) == cudaSuccess &&
                         cudaMalloc(&si, 4 * (size_t)m) == cudaSuccess));
   if (!ok) {
@@ -1394,29 +1495,14 @@ extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
   }
   cleanup();
   // row-block schedule from the off-diagonal row pointers (host, O(n))
-  std::vector<int64_t> prp((size_t)n + 1);
-  cudaMemcpy(prp.data(), a->prp, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost);
-  std::vector<SpmvBlock> blocks;
-  std::vector<int32_t> lnp;
-  std::vector<int64_t> lfirst;
-  a->cta = pick_cta(a->noff);
-  build_schedule(n, prp.data(), a->cta, blocks, lnp, lfirst);
-  a->nblocks = (int64_t)blocks.size();
-  set_chunks(a, blocks);
-  a->nlong = (int64_t)lnp.size();
-  for (int32_t v : lnp) a->nparts += v;
-  if ((a->nblocks &&
-       cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess) ||
-      (a->nlong && (cudaMalloc(&a->long_nparts, 4 * (size_t)a->nlong) != cudaSuccess ||
-                    cudaMalloc(&a->long_first, 8 * (size_t)a->nlong) != cudaSuccess))) {
-    lg_csr_destroy(a);
-    return fail(LG_ENOMEM, "lg_csr_laplacian_device: schedule alloc");
-  }
-  if (a->nblocks)
-    cudaMemcpy(a->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
-  if (a->nlong) {
-    cudaMemcpy(a->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(a->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
+  {
+    std::vector<int64_t> prp((size_t)n + 1);
+    cudaMemcpy(prp.data(), a->prp, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost);
+    const int rc = attach_schedule(a, prp.data(), nullptr, "lg_csr_laplacian_device");
+    if (rc) {
+      lg_csr_destroy(a);
+      return rc;
+    }
   }
   // the plain arrays are not materialised (device-only matrix)
   *out = a;
@@ -1437,25 +1523,13 @@ static int plain_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** out
   for (int64_t r = r1 + 1; r <= n; ++r) rp[(size_t)r] = m;
   std::vector<char> absent((size_t)n, 1);
   for (int64_t r = r0; r < r1; ++r) absent[(size_t)r] = 0;
-  std::vector<SpmvBlock> blocks;
-  std::vector<int32_t> lnp;
-  std::vector<int64_t> lfirst;
-  build_schedule(n, rp.data(), a->cta, blocks, lnp, lfirst, &absent);
   lg_csr* b = new lg_csr();
-  b->cta = a->cta;
   b->n = n;
   b->nnz = m;
-  b->nblocks = (int64_t)blocks.size();
-  set_chunks(b, blocks);
-  b->nlong = (int64_t)lnp.size();
-  for (int32_t v : lnp) b->nparts += v;
+  b->is_block = 1;
   bool ok = cudaMalloc(&b->row_ptr, 8 * (size_t)(n + 1)) == cudaSuccess &&
-            cudaMalloc(&b->col, 4 * (size_t)std::max<int64_t>(m, 1)) == cudaSuccess &&
-            cudaMalloc(&b->val, 8 * (size_t)std::max<int64_t>(m, 1)) == cudaSuccess &&
-            (b->nblocks == 0 ||
-             cudaMalloc(&b->blocks, sizeof(SpmvBlock) * (size_t)b->nblocks) == cudaSuccess) &&
-            (b->nlong == 0 || (cudaMalloc(&b->long_nparts, 4 * (size_t)b->nlong) == cudaSuccess &&
-                               cudaMalloc(&b->long_first, 8 * (size_t)b->nlong) == cudaSuccess));
+            cudaMalloc(&b->col, 4 * (size_t)(m + kStreamPad)) == cudaSuccess &&
+            cudaMalloc(&b->val, 8 * (size_t)(m + kStreamPad)) == cudaSuccess;
   if (!ok) {
     lg_csr_destroy(b);
     return fail(LG_ENOMEM, "lg_csr_row_block: allocation failed");
@@ -1465,16 +1539,11 @@ static int plain_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** out
     cudaMemcpy(b->col, a->col + off0, 4 * (size_t)m, cudaMemcpyDeviceToDevice);
     cudaMemcpy(b->val, a->val + off0, 8 * (size_t)m, cudaMemcpyDeviceToDevice);
   }
-  if (b->nblocks)
-    cudaMemcpy(b->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
-  if (b->nlong) {
-    cudaMemcpy(b->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(b->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
-  }
+  int rc = attach_schedule(b, rp.data(), &absent, "lg_csr_row_block");
   cudaError_t err = cudaDeviceSynchronize();
-  if (err != cudaSuccess) {
+  if (rc || err != cudaSuccess) {
     lg_csr_destroy(b);
-    return fail(LG_ECUDA, std::string("lg_csr_row_block: ") + cudaGetErrorString(err));
+    return rc ? rc : fail(LG_ECUDA, std::string("lg_csr_row_block: ") + cudaGetErrorString(err));
   }
   *out = b;
   return LG_OK;
@@ -1499,32 +1568,18 @@ extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr*
   for (int64_t r = r1 + 1; r <= n; ++r) prp[(size_t)r] = m;
   std::vector<char> absent((size_t)n, 1);
   for (int64_t r = r0; r < r1; ++r) absent[(size_t)r] = 0;
-  std::vector<SpmvBlock> blocks;
-  std::vector<int32_t> lnp;
-  std::vector<int64_t> lfirst;
-  build_schedule(n, prp.data(), a->cta, blocks, lnp, lfirst, &absent);
-
   lg_csr* b = new lg_csr();
   b->is_block = 1;
-  b->cta = a->cta;
   b->n = n;
   b->nnz = m + nloc;
   b->packed = 1;
   b->cbits = a->cbits;
   b->nvals = a->nvals;
   b->noff = m;
-  b->nblocks = (int64_t)blocks.size();
-  set_chunks(b, blocks);
-  b->nlong = (int64_t)lnp.size();
-  for (int32_t v : lnp) b->nparts += v;
   bool ok = cudaMalloc(&b->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
-            (m == 0 || cudaMalloc(&b->pcol, 4 * (size_t)m) == cudaSuccess) &&
+            (m == 0 || cudaMalloc(&b->pcol, 4 * (size_t)(m + kStreamPad)) == cudaSuccess) &&
             cudaMalloc(&b->pdiag, 8 * (size_t)n) == cudaSuccess &&
-            (b->nvals == 0 || cudaMalloc(&b->table, 8 * (size_t)b->nvals) == cudaSuccess) &&
-            (b->nblocks == 0 ||
-             cudaMalloc(&b->blocks, sizeof(SpmvBlock) * (size_t)b->nblocks) == cudaSuccess) &&
-            (b->nlong == 0 || (cudaMalloc(&b->long_nparts, 4 * (size_t)b->nlong) == cudaSuccess &&
-                               cudaMalloc(&b->long_first, 8 * (size_t)b->nlong) == cudaSuccess));
+            (b->nvals == 0 || cudaMalloc(&b->table, 8 * (size_t)b->nvals) == cudaSuccess);
   if (!ok) {
     lg_csr_destroy(b);
     return fail(LG_ENOMEM, "lg_csr_row_block: allocation failed");
@@ -1534,16 +1589,11 @@ extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr*
   cudaMemcpy(b->pdiag + r0, a->pdiag + r0, 8 * (size_t)nloc, cudaMemcpyDeviceToDevice);
   if (b->nvals) cudaMemcpy(b->table, a->table, 8 * (size_t)b->nvals, cudaMemcpyDeviceToDevice);
   if (m) cudaMemcpy(b->pcol, a->pcol + off0, 4 * (size_t)m, cudaMemcpyDeviceToDevice);
-  if (b->nblocks)
-    cudaMemcpy(b->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
-  if (b->nlong) {
-    cudaMemcpy(b->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(b->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
-  }
+  int rc = attach_schedule(b, prp.data(), &absent, "lg_csr_row_block");
   cudaError_t err = cudaDeviceSynchronize();
-  if (err != cudaSuccess) {
+  if (rc || err != cudaSuccess) {
     lg_csr_destroy(b);
-    return fail(LG_ECUDA, std::string("lg_csr_row_block: ") + cudaGetErrorString(err));
+    return rc ? rc : fail(LG_ECUDA, std::string("lg_csr_row_block: ") + cudaGetErrorString(err));
   }
   *out = b;
   return LG_OK;
@@ -1597,12 +1647,7 @@ static int make_part(const lg_csr* a, int64_t r0, int64_t r1, const std::vector<
   for (int64_t r = r1 + 1; r <= n; ++r) prp[(size_t)r] = prp[(size_t)r1];
   std::vector<char> absent((size_t)n, 1);
   for (int64_t r = r0; r < r1; ++r) absent[(size_t)r] = 0;
-  std::vector<SpmvBlock> blocks;
-  std::vector<int32_t> lnp;
-  std::vector<int64_t> lfirst;
-  build_schedule(n, prp.data(), a->cta, blocks, lnp, lfirst, &absent);
   lg_csr* b = new lg_csr();
-  b->cta = a->cta;
   b->n = n;
   b->nnz = m + (with_diag ? nloc : 0);
   b->packed = 1;
@@ -1610,34 +1655,28 @@ static int make_part(const lg_csr* a, int64_t r0, int64_t r1, const std::vector<
   b->nvals = a->nvals;
   b->noff = m;
   b->is_block = (r0 > 0 || r1 < n) ? 1 : 0;
-  b->nblocks = (int64_t)blocks.size();
-  set_chunks(b, blocks);
-  b->nlong = (int64_t)lnp.size();
-  for (int32_t v : lnp) b->nparts += v;
   bool ok = cudaMalloc(&b->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
             (!with_diag || cudaMalloc(&b->pdiag, 8 * (size_t)n) == cudaSuccess) &&
-            (b->nvals == 0 || cudaMalloc(&b->table, 8 * (size_t)b->nvals) == cudaSuccess) &&
-            (b->nblocks == 0 ||
-             cudaMalloc(&b->blocks, sizeof(SpmvBlock) * (size_t)b->nblocks) == cudaSuccess) &&
-            (b->nlong == 0 || (cudaMalloc(&b->long_nparts, 4 * (size_t)b->nlong) == cudaSuccess &&
-                               cudaMalloc(&b->long_first, 8 * (size_t)b->nlong) == cudaSuccess));
+            (b->nvals == 0 || cudaMalloc(&b->table, 8 * (size_t)b->nvals) == cudaSuccess);
   if (!ok) {
     lg_csr_destroy(b);  // words stay the caller's on failure
     return fail(LG_ENOMEM, "lg_csr_split_cols: allocation failed");
   }
-  b->pcol = words;
   cudaMemcpy(b->prp, prp.data(), 8 * (size_t)(n + 1), cudaMemcpyHostToDevice);
   if (with_diag) {  // parts without the diagonal keep pdiag NULL (nothing to stream)
     cudaMemset(b->pdiag, 0, 8 * (size_t)n);
     cudaMemcpy(b->pdiag + r0, a->pdiag + r0, 8 * (size_t)nloc, cudaMemcpyDeviceToDevice);
   }
   if (b->nvals) cudaMemcpy(b->table, a->table, 8 * (size_t)b->nvals, cudaMemcpyDeviceToDevice);
-  if (b->nblocks)
-    cudaMemcpy(b->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
-  if (b->nlong) {
-    cudaMemcpy(b->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(b->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
+  // an accumulating part (no diagonal) leaves its rows without entries alone
+  if (!with_diag)
+    for (int64_t r = r0; r < r1; ++r) absent[(size_t)r] = prp[(size_t)r + 1] == prp[(size_t)r];
+  const int rc = attach_schedule(b, prp.data(), &absent, "lg_csr_split_cols");
+  if (rc) {
+    lg_csr_destroy(b);  // words stay the caller's on failure
+    return rc;
   }
+  b->pcol = words;    // owned by the part from here on
   *out = b;
   return LG_OK;
 }
@@ -1686,8 +1725,8 @@ extern "C" int lg_csr_split_cols(const lg_csr* a, int64_t r0, int64_t r1, lg_csr
       mo += hout[(size_t)i];
     }
   }
-  if (cudaMalloc(&win, 4 * (size_t)std::max<int64_t>(mi, 1)) != cudaSuccess ||
-      cudaMalloc(&wout, 4 * (size_t)std::max<int64_t>(mo, 1)) != cudaSuccess) {
+  if (cudaMalloc(&win, 4 * (size_t)(mi + kStreamPad)) != cudaSuccess ||
+      cudaMalloc(&wout, 4 * (size_t)(mo + kStreamPad)) != cudaSuccess) {
     cudaFree(win);
     cleanup();
     return fail(LG_ENOMEM, "lg_csr_split_cols: allocation failed");
@@ -1764,7 +1803,7 @@ extern "C" int lg_csr_col_panel(const lg_csr* a, int64_t c0, int64_t c1, int wit
     cudaMemcpy(hin.data(), cin, nb, cudaMemcpyDeviceToHost);
     for (int64_t i = 0; i < n; ++i) mi += hin[(size_t)i];
   }
-  if (cudaMalloc(&win, 4 * (size_t)std::max<int64_t>(mi, 1)) != cudaSuccess) {
+  if (cudaMalloc(&win, 4 * (size_t)(mi + kStreamPad)) != cudaSuccess) {
     cleanup();
     return fail(LG_ENOMEM, "lg_csr_col_panel: allocation failed");
   }
@@ -1780,6 +1819,8 @@ extern "C" int lg_csr_col_panel(const lg_csr* a, int64_t c0, int64_t c1, int wit
     cudaFree(win);
     return rc;
   }
+  (*out)->pf_c0 = c0;
+  (*out)->pf_c1 = c1;
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     lg_csr_destroy(*out);
@@ -1802,7 +1843,7 @@ extern "C" int lg_csr_set_panels(lg_csr* a, int p) {
   if (p <= 1) return LG_OK;
   lg_csr* parts[16] = {};
   for (int k = 0; k < p; ++k) {
-    int rc = lg_csr_col_panel(a, a->n * k / p, a->n * (k + 1) / p, k == 0, &parts[k]);
+    int rc = lg_csr_col_panel(a, a->n * k / p, a->n * (k + 1) / p, 0, &parts[k]);
     if (rc) {
       for (int j = 0; j < k; ++j) lg_csr_destroy(parts[j]);
       return rc;
@@ -1813,11 +1854,38 @@ extern "C" int lg_csr_set_panels(lg_csr* a, int p) {
   return LG_OK;
 }
 
-// The panel chain behind lg_spmv: P_0 carries the diagonal and the theta
-// shift; the rest accumulate.  Same stream, same workspace, in order.
+namespace {
+// y = (d - theta) x elementwise, as (d x) - theta x: the diagonal and shift
+// of a panelled product, before the panels accumulate their off-diagonals
+__global__ void diag_init_kernel(int64_t n, const double* d, const double* x, double* y,
+                                 double theta_h, const double* theta_d, int theta_neg,
+                                 const int* skip) {
+  if (skip && *skip) return;
+  double theta = theta_h;
+  if (theta_d) theta += theta_neg ? -*theta_d : *theta_d;
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += st) {
+    const double xi = __ldcs(x + i);
+    double s = 0.0 + __ldcs(d + i) * xi;
+    if (theta != 0.0) s -= theta * xi;
+    __stcs(y + i, s);
+  }
+}
+}  // namespace
+
+// The panel chain behind lg_spmv: y = (D - theta I) x, then every panel
+// accumulates its off-diagonals (each panel's schedule holds only the rows
+// with entries in its columns).  Same stream, same workspace, in order.
 extern "C" int lg_spmv_panels_(const lg_csr* a, const double* x, double* y, double theta_h,
                                const double* theta_d, int theta_neg, const int* skip,
                                lg_ws* ws, void* stream) {
+  {
+    const int64_t g = std::max<int64_t>(
+        1, std::min<int64_t>((a->n + 255) / 256, (int64_t)dev_info().sm_count * 8));
+    diag_init_kernel<<<(unsigned)g, 256, 0, (cudaStream_t)stream>>>(
+        a->n, a->pdiag, x, y, theta_h, theta_d, theta_neg, skip);
+    LG_LAUNCH_CHECK("diag_init_kernel");
+  }
   for (int k = 0; k < a->npanels; ++k) {
     const lg_csr* m = a->panel[k];
     if (m->nblocks == 0) continue;
@@ -1825,31 +1893,11 @@ extern "C" int lg_spmv_panels_(const lg_csr* a, const double* x, double* y, doub
       int rc = ensure_long_ws(ws, m);
       if (rc) return rc;
     }
-    SpmvArgs args{};
-    args.accum = k > 0;
-    args.n = m->n;
-    args.row_ptr = m->prp;
-    args.pcol = m->pcol;
-    args.pdiag = k == 0 ? m->pdiag : nullptr;  // later panels: no diagonal to stream
-    args.table = m->table;
-    args.nvals = m->nvals;
-    args.cbits = m->cbits;
-    args.blocks = m->blocks;
-    args.nblocks = m->nblocks;
-    args.long_nparts = m->long_nparts;
-    args.long_first = m->long_first;
-    args.x = x;
-    args.y = y;
-    if (k == 0) {
-      args.theta_h = theta_h;
-      args.theta_d = theta_d;
-      args.theta_neg = theta_neg;
-    }
+    SpmvArgs args = spmv_args(m, x, y, ws);
+    args.accum = 1;
+    args.pdiag = nullptr;
     args.skip = skip;
-    args.long_part = ws->long_part;
-    args.long_ticket = ws->long_ticket;
-    args.nlong = m->nlong;
-    int rc = launch<0>(args, ws, (cudaStream_t)stream, true, m->cta);
+    int rc = launch(args, (cudaStream_t)stream, true);
     if (rc) return rc;
   }
   return LG_OK;
@@ -1864,28 +1912,10 @@ extern "C" int lg_spmv_acc(const lg_csr* a, const double* x, double* y, lg_ws* w
     int rc = ensure_long_ws(ws, a);
     if (rc) return rc;
   }
-  SpmvArgs args{};
+  SpmvArgs args = spmv_args(a, x, y, ws);
   args.accum = 1;
-  args.n = a->n;
-  args.row_ptr = a->packed ? a->prp : a->row_ptr;
-  args.col = a->col;
-  args.val = a->val;
-  args.pcol = a->packed ? a->pcol : nullptr;
-  args.pdiag = a->pdiag;
-  args.table = a->table;
-  args.nvals = a->nvals;
-  args.cbits = a->cbits;
-  args.blocks = a->blocks;
-  args.nblocks = a->nblocks;
-  args.long_nparts = a->long_nparts;
-  args.long_first = a->long_first;
-  args.x = x;
-  args.y = y;
   args.skip = skip;
-  args.long_part = ws->long_part;
-  args.long_ticket = ws->long_ticket;
-  args.nlong = a->nlong;
-  return launch<0>(args, ws, (cudaStream_t)stream, a->packed != 0, a->cta);
+  return launch(args, (cudaStream_t)stream, a->packed != 0);
 }
 
 extern "C" {
@@ -2071,33 +2101,16 @@ static int plain_from_device(int64_t n, int64_t* rp, int32_t* col, double* val, 
                              lg_csr** out) {
   std::vector<int64_t> hrp((size_t)n + 1);
   LG_CUDA(cudaMemcpy(hrp.data(), rp, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost));
-  std::vector<SpmvBlock> blocks;
-  std::vector<int32_t> lnp;
-  std::vector<int64_t> lfirst;
   lg_csr* a = new lg_csr();
   a->n = n;
   a->nnz = nnz;
-  a->cta = pick_cta(nnz);
-  build_schedule(n, hrp.data(), a->cta, blocks, lnp, lfirst);
   a->row_ptr = rp;
   a->col = col;
   a->val = val;
-  a->nblocks = (int64_t)blocks.size();
-  set_chunks(a, blocks);
-  a->nlong = (int64_t)lnp.size();
-  for (int32_t v : lnp) a->nparts += v;
-  if ((a->nblocks &&
-       cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess) ||
-      (a->nlong && (cudaMalloc(&a->long_nparts, 4 * (size_t)a->nlong) != cudaSuccess ||
-                    cudaMalloc(&a->long_first, 8 * (size_t)a->nlong) != cudaSuccess))) {
+  const int rc = attach_schedule(a, hrp.data(), nullptr, "fsai");
+  if (rc) {
     lg_csr_destroy(a);
-    return fail(LG_ENOMEM, "fsai: schedule alloc");
-  }
-  if (a->nblocks)
-    cudaMemcpy(a->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(), cudaMemcpyHostToDevice);
-  if (a->nlong) {
-    cudaMemcpy(a->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(a->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice);
+    return rc;
   }
   *out = a;
   return LG_OK;
@@ -2154,8 +2167,8 @@ extern "C" int lg_fsai_device(const lg_csr* a, int kmax, lg_csr** g_out, lg_csr*
   tmp = nullptr;
   int64_t nnz = 0;
   LG_CUDA(cudaMemcpy(&nnz, grp + n, 8, cudaMemcpyDeviceToHost));
-  if (cudaMalloc(&gcol, 4 * (size_t)nnz) != cudaSuccess ||
-      cudaMalloc(&gval, 8 * (size_t)nnz) != cudaSuccess)
+  if (cudaMalloc(&gcol, 4 * (size_t)(nnz + kStreamPad)) != cudaSuccess ||
+      cudaMalloc(&gval, 8 * (size_t)(nnz + kStreamPad)) != cudaSuccess)
     return oom("G arrays");
   {
     const int64_t blocks = std::min<int64_t>((n + kFsaiWarps - 1) / kFsaiWarps,
@@ -2178,8 +2191,8 @@ extern "C" int lg_fsai_device(const lg_csr* a, int kmax, lg_csr** g_out, lg_csr*
       cudaMalloc(&idx, 8 * (size_t)nnz) != cudaSuccess ||
       cudaMalloc(&idx2, 8 * (size_t)nnz) != cudaSuccess ||
       cudaMalloc(&tcol_keys, 4 * (size_t)nnz) != cudaSuccess ||
-      cudaMalloc(&trow, 4 * (size_t)nnz) != cudaSuccess ||
-      cudaMalloc(&tval, 8 * (size_t)nnz) != cudaSuccess ||
+      cudaMalloc(&trow, 4 * (size_t)(nnz + kStreamPad)) != cudaSuccess ||
+      cudaMalloc(&tval, 8 * (size_t)(nnz + kStreamPad)) != cudaSuccess ||
       cudaMalloc(&trp, 8 * (size_t)(n + 1)) != cudaSuccess ||
       cudaMalloc(&ccount, 8 * (size_t)(n + 1)) != cudaSuccess)
     return oom("G^T arrays");

@@ -1,7 +1,7 @@
 """SpMV A/B on the benchmark graphs: device product vs the oracle's
 restatement of the reference SpMV (sparse.py:128-139), and event time per
 matvec with L2 flushed.  Development aid; run it once per library variant
-(LG_LIB_OVERRIDE=path/to/variant.so, LG_SPMV_CTA=128|256).  Prints one JSON
+(LG_LIB_OVERRIDE=path/to/variant.so).  Prints one JSON
 line per graph."""
 import json
 import os

@@ -405,8 +405,10 @@ def test_device_rmat_lcc_laplacian_pipeline(L):
 def test_row_partitioned_spmv_row_blocks(L, world):
     """The multi-GPU SpMV's per-rank operators (the rank's rows, global
     columns, other rows absent from the schedule), run one after another on
-    one device on the exchanged x, reproduce the single-device product bit
-    for bit and write only their own rows."""
+    one device on the exchanged x, reproduce the single-device product to
+    roundoff (a row block's warp windows need not fall where the full
+    operator's do, so the per-row summation order may differ) and write only
+    their own rows."""
     import torch
     from paper_1311_1695_b200 import _device as dev
     from paper_1311_1695_b200.dist import RowPartition, local_operator
@@ -425,14 +427,14 @@ def test_row_partitioned_spmv_row_blocks(L, world):
         r0, r1 = part.rows(r)
         assert torch.all(ys[:r0] == 12345.0) and torch.all(ys[r1:] == 12345.0)
         y[r0:r1] = ys[r0:r1]
-    assert torch.equal(y, y_ref)
+    assert float((y - y_ref).abs().max()) <= 1e-14 * float(y_ref.abs().max())
 
 
 @pytest.mark.parametrize("world", [2, 5])
 def test_row_partitioned_spmv_device_sliced(L, world):
     """Device-side row blocks of a device-only packed Laplacian (the C5 path:
     R-MAT sampled, LCC and assembled on the device) reproduce the full
-    product bit for bit."""
+    product to roundoff."""
     import torch
     from paper_1311_1695_b200 import _device as dev
     from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
@@ -451,7 +453,7 @@ def test_row_partitioned_spmv_device_sliced(L, world):
         r0, r1 = part.rows(r)
         assert torch.all(ys[:r0] == -7.0) and torch.all(ys[r1:] == -7.0)
         y[r0:r1] = ys[r0:r1]
-    assert torch.equal(y, y_ref)
+    assert float((y - y_ref).abs().max()) <= 1e-14 * float(y_ref.abs().max())
 
 
 def test_spmv_host_buffers_cabi_and_public():
@@ -636,44 +638,56 @@ def test_set_panels_rejects_row_blocks():
     assert bool((y[r1:] == 7.0).all())
 
 
-def test_spmv_256_thread_schedule_parity():
-    """The 256-thread schedule (chosen for matrices with >= 2^27
-    off-diagonals, forced here with LG_SPMV_CTA=256 in a child process) gives
-    the same products as the oracle on fixtures with empty rows, hub rows
-    longer than one block, weighted values and a row-block operator."""
-    import subprocess
-    import sys
-    code = r'''
-import numpy as np, torch
-import paper_1311_1695_b200 as L
-from oracle import lapeig_oracle as O
-from paper_1311_1695_b200 import _device as dev
-from paper_1311_1695_b200.dist import RowPartition, local_operator
-rng = np.random.default_rng(7)
-gs = [L.largest_component(L.generators.chung_lu_graph(20000, 2.1, 8.0, max_degree=6000,
-                                                      weighted=True, seed=11))[0],
-      L.generators.star_graph(5000), L.generators.grid_graph(60, 70)]
-for g in gs:
+def test_spmv_warp_schedule_edge_cases():
+    """The warp-block schedule on the shapes that exercise each block kind:
+    hub rows longer than a part (ticketed long-row parts), rows with no
+    off-diagonal entry (row-serial blocks: isolated vertices outside an LCC,
+    and rows of a SKIP_EMPTY operator), weighted values (value table), a plain
+    (unpacked) matrix, rows that straddle lanes and the 16-byte window phase
+    of every block start; each product matches the oracle's reduceat SpMV,
+    theta-shifted and accumulating forms included, and is bitwise the same
+    run to run."""
+    import torch
+
+    import paper_1311_1695_b200 as L
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200.graphs import EdgeList
+    rng = np.random.default_rng(7)
+    cl = L.generators.chung_lu_graph(20000, 2.1, 8.0, max_degree=6000, weighted=True, seed=11)
+    gs = [L.largest_component(cl)[0], cl, L.generators.star_graph(5000),
+          L.generators.grid_graph(60, 70), L.generators.path_graph(3),
+          L.generators.complete_graph(300)]
+    for g in gs:
+        a = L.build_laplacian(g)
+        oa = O.Csr(a.n, a.row_ptr, a.col_idx, a.values)
+        x = rng.standard_normal(a.n)
+        want = O.spmv(oa, x)
+        tol = 1e-13 * max(1.0, float(np.max(np.abs(want))))
+        y = L.spmv(a, x)
+        assert np.max(np.abs(y - want)) <= tol
+        d = a.device()
+        xd = dev.to_device(x)
+        y1, y2 = dev.empty(a.n), dev.empty(a.n)
+        d.matvec(xd, y1)
+        d.matvec(xd, y2)
+        assert torch.equal(y1, y2)
+        yt = dev.empty(a.n)
+        d.matvec(xd, yt, theta=0.75)
+        assert np.max(np.abs(dev.to_host(yt) - (want - 0.75 * x))) <= tol
+    # a plain-format operator: more distinct values than the packed table holds
+    n = 3000
+    i = rng.integers(0, n, 40000)
+    j = rng.integers(0, n, 40000)
+    keep = i != j
+    lo, hi = np.minimum(i[keep], j[keep]), np.maximum(i[keep], j[keep])
+    key = np.unique(lo.astype(np.int64) * n + hi)
+    g = EdgeList(n, key // n, key % n, rng.random(key.size) + 0.5)
     a = L.build_laplacian(g)
+    assert not a.device().packed
     x = rng.standard_normal(a.n)
     want = O.spmv(O.Csr(a.n, a.row_ptr, a.col_idx, a.values), x)
-    y = L.spmv(a, x)
-    assert np.max(np.abs(y - want)) <= 1e-13 * np.max(np.abs(want)), "spmv"
-    part = RowPartition(a.row_ptr, 2)
-    yd = dev.empty(a.n)
-    full = dev.empty(a.n)
-    a.device().matvec(dev.to_device(x), full)
-    for r in range(2):
-        r0, r1 = part.rows(r)
-        local_operator(a, part, r).matvec(dev.to_device(x), yd)
-        torch.cuda.synchronize()
-        assert torch.equal(yd[r0:r1], full[r0:r1]), "row block"
-print("OK")
-'''
-    env = dict(os.environ, LG_SPMV_CTA="256")
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                         timeout=600, cwd=str(ROOT))
-    assert out.returncode == 0 and "OK" in out.stdout, out.stderr[-2000:]
+    assert np.max(np.abs(L.spmv(a, x) - want)) <= 1e-13 * np.max(np.abs(want))
 
 
 @pytest.mark.gpu
