@@ -108,6 +108,7 @@ struct lg_csr {
   uint32_t* pcol = nullptr;        // col | vidx << cbits
   double* pdiag = nullptr;         // diagonal [n]
   double* table = nullptr;         // distinct off-diagonal values [nvals]
+  int intw = 0;                    // table[i] == -(i + 1) for every i (integer weights)
   int32_t* long_nparts = nullptr;  // device [nlong]
   int64_t* long_first = nullptr;   // device [nlong] slot of part 0
   // row chunks of the schedule for the host-buffer path (lg_spmv_host):
@@ -143,6 +144,7 @@ struct SpmvArgs {
   const double* table;
   int nvals;
   int cbits;
+  int intw;                 // value of index i is -(i + 1): computed, no table
   int64_t nzs;              // stream length (bounds the 128-bit loads)
   const SpmvBlock* blocks;
   int64_t nblocks;
@@ -208,7 +210,9 @@ __device__ __forceinline__ void wproducts(const SpmvArgs& a, const WWords<PACKED
   }
 #pragma unroll
   for (int j = 0; j < kWPer; ++j) {
-    if constexpr (PACKED) p[j] = xv[j] * tab[((vm >> j) & 1u) ? (L.w[j] >> a.cbits) : 0u];
+    if constexpr (PACKED)
+      p[j] = a.intw ? -(xv[j] * __uint2double_rn((L.w[j] >> a.cbits) + 1u))
+                    : xv[j] * tab[((vm >> j) & 1u) ? (L.w[j] >> a.cbits) : 0u];
     else p[j] = ((vm >> j) & 1u) ? L.v[j] * xv[j] : 0.0;
   }
 }
@@ -644,6 +648,7 @@ static SpmvArgs spmv_args(const lg_csr* m, const double* x, double* y, lg_ws* ws
   args.table = m->table;
   args.nvals = m->nvals;
   args.cbits = m->cbits;
+  args.intw = m->intw;
   args.nzs = m->packed ? m->noff : m->nnz;
   args.blocks = m->blocks;
   args.nblocks = m->nblocks;
@@ -772,6 +777,29 @@ static bool make_packed(int64_t n, const int64_t* rp, const int64_t* col, const 
   }
   table.resize(uniq.size());
   for (size_t i = 0; i < uniq.size(); ++i) std::memcpy(&table[i], &uniq[i], 8);
+  // integer weights (every off-diagonal value is -k for an integer k >= 1,
+  // e.g. unit graphs or C4's Geometric counts): a dense table -1, -2, ...,
+  // -kmax (unused entries included) so the value of index i is -(i + 1) and
+  // the SpMV computes it instead of looking it up (lg_csr.intw)
+  {
+    bool ints = !uniq.empty();
+    int64_t kmax = 0;
+    for (double v : table) {
+      const double k = -v;
+      if (!(k >= 1.0 && k <= 2048.0 && k == (double)(int64_t)k)) {
+        ints = false;
+        break;
+      }
+      kmax = std::max<int64_t>(kmax, (int64_t)k);
+    }
+    if (ints && kmax <= maxvals) {
+      std::vector<double> dense((size_t)kmax);
+      for (int64_t i = 0; i < kmax; ++i) dense[(size_t)i] = -(double)(i + 1);
+      table.swap(dense);
+      uniq.resize((size_t)kmax);
+      for (int64_t i = 0; i < kmax; ++i) std::memcpy(&uniq[(size_t)i], &table[(size_t)i], 8);
+    }
+  }
   prp.assign((size_t)n + 1, 0);
   diag.assign((size_t)n, 0.0);
   const int64_t noff = rp[n] - ndiag;
@@ -835,6 +863,8 @@ int lg_csr_create(int64_t n, int64_t nnz, const int64_t* rp, const int64_t* col,
   a->packed = packed ? 1 : 0;
   a->cbits = cbits;
   a->nvals = (int)table.size();
+  a->intw = packed && !table.empty() ? 1 : 0;
+  for (size_t i = 0; i < table.size() && a->intw; ++i) a->intw = table[i] == -(double)(i + 1);
   a->noff = packed ? (int64_t)pcol.size() : 0;
   a->is_block = (flags & LG_CSR_SKIP_EMPTY) ? 1 : 0;
   auto cleanup = [&](const char* what) {
@@ -1420,6 +1450,7 @@ extern "C" int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,
   a->packed = 1;
   a->cbits = cbits;
   a->nvals = 1;
+  a->intw = 1;   // table = {-1}
   a->noff = 2 * m;
   int32_t *up = nullptr, *lo = nullptr, *sj = nullptr, *si = nullptr;
   int64_t *len = nullptr, *up64 = nullptr, *lo64 = nullptr, *ustart = nullptr,
@@ -1575,6 +1606,7 @@ extern "C" int lg_csr_row_block(const lg_csr* a, int64_t r0, int64_t r1, lg_csr*
   b->packed = 1;
   b->cbits = a->cbits;
   b->nvals = a->nvals;
+  b->intw = a->intw;
   b->noff = m;
   bool ok = cudaMalloc(&b->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&
             (m == 0 || cudaMalloc(&b->pcol, 4 * (size_t)(m + kStreamPad)) == cudaSuccess) &&
@@ -1653,6 +1685,7 @@ static int make_part(const lg_csr* a, int64_t r0, int64_t r1, const std::vector<
   b->packed = 1;
   b->cbits = a->cbits;
   b->nvals = a->nvals;
+  b->intw = a->intw;
   b->noff = m;
   b->is_block = (r0 > 0 || r1 < n) ? 1 : 0;
   bool ok = cudaMalloc(&b->prp, 8 * (size_t)(n + 1)) == cudaSuccess &&

@@ -135,8 +135,12 @@ struct ProgDev {
   int* fg;
 };
 
+#ifndef LG_FUSED_MINB4
+#define LG_FUSED_MINB4 3   // resident CTAs for the 4-wide tiles (NA <= 4): 85 registers, no spill
+#endif
 template <int NA, bool PROG>
-__global__ void __launch_bounds__(kThreads, (NA <= 8 ? 4 : (NA <= 16 ? 2 : 1)))
+__global__ void __launch_bounds__(kThreads, (NA <= 4 ? LG_FUSED_MINB4
+                                             : (NA <= 8 ? 4 : (NA <= 16 ? 2 : 1))))
 fused_kernel(FusedDev a, lg_ws ws, const __grid_constant__ ProgDev pd) {
   constexpr int U = fused_u<NA>();
   if (a.skip && *a.skip) return;

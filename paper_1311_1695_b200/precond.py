@@ -10,13 +10,15 @@ apply_raw(r_ptr, z_ptr, skip, stream); device_preconditioner() adapts:
     any other object with .apply / callable       -> called on CUDA tensors
 """
 
+import weakref
+
 import numpy as np
 
 from . import _device as dev
 from . import _native as nat
 from ._plan import Fused
 
-_cache = {}
+_cache = weakref.WeakKeyDictionary()
 
 
 class IdentityPrec:
@@ -339,10 +341,14 @@ def device_preconditioner(f, n):
     if isinstance(f, (JacobiFactor, FsaiFactor, Ic0JacobiFactor)):
         return f.device()
     if hasattr(f, "l") and hasattr(f.l, "row_ptr"):
-        hit = _cache.get(id(f))
-        if hit is None or hit[0] is not f:
-            hit = (f, DeviceIc0(f.l))
-            _cache[id(f)] = hit
-        return hit[1]
+        # a foreign Ic0Factor-like object (the reference's own, ic0.py:24-45):
+        # its device copy lives as long as the object, never longer
+        try:
+            hit = _cache.get(f)
+            if hit is None:
+                hit = _cache[f] = DeviceIc0(f.l)
+            return hit
+        except TypeError:   # not weak-referenceable: no caching
+            return DeviceIc0(f.l)
     fn = f if callable(f) else f.apply
     return CallablePrec(fn, n)
