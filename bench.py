@@ -764,7 +764,7 @@ def main():
         sys.path.insert(0, str(ROOT / "scripts"))
         from vendor_cusparse import vendor_block
         fv = line_factor.get("f")
-        line["vendor"] = vendor_block(a, fv, x, _event_timer)
+        line["vendor"] = vendor_block(a, fv, x, _event_timer, flush)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -111,6 +111,7 @@ struct lg_csr {
   int intw = 0;                    // table[i] == -(i + 1) for every i (integer weights)
   int32_t* long_nparts = nullptr;  // device [nlong]
   int64_t* long_first = nullptr;   // device [nlong] slot of part 0
+  int32_t* long_row = nullptr;     // device [nlong] schedule row of each long row
   // row chunks of the schedule for the host-buffer path (lg_spmv_host):
   // blocks [chunk_b[c], chunk_b[c+1]) cover rows [chunk_row[c], chunk_row[c+1])
   int nchunks = 0;
@@ -133,6 +134,9 @@ struct lg_csr {
 namespace lg {
 
 constexpr int kMaxTable = 2048;   // value-table entries kept in shared memory
+// long-row parts from which the deferred finish (one more launch) beats a
+// ticket per part: measured C5 13.6 -> 9.6 ms, C3 35.4 -> 33.8 us, C4 equal
+constexpr int64_t kDeferParts = 1;
 
 struct SpmvArgs {
   int64_t n;
@@ -150,6 +154,8 @@ struct SpmvArgs {
   int64_t nblocks;
   const int32_t* long_nparts;
   const int64_t* long_first;
+  const int32_t* long_row;
+  int defer_long;           // parts only publish; long_finish_kernel sums them
   const double* x;
   double* y;
   int accum;        // y += A x (the second half of a split row block)
@@ -360,7 +366,9 @@ __global__ void __launch_bounds__(kWThreads, PACKED ? LG_SPMV_MINB : 3) wspmv_ke
       s = warp_sum(s);
       unsigned last = 0u;
       const int lr = d.nrows;
-      if (lane == 0) {
+      if (a.defer_long) {   // long_finish_kernel sums the parts after this launch
+        if (lane == 0) a.long_part[d.part] = s;
+      } else if (lane == 0) {
         LG_CK(d.part >= 0 && d.part < a.nparts && lr >= 0 && lr < a.nlong, "long part");
         a.long_part[d.part] = s;
         // release: the partial is visible before the ticket moves
@@ -447,6 +455,29 @@ __global__ void __launch_bounds__(kWThreads, PACKED ? LG_SPMV_MINB : 3) wspmv_ke
   }
 }
 
+// Deferred long rows (SpmvArgs.defer_long): after the product kernel, one warp
+// per long row sums its parts lane-strided then by butterfly -- the same
+// order as the ticket finish, so the same bits -- and finishes the row.  One
+// extra launch instead of an atomic ticket and a release per part (C5: ~7 M
+// parts a product).
+template <bool PACKED>
+__global__ void __launch_bounds__(256) long_finish_kernel(SpmvArgs a) {
+  if (a.skip && *a.skip) return;
+  double theta = a.theta_h;
+  if (a.theta_d) theta += a.theta_neg ? -*a.theta_d : *a.theta_d;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t lr = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; lr < a.nlong;
+       lr += nw) {
+    const int64_t first = a.long_first[lr];
+    const int np = a.long_nparts[lr];
+    double t = 0.0;
+    for (int q = lane; q < np; q += 32) t += a.long_part[first + q];
+    t = warp_sum(t);
+    if (lane == 0) finish_row<PACKED>(a, a.long_row[lr], t, theta);
+  }
+}
+
 // Build the warp-block schedule on the host.
 // absent (optional): rows left out of the schedule altogether (y is not
 // written there) -- the row block of one rank in the row-partitioned
@@ -454,6 +485,7 @@ __global__ void __launch_bounds__(kWThreads, PACKED ? LG_SPMV_MINB : 3) wspmv_ke
 static void build_schedule(int64_t n, const int64_t* rp, std::vector<SpmvBlock>& blocks,
                            std::vector<int32_t>& long_nparts,
                            std::vector<int64_t>& long_first,
+                           std::vector<int32_t>& long_row,
                            const std::vector<char>* absent = nullptr) {
   int64_t r = 0, part_total = 0;
   blocks.reserve((size_t)(rp[n] / (kWin - 16) + n / kWRows + 16));
@@ -470,6 +502,7 @@ static void build_schedule(int64_t n, const int64_t* rp, std::vector<SpmvBlock>&
       const int64_t slot0 = part_total;
       part_total += np;
       long_first.push_back(slot0);
+      long_row.push_back((int32_t)r);
       for (int32_t q = 0; q < np; ++q) {
         SpmvBlock b{};
         b.nz0 = rp[r] + (int64_t)q * kLongPart;
@@ -551,7 +584,7 @@ static void set_chunks(lg_csr* a, const std::vector<SpmvBlock>& blocks) {
 static int attach_schedule(lg_csr* a, const int64_t* rp, const std::vector<char>* absent,
                            const char* who) {
   std::vector<SpmvBlock> blocks;
-  std::vector<int32_t> lnp;
+  std::vector<int32_t> lnp, lrow;
   std::vector<int64_t> lfirst;
   // Present rows in many separate runs (a column panel leaves every row
   // without an entry in its columns absent): schedule the present rows as one
@@ -582,12 +615,12 @@ static int attach_schedule(lg_csr* a, const int64_t* rp, const std::vector<char>
   }
   if (!map.empty()) {
     const int64_t nc = (int64_t)map.size();
-    build_schedule(nc, crp.data(), blocks, lnp, lfirst, nullptr);
+    build_schedule(nc, crp.data(), blocks, lnp, lfirst, lrow, nullptr);
     if (cudaMalloc(&a->rowmap, 4 * (size_t)nc) != cudaSuccess)
       return fail(LG_ENOMEM, std::string(who) + ": row map alloc");
     LG_CUDA(cudaMemcpy(a->rowmap, map.data(), 4 * (size_t)nc, cudaMemcpyHostToDevice));
   } else {
-    build_schedule(a->n, rp, blocks, lnp, lfirst, absent);
+    build_schedule(a->n, rp, blocks, lnp, lfirst, lrow, absent);
   }
   a->nblocks = (int64_t)blocks.size();
   set_chunks(a, blocks);
@@ -602,7 +635,8 @@ static int attach_schedule(lg_csr* a, const int64_t* rp, const std::vector<char>
   if ((a->nblocks &&
        cudaMalloc(&a->blocks, sizeof(SpmvBlock) * (size_t)a->nblocks) != cudaSuccess) ||
       (a->nlong && (cudaMalloc(&a->long_nparts, 4 * (size_t)a->nlong) != cudaSuccess ||
-                    cudaMalloc(&a->long_first, 8 * (size_t)a->nlong) != cudaSuccess)))
+                    cudaMalloc(&a->long_first, 8 * (size_t)a->nlong) != cudaSuccess ||
+                    cudaMalloc(&a->long_row, 4 * (size_t)a->nlong) != cudaSuccess)))
     return fail(LG_ENOMEM, std::string(who) + ": schedule alloc");
   if (a->nblocks)
     LG_CUDA(cudaMemcpy(a->blocks, blocks.data(), sizeof(SpmvBlock) * blocks.size(),
@@ -610,6 +644,7 @@ static int attach_schedule(lg_csr* a, const int64_t* rp, const std::vector<char>
   if (a->nlong) {
     LG_CUDA(cudaMemcpy(a->long_nparts, lnp.data(), 4 * lnp.size(), cudaMemcpyHostToDevice));
     LG_CUDA(cudaMemcpy(a->long_first, lfirst.data(), 8 * lfirst.size(), cudaMemcpyHostToDevice));
+    LG_CUDA(cudaMemcpy(a->long_row, lrow.data(), 4 * lrow.size(), cudaMemcpyHostToDevice));
   }
   return LG_OK;
 }
@@ -654,6 +689,15 @@ static SpmvArgs spmv_args(const lg_csr* m, const double* x, double* y, lg_ws* ws
   args.nblocks = m->nblocks;
   args.long_nparts = m->long_nparts;
   args.long_first = m->long_first;
+  args.long_row = m->long_row;
+  {
+    static const int defer_env = [] {
+      const char* e = getenv("LG_SPMV_DEFER");
+      return e ? atoi(e) : -1;
+    }();
+    args.defer_long = defer_env >= 0 ? (defer_env != 0 && m->nlong > 0)
+                                     : (m->nparts >= kDeferParts);
+  }
   args.x = x;
   args.y = y;
   args.long_part = ws ? ws->long_part : nullptr;
@@ -706,6 +750,12 @@ static int launch_t(const SpmvArgs& args, cudaStream_t s) {
   const size_t dyn = PACKED ? sizeof(double) * (size_t)std::max(args.nvals, 1) : 0;
   wspmv_kernel<PACKED><<<(unsigned)g, kWThreads, dyn, s>>>(args);
   LG_LAUNCH_CHECK("wspmv_kernel");
+  if (args.defer_long && args.nlong > 0) {
+    const int64_t gl = std::max<int64_t>(
+        1, std::min<int64_t>((args.nlong + 7) / 8, (int64_t)dev_info().sm_count * 8));
+    long_finish_kernel<PACKED><<<(unsigned)gl, 256, 0, s>>>(args);
+    LG_LAUNCH_CHECK("long_finish_kernel");
+  }
   return LG_OK;
 }
 
@@ -725,6 +775,7 @@ static int spmv_range(const lg_csr* a, const double* x, double* y, int64_t b0, i
   args.accum = accum;
   args.blocks = a->blocks + b0;
   args.nblocks = b1 - b0;
+  args.defer_long = 0;   // a chunk finishes its own long rows (tickets)
   return launch(args, s, a->packed != 0);
 }
 
@@ -924,6 +975,7 @@ int lg_csr_destroy(lg_csr* a) {
   cudaFree(a->blocks);
   cudaFree(a->long_nparts);
   cudaFree(a->long_first);
+  cudaFree(a->long_row);
   cudaFree(a->prp);
   cudaFree(a->pcol);
   cudaFree(a->pdiag);

@@ -4,8 +4,8 @@ API with ctypes -- descriptors, buffers and the SpSV analysis are built once,
 so each timed call is the vendor kernel alone (the best case for it).
 
 What it stands beside ("vendor comparator"):
-  * SpMV y = L x on the canonical CSR (int64 row offsets, int32 columns, f64
-    values): the reference's spmv, /root/reference/pkg/src/lapeig/sparse.py:128-139,
+  * SpMV y = L x on the canonical CSR (f64 values; int32 row offsets and
+    columns, the one index type cuSPARSE takes for both below 2^31 nonzeros): the reference's spmv, /root/reference/pkg/src/lapeig/sparse.py:128-139,
     next to lg_spmv (wspmv_kernel).
   * z = (L L^T)^{-1} r as two SpSV calls on the IC(0) factor L (lower, non-unit
     diagonal; the second with op = TRANSPOSE): the reference's Ic0Factor.apply,
@@ -58,12 +58,23 @@ class Handle:
         _ck(lib().cusparseSetStream(self.h, ctypes.c_void_p(stream_ptr)), "cusparseSetStream")
 
 
-def _csr(n, nnz, rp, col, val):
+def _index_arrays(row_ptr, col_idx):
+    """Row offsets and columns in ONE index type (cuSPARSE's generic CSR API
+    rejects mixed 64/32-bit index types): int32 when nnz < 2^31, else int64."""
+    import torch
+    wide = int(row_ptr[-1]) >= 2**31 - 1
+    dt = np.int64 if wide else np.int32
+    rp = torch.from_numpy(np.asarray(row_ptr, dtype=dt)).cuda()
+    col = torch.from_numpy(np.asarray(col_idx, dtype=dt)).cuda()
+    return rp, col, (_IDX64 if wide else _IDX32)
+
+
+def _csr(n, nnz, rp, col, val, idx):
     m = ctypes.c_void_p()
     _ck(lib().cusparseCreateCsr(ctypes.byref(m), ctypes.c_int64(n), ctypes.c_int64(n),
                                 ctypes.c_int64(nnz), ctypes.c_void_p(rp.data_ptr()),
                                 ctypes.c_void_p(col.data_ptr()), ctypes.c_void_p(val.data_ptr()),
-                                _IDX64, _IDX32, _BASE0, _CUDA_R_64F), "cusparseCreateCsr")
+                                idx, idx, _BASE0, _CUDA_R_64F), "cusparseCreateCsr")
     return m
 
 
@@ -82,10 +93,9 @@ class SpMV:
         import torch
         self.h = handle
         n = len(row_ptr) - 1
-        self.rp = torch.from_numpy(np.asarray(row_ptr, dtype=np.int64)).cuda()
-        self.col = torch.from_numpy(np.asarray(col_idx, dtype=np.int32)).cuda()
+        self.rp, self.col, idx = _index_arrays(row_ptr, col_idx)
         self.val = torch.from_numpy(np.asarray(values, dtype=np.float64)).cuda()
-        self.A = _csr(n, len(values), self.rp, self.col, self.val)
+        self.A = _csr(n, len(values), self.rp, self.col, self.val, idx)
         self.vx, self.vy = _dn(x), _dn(y)
         self.alg = SPMV_ALGS[alg]
         self.one, self.zero = ctypes.c_double(1.0), ctypes.c_double(0.0)
@@ -115,10 +125,9 @@ class Ic0Apply:
         import torch
         self.h = handle
         n = len(row_ptr) - 1
-        self.rp = torch.from_numpy(np.asarray(row_ptr, dtype=np.int64)).cuda()
-        self.col = torch.from_numpy(np.asarray(col_idx, dtype=np.int32)).cuda()
+        self.rp, self.col, idx = _index_arrays(row_ptr, col_idx)
         self.val = torch.from_numpy(np.asarray(values, dtype=np.float64)).cuda()
-        self.L = _csr(n, len(values), self.rp, self.col, self.val)
+        self.L = _csr(n, len(values), self.rp, self.col, self.val, idx)
         fill, diag = ctypes.c_int(_LOWER), ctypes.c_int(_NON_UNIT)
         _ck(lib().cusparseSpMatSetAttribute(self.L, _FILL, ctypes.byref(fill), 4), "fill")
         _ck(lib().cusparseSpMatSetAttribute(self.L, _DIAG, ctypes.byref(diag), 4), "diag")
@@ -155,7 +164,7 @@ def vendor_block(a, f, x_dev, timer, flush=None):
     from paper_1311_1695_b200 import _device as dev
     h = Handle(torch.cuda.current_stream().cuda_stream)
     out = {"library": f"cuSPARSE (libcusparse {os.path.basename(lib()._name)})",
-           "spmv": {}, "format": "CSR int64 row offsets / int32 columns / f64 values"}
+           "spmv": {}, "format": "CSR int32 row offsets and columns (int64 when nnz >= 2^31), f64 values"}
     d = a.device()
     y_ours = dev.empty(a.n)
     d.matvec(x_dev, y_ours)
