@@ -166,6 +166,10 @@ int lg_spmv_acc(const lg_csr* a, const double* x, double* y, lg_ws* ws, const in
                 void* stream);
 /* Stream row pointers (packed: off-diagonal; plain: row_ptr), n + 1 int64. */
 int lg_csr_row_ptr(const lg_csr* a, int64_t* host_out);
+/* Host CSR (row_ptr [n+1], col / val [nnz], diagonal in sorted position) of
+ * any matrix, device-only packed ones included (C5's device-built Laplacian):
+ * the input of the host IC(0) factorization (ic0.py:48-116). */
+int lg_csr_export_host(const lg_csr* a, int64_t* rp_h, int64_t* col_h, double* val_h);
 /* Unit-weight Laplacian of a canonical device edge list, built directly in
  * the packed SpMV format on the device (no host copy of the matrix). */
 int lg_csr_laplacian_device(int64_t n, int64_t m, const int32_t* d_i,

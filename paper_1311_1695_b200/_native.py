@@ -116,6 +116,7 @@ _SIGS = {
     "lg_fused": (c_int, [c_p, c_p, c_p]),
     "lg_csr_row_block": (c_int, [c_p, c_i64, c_i64, c_p]),
     "lg_csr_row_ptr": (c_int, [c_p, c_p]),
+    "lg_csr_export_host": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_csr_split_cols": (c_int, [c_p, c_i64, c_i64, c_p, c_p]),
     "lg_csr_col_panel": (c_int, [c_p, c_i64, c_i64, c_int, c_p]),
     "lg_csr_set_panels": (c_int, [c_p, c_int]),

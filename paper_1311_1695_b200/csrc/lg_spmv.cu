@@ -2008,6 +2008,50 @@ extern "C" {
 // Stream row pointers of a matrix (packed: off-diagonal row pointers; plain:
 // row_ptr) to the host, n + 1 entries -- what the nnz-balanced row
 // partition of a device-only matrix is computed from.
+// Host CSR of a packed matrix (also device-only ones, e.g. C5's device-built
+// Laplacian): row pointers, columns and values with the diagonal in its
+// sorted position -- what the host IC(0) factorization (ic0.py:48-116)
+// consumes.  rp_h [n+1], col_h / val_h [noff + n] (every packed row stores
+// its diagonal).
+extern "C" int lg_csr_export_host(const lg_csr* a, int64_t* rp_h, int64_t* col_h,
+                                  double* val_h) {
+  if (!a || !rp_h || !col_h || !val_h) return fail(LG_EINVAL, "lg_csr_export_host: bad argument");
+  if (!a->packed) return lg_csr_download(a, rp_h, col_h, val_h);
+  const int64_t n = a->n;
+  std::vector<int64_t> prp((size_t)n + 1);
+  std::vector<uint32_t> pcol((size_t)a->noff);
+  std::vector<double> diag((size_t)n), table((size_t)std::max(a->nvals, 1));
+  LG_CUDA(cudaMemcpy(prp.data(), a->prp, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost));
+  if (a->noff)
+    LG_CUDA(cudaMemcpy(pcol.data(), a->pcol, 4 * (size_t)a->noff, cudaMemcpyDeviceToHost));
+  LG_CUDA(cudaMemcpy(diag.data(), a->pdiag, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+  if (a->nvals)
+    LG_CUDA(cudaMemcpy(table.data(), a->table, 8 * (size_t)a->nvals, cudaMemcpyDeviceToHost));
+  const uint32_t cmask = (a->cbits >= 32) ? 0xffffffffu : ((1u << a->cbits) - 1u);
+  int64_t o = 0;
+  rp_h[0] = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    bool placed = false;
+    for (int64_t k = prp[(size_t)r]; k < prp[(size_t)r + 1]; ++k) {
+      const uint32_t w = pcol[(size_t)k];
+      const int64_t c = w & cmask;
+      if (!placed && c > r) {
+        col_h[o] = r;
+        val_h[o++] = diag[(size_t)r];
+        placed = true;
+      }
+      col_h[o] = c;
+      val_h[o++] = table[(size_t)(w >> a->cbits)];
+    }
+    if (!placed) {
+      col_h[o] = r;
+      val_h[o++] = diag[(size_t)r];
+    }
+    rp_h[r + 1] = o;
+  }
+  return LG_OK;
+}
+
 extern "C" int lg_csr_row_ptr(const lg_csr* a, int64_t* host_out) {
   if (!a || !host_out) return fail(LG_EINVAL, "lg_csr_row_ptr: bad argument");
   LG_CUDA(cudaMemcpy(host_out, a->packed ? a->prp : a->row_ptr, 8 * (size_t)(a->n + 1),

@@ -10,9 +10,15 @@ name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 a = L.build_laplacian(L.config_graph(name))
 f = L.ic0_factorize_multicolor(a) if "--mc" in sys.argv else L.ic0_factorize(a)
 with dev.solver_stream() as st:
+    k = int(sys.argv[sys.argv.index("--k") + 1]) if "--k" in sys.argv else 1
     pl = _DacgPlan(a, f, a.n, 11)
-    pl.C[0] = 1.0 / np.sqrt(a.n)
-    pl.k = 1
+    # deflation basis: the kernel vector plus k - 1 orthonormal columns
+    # (a mid-solve iteration: k - 1 pairs already locked)
+    Qm = np.linalg.qr(np.column_stack([np.ones(a.n)] + [np.random.default_rng(j).standard_normal(a.n)
+                                                        for j in range(k - 1)]))[0]
+    for j in range(k):
+        pl.C[j] = torch.from_numpy(np.ascontiguousarray(Qm[:, j])).cuda()
+    pl.k = k
     x = dev.to_device(np.random.default_rng(0).standard_normal(a.n))
     pl.X[0].copy_(x / x.norm()); pl.X[1].copy_(pl.X[0])
     Spmv(pl.csr, pl.X[0], pl.AX[0])(); pl.AX[1].copy_(pl.AX[0])
