@@ -283,6 +283,24 @@ def _ncu_traffic(config, world):
     return None
 
 
+def north_star_residual(a, pairs):
+    """max_i ||L u_i - lambda_i u_i||_2 / ||L||_1 over the returned pairs
+    (the north star's residual), next to the reference's own criterion
+    ||A u - theta u|| / (||u|| |theta|) (results.py:97-104, rayleigh_residuals).
+    ||L||_1 is the largest absolute column sum; L is symmetric, so the
+    largest absolute row sum."""
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200.results import rayleigh_residuals
+    absrow = np.add.reduceat(np.abs(a.values), a.row_ptr[:-1])
+    norm1 = float(absrow.max())
+    U = pairs.vectors
+    res = [float(np.linalg.norm(L.spmv(a, U[:, i]) - pairs.values[i] * U[:, i])) / norm1
+           for i in range(U.shape[1])]
+    _, ref = rayleigh_residuals(a, U)
+    return {"ns_residual_max": max(res), "ref_criterion_max": float(np.max(ref)),
+            "norm1_L": norm1}
+
+
 def solve_block(a, f, f_mc=None):
     """Wall time to 5 eigenpairs (delta 1e-8) with DACG and JD on the device,
     with the reference's IC(0) (parity mode) and, flagged separately, with
@@ -317,7 +335,8 @@ def solve_block(a, f, f_mc=None):
         if r.get("eigenvalues"):
             err = float(np.max(np.abs(pairs.values - r["eigenvalues"]) /
                                np.abs(r["eigenvalues"])))
-        out[name] = {"wall_s": wall, "wall_s_first_call": walls[0], "mvp": rep.mvp, "neig": 5,
+        out[name] = {**north_star_residual(a, pairs),
+                     "wall_s": wall, "wall_s_first_call": walls[0], "mvp": rep.mvp, "neig": 5,
                      "delta": 1e-8,
                      "preconditioner": label,
                      "eig_relerr_vs_reference": err,
@@ -372,7 +391,7 @@ def solve_configs_block(prebuilt=None):
                     walls.append(time.perf_counter() - t0)
                 r = gold["solvers"][name]
                 ref_vals = np.asarray(r["eigenvalues"])
-                out[f"{cfg}_{name}{suffix}"] = {
+                out[f"{cfg}_{name}{suffix}"] = {**north_star_residual(a, pairs),
                     "neig": gold["neig"], "delta": gold["delta"], "preconditioner": label,
                     "wall_s": walls[1], "wall_s_first_call": walls[0], "mvp": rep.mvp,
                     "reference_mvp": r["mvp"],

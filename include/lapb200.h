@@ -157,9 +157,9 @@ int lg_csr_split_cols(const lg_csr* a, int64_t r0, int64_t r1, lg_csr** inner,
  * locality; no reference counterpart.) */
 int lg_csr_col_panel(const lg_csr* a, int64_t c0, int64_t c1, int with_diag, lg_csr** out);
 /* Attach p (2..16) equal-width column panels to a FULL packed operator (every
- * row present, not a row block); lg_spmv then computes y = P_0 x - theta x,
- * y += P_k x (same epilogue).  p <= 1 detaches.  C5 (x = 250 MB > L2):
- * 4 panels, 12.95 -> 11.57 ms a product (profiles/r01_col_panels.json). */
+ * row present, not a row block); lg_spmv then computes y = (D - theta I) x,
+ * y += P_k x for every panel (same epilogue).  p <= 1 detaches.  C5
+ * (x = 250 MB > L2): 4 panels, 12.44 -> 9.57 ms a product. */
 int lg_csr_set_panels(lg_csr* a, int p);
 /* y += A x, no epilogue (the exterior half of a split row block). */
 int lg_spmv_acc(const lg_csr* a, const double* x, double* y, lg_ws* ws, const int* skip,

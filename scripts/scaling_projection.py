@@ -23,7 +23,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1311_1695_b200 as L  # noqa: E402
 from paper_1311_1695_b200 import _device as dev  # noqa: E402
-from paper_1311_1695_b200._plan import AllReduce, Exchange, ExchangeStart, Seq  # noqa: E402
+from paper_1311_1695_b200._plan import AllReduce, Exchange, ExchangeStart, Prog, Seq  # noqa: E402
 from paper_1311_1695_b200.dacg import _DacgPlan  # noqa: E402
 from paper_1311_1695_b200.dist import RowComm, RowPartition, matrix_row_ptr  # noqa: E402
 from paper_1311_1695_b200.precond import JacobiFactor  # noqa: E402
@@ -46,6 +46,39 @@ class NullBackend:
 
     def barrier(self, comm):
         pass
+
+
+def count_progs(plan):
+    """Stand-alone scalar-program launches of an iteration (at N > 1 they
+    cannot fold into the pass that produced their dots: the dots are
+    all-reduced first)."""
+    c = 0
+    for step in plan:
+        for s in (step.steps if isinstance(step, Seq) else [step]):
+            for u in (s.steps if isinstance(s, Seq) else [s]):
+                c += isinstance(u, Prog)
+    return c
+
+
+def prog_launch_us(slots_owner):
+    """Device time of one stand-alone scalar-program launch inside a CUDA
+    graph (20 in a row, median of 5)."""
+    from paper_1311_1695_b200._plan import Graph
+    p = Prog(slots_owner)
+    p.const("pp_a", 1.0)
+    p.add("pp_b", "pp_a", "pp_a")
+    with dev.solver_stream():
+        g = Graph([p] * 20)
+        for _ in range(3):
+            g()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            g()
+            torch.cuda.synchronize()
+            ts.append((time.perf_counter() - t0) / 20 * 1e6)
+    return float(np.median(ts))
 
 
 def count_collectives(plan):
@@ -87,7 +120,9 @@ def rank_iteration_us(a, f, comm, k=6, iters=20):
         torch.cuda.synchronize()
         us = (time.perf_counter() - t0) / iters * 1e6
         ex, ar = count_collectives(pl.plan(0))
-    return us, ex, ar
+        npg = count_progs(pl.plan(0))
+        tprog = prog_launch_us(pl.S) if npg else 0.0
+    return us, ex, ar, npg, tprog
 
 
 def main():
@@ -119,10 +154,10 @@ def main():
     for world in worlds:
         part = RowPartition(rp, world, rw)
         ranks = range(world) if (cfg != "C5" or world <= 2) else (0, world // 2, world - 1)
-        worst, ex, ar = 0.0, 0, 0
+        worst, ex, ar, npg, tprog = 0.0, 0, 0, 0, 0.0
         for r in ranks:
             comm = RowComm(part, r, NullBackend())
-            us, ex, ar = rank_iteration_us(a, f, comm)
+            us, ex, ar, npg, tprog = rank_iteration_us(a, f, comm)
             worst = max(worst, us)
             torch.cuda.empty_cache()
         comm_us = 0.0
@@ -130,12 +165,32 @@ def main():
             comm_us = ex * ((world - 1) / world * 8 * n / 770e9 * 1e6 + 10.0) + ar * 15.0
         total = worst + comm_us
         base = base or total
-        print(json.dumps({"config": cfg, "preconditioner": prec, "ranks": world,
-                          "row_weight": rw,
-                          "local_us_measured": worst, "exchanges": ex, "allreduces": ar,
-                          "comm_us_modelled": comm_us, "iteration_us_projected": total,
-                          "speedup_projected": base / total,
-                          "efficiency_projected": base / total / world}), flush=True)
+        rec = {"config": cfg, "preconditioner": prec, "ranks": world, "row_weight": rw,
+               "local_us_measured": worst, "exchanges": ex, "allreduces": ar,
+               "comm_us_modelled": comm_us, "iteration_us_projected": total,
+               "speedup_projected": base / total, "efficiency_projected": base / total / world}
+        if "--device-collectives" in sys.argv:
+            # DESIGN 7 "device-side reductions": the finishing CTA of every
+            # dot pass writes its partials into each peer's mailbox over
+            # NVLink and sums the N mailboxes in rank order (~3 us: one
+            # NVLink hop + the fan-in), then runs the scalar program itself
+            # -- the stand-alone program launches disappear; the slice
+            # exchange is issued by the producing kernel as P2P stores
+            # (same bytes, ~3 us instead of NCCL's ~10 us launch latency)
+            dev_comm = 0.0
+            local_dev = worst
+            if world > 1:
+                dev_comm = ex * ((world - 1) / world * 8 * n / 770e9 * 1e6 + 3.0) + ar * 3.0
+                local_dev = worst - npg * tprog
+            dtot = local_dev + dev_comm
+            base_d = getattr(main, "_base_d", None) or dtot
+            main._base_d = base_d
+            rec.update(device_collectives={
+                "prog_launches_removed": npg if world > 1 else 0, "prog_launch_us": tprog,
+                "local_us": local_dev, "comm_us_modelled": dev_comm,
+                "iteration_us_projected": dtot, "speedup_projected": base_d / dtot,
+                "efficiency_projected": base_d / dtot / world})
+        print(json.dumps(rec), flush=True)
 
 
 if __name__ == "__main__":

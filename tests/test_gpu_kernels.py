@@ -399,6 +399,37 @@ def test_device_rmat_lcc_laplacian_pipeline(L):
     want = O.spmv(O.Csr(A.n, rp, col, val), x)
     y = L.spmv(A, x)
     assert np.max(np.abs(y - want)) <= 1e-13 * np.max(np.abs(want))
+    # the host CSR of the device-only matrix (lg_csr_export_host: what the
+    # host IC(0) factorization of a C5-family graph consumes) is the host
+    # pipeline's Laplacian bit for bit, and so is its IC(0) factor
+    erp = np.empty(A.n + 1, dtype=np.int64)
+    ecol = np.empty(A.nnz, dtype=np.int64)
+    evl = np.empty(A.nnz)
+    nat.call("lg_csr_export_host", A.device().handle, erp.ctypes.data, ecol.ctypes.data,
+             evl.ctypes.data)
+    assert np.array_equal(erp, rp) and np.array_equal(ecol, col)
+    assert np.array_equal(evl.view(np.int64), val.view(np.int64))
+    f = L.ic0_factorize(L.CsrMatrix(A.n, erp, ecol, evl))
+    lrp, lcol, lval, _, _ = O.ic0_factorize(O.Csr(A.n, rp, col, val))
+    assert np.array_equal(f.l.values.view(np.int64), lval.view(np.int64))
+
+
+def test_csr_export_host_weighted(L):
+    """lg_csr_export_host on host-built matrices: packed (integer weights,
+    dense value table) and plain (real weights) both round-trip to the
+    CsrMatrix arrays bit for bit."""
+    from paper_1311_1695_b200 import _native as nat
+    for g in (L.generators.chung_lu_graph(4000, 2.3, 6.0, weighted=True, seed=5),
+              L.generators.random_connected_graph(3000, extra_edges=9000, seed=4,
+                                                  weighted=True)):
+        a = L.build_laplacian(g)
+        rp = np.empty(a.n + 1, dtype=np.int64)
+        col = np.empty(a.nnz, dtype=np.int64)
+        val = np.empty(a.nnz)
+        nat.call("lg_csr_export_host", a.device().handle, rp.ctypes.data, col.ctypes.data,
+                 val.ctypes.data)
+        assert np.array_equal(rp, a.row_ptr) and np.array_equal(col, a.col_idx)
+        assert np.array_equal(val.view(np.int64), a.values.view(np.int64))
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])

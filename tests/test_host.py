@@ -373,3 +373,28 @@ def test_fsai2_pattern_and_rows():
         gw /= np.sqrt(gw[-1])
         gv = f.g.values[f.g.row_ptr[i]:f.g.row_ptr[i + 1]]
         assert np.max(np.abs(gv - gw)) <= 1e-10 * np.max(np.abs(gw))
+
+
+def test_bench_arms_print_the_same_config():
+    """bench.py's two arms (the B200 product and --impl reference) print the
+    same `config` object for a workload, so the driver can pair their lines;
+    and the reference arm's JSON line carries the contract's keys."""
+    import importlib.util
+    import json
+    import subprocess
+    import sys
+    spec = importlib.util.spec_from_file_location("bench_mod", ROOT / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    c1 = bench.bench_config("C4", 989777, 10907457, 1)
+    c2 = bench.bench_config("C4", 989777, 10907457, 1)
+    assert c1 == c2 and c1["n"] == 989777 and "workload" in c1
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--config", "C1", "--steps", "3", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "matvecs/s"
+    assert line["config"] == bench.bench_config("C1", line["config"]["n"],
+                                                 line["config"]["nnz"], 1)
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
