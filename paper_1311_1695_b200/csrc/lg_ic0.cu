@@ -34,6 +34,8 @@
 #include <cstring>
 #include <vector>
 
+#include <omp.h>
+
 #include "lg_common.cuh"
 
 namespace lg {
@@ -121,54 +123,90 @@ namespace lg {
 // lval receives the factor.
 #pragma GCC push_options
 #pragma GCC optimize("fp-contract=off")
+// Row i of the factor, given rows < i (ic0.py:56-78): for each lower entry
+// k of row i (ascending), s = a_ik - sum_p l_ip l_kp over the common pattern
+// in ascending p, l_ik = s / l_kk; then l_ii = sqrt(diag (1 + alpha) -
+// sum_k l_ik^2).  The common p are enumerated in ascending order whichever
+// row is walked (the shorter one; p looked up in the other by binary search
+// or a linear advance), so the arithmetic -- hence every bit -- is the
+// reference's.  Returns false on a pivot below the floor.
+static inline bool ic0_row(int64_t i, const std::vector<double>& diag,
+                           const std::vector<int64_t>& lrp, const std::vector<int64_t>& lcol,
+                           const std::vector<double>& aval, double alpha,
+                           std::vector<double>& lval, int64_t* stamp, int64_t* pos) {
+  const double floor_ = 1e-14;  // _PIVOT_FLOOR, ic0.py:17
+  const int64_t lo = lrp[i], hi = lrp[i + 1] - 1;  // hi: diagonal slot
+  const int64_t* C = lcol.data();
+  for (int64_t t = lo; t < hi; ++t) {
+    stamp[C[t]] = i;
+    pos[C[t]] = t;
+  }
+  for (int64_t t = lo; t < hi; ++t) {
+    const int64_t k = C[t];
+    double s = aval[t];
+    const int64_t klo = lrp[k], khi = lrp[k + 1] - 1;  // row k strictly lower
+    const int64_t nli = t - lo, nk = khi - klo;
+    if (nli <= nk) {
+      // walk the computed prefix of row i (ascending p), find p in row k
+      int64_t q = klo;
+      for (int64_t u = lo; u < t; ++u) {
+        const int64_t p = C[u];
+        if (nk > 32) q = std::lower_bound(C + q, C + khi, p) - C;
+        else
+          while (q < khi && C[q] < p) ++q;
+        if (q < khi && C[q] == p) s -= lval[u] * lval[q];
+      }
+    } else {
+      // walk row k (ascending p), look p up in row i's computed prefix
+      // (stamp / pos: this thread's map of row i's columns)
+      for (int64_t q = klo; q < khi; ++q) {
+        const int64_t p = C[q];
+        if (stamp[p] == i && pos[p] < t) s -= lval[pos[p]] * lval[q];
+      }
+    }
+    lval[t] = s / lval[khi];
+  }
+  const double scaled = diag[i] * (1.0 + alpha);
+  double d = scaled;
+  for (int64_t t = lo; t < hi; ++t) d -= lval[t] * lval[t];
+  if (d <= floor_ * std::fabs(scaled) || d <= 0.0) return false;
+  lval[hi] = std::sqrt(d);
+  return true;
+}
+
+// One no-fill factorization pass (ic0.py:48-78).  Returns true on success.
+// lrp/lcol describe the lower pattern of A plus the diagonal (last per row);
+// lval receives the factor.  Rows of one dependency level (rows whose lower
+// neighbours all sit in earlier levels) are independent, so a level's rows
+// are factored in parallel (OpenMP) -- every row still reads exactly the
+// finished rows it reads in the sequential order, so the factor is the same
+// bit for bit.  order / lstart: rows grouped by level.
 static bool ic0_attempt(int64_t n, const std::vector<double>& diag,
                         const std::vector<int64_t>& lrp,
                         const std::vector<int64_t>& lcol,
                         const std::vector<double>& aval, double alpha,
-                        std::vector<double>& lval, std::vector<int64_t>& stamp,
-                        std::vector<int64_t>& pos) {
-  std::fill(stamp.begin(), stamp.end(), (int64_t)-1);
-  const double floor_ = 1e-14;  // _PIVOT_FLOOR, ic0.py:17
-  for (int64_t i = 0; i < n; ++i) {
-    const int64_t lo = lrp[i], hi = lrp[i + 1] - 1;  // hi: diagonal slot
-    for (int64_t t = lo; t < hi; ++t) {
-      stamp[lcol[t]] = i;
-      pos[lcol[t]] = t;
-    }
-    for (int64_t t = lo; t < hi; ++t) {
-      const int64_t k = lcol[t];
-      double s = aval[t];
-      const int64_t klo = lrp[k], khi = lrp[k + 1] - 1;  // row k strictly lower
-      const int64_t nli = t - lo, nk = khi - klo;
-      if (nli <= nk) {
-        // iterate the computed prefix of row i (ascending p), look p up in row k
-        int64_t q = klo;
-        for (int64_t u = lo; u < t; ++u) {
-          const int64_t p = lcol[u];
-          // row k columns ascending: advance (galloping is unnecessary here)
-          if (nk > 32) {
-            const int64_t* b = lcol.data() + q;
-            const int64_t* e = lcol.data() + khi;
-            const int64_t* f = std::lower_bound(b, e, p);
-            q = f - lcol.data();
-          } else {
-            while (q < khi && lcol[q] < p) ++q;
-          }
-          if (q < khi && lcol[q] == p) s -= lval[u] * lval[q];
-        }
-      } else {
-        for (int64_t q = klo; q < khi; ++q) {
-          const int64_t p = lcol[q];
-          if (stamp[p] == i && pos[p] < t) s -= lval[pos[p]] * lval[q];
-        }
+                        std::vector<double>& lval, const std::vector<int64_t>& order,
+                        const std::vector<int64_t>& lstart,
+                        std::vector<std::vector<int64_t>>& maps) {
+  const int64_t nlev = (int64_t)lstart.size() - 1;
+  for (auto& m : maps) std::fill(m.begin(), m.end(), (int64_t)-1);
+  for (int64_t L = 0; L < nlev; ++L) {
+    const int64_t a = lstart[(size_t)L], b = lstart[(size_t)L + 1];
+    int ok = 1;
+    if (b - a >= 64 && maps.size() > 1) {
+#pragma omp parallel num_threads((int)maps.size()) reduction(min : ok)
+      {
+        int64_t* st = maps[(size_t)omp_get_thread_num()].data();
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t q = a; q < b; ++q)
+          if (!ic0_row(order[(size_t)q], diag, lrp, lcol, aval, alpha, lval, st, st + n)) ok = 0;
       }
-      lval[t] = s / lval[khi];
+    } else {
+      int64_t* st = maps[0].data();
+      for (int64_t q = a; q < b && ok; ++q)
+        if (!ic0_row(order[(size_t)q], diag, lrp, lcol, aval, alpha, lval, st, st + n)) ok = 0;
     }
-    const double scaled = diag[i] * (1.0 + alpha);
-    double d = scaled;
-    for (int64_t t = lo; t < hi; ++t) d -= lval[t] * lval[t];
-    if (d <= floor_ * std::fabs(scaled) || d <= 0.0) return false;
-    lval[hi] = std::sqrt(d);
+    if (!ok) return false;
   }
   return true;
 }
@@ -1337,11 +1375,32 @@ int lg_ic0_factorize(int64_t n, const int64_t* rp, const int64_t* col,
   const double last = 0.1 * dmax;
   if (dmax > 0 && (shifts.empty() || last > shifts.back())) shifts.push_back(last);
   std::vector<double> lval((size_t)nl, 0.0);
-  std::vector<int64_t> stamp((size_t)n), pos((size_t)n);
+  // dependency levels of the lower pattern, rows grouped by level
+  std::vector<int64_t> order((size_t)n), lstart;
+  {
+    std::vector<int32_t> lev((size_t)n, 0);
+    int32_t maxl = -1;
+    for (int64_t i = 0; i < n; ++i) {
+      int32_t l = 0;
+      for (int64_t t = lrp[(size_t)i]; t < lrp[(size_t)i + 1] - 1; ++t)
+        l = std::max(l, lev[(size_t)lcol[(size_t)t]] + 1);
+      lev[(size_t)i] = l;
+      maxl = std::max(maxl, l);
+    }
+    lstart.assign((size_t)maxl + 2, 0);
+    for (int64_t i = 0; i < n; ++i) lstart[(size_t)lev[(size_t)i] + 1]++;
+    for (int32_t l = 0; l <= maxl; ++l) lstart[(size_t)l + 1] += lstart[(size_t)l];
+    std::vector<int64_t> fill(lstart.begin(), lstart.end() - 1);
+    for (int64_t i = 0; i < n; ++i) order[(size_t)fill[(size_t)lev[(size_t)i]]++] = i;
+  }
+  // per-thread column maps of the row being factored (stamp | pos, 16 B a
+  // node each): 16 threads x 0.5 GB at C5 size
+  const int nthr = std::max(1, std::min(omp_get_max_threads(), 64));
+  std::vector<std::vector<int64_t>> maps((size_t)nthr, std::vector<int64_t>(2 * (size_t)n));
   int tries = 0;
   for (double alpha : shifts) {
     ++tries;
-    if (ic0_attempt(n, diag, lrp, lcol, aval, alpha, lval, stamp, pos)) {
+    if (ic0_attempt(n, diag, lrp, lcol, aval, alpha, lval, order, lstart, maps)) {
       std::memcpy(l_rp, lrp.data(), sizeof(int64_t) * (size_t)(n + 1));
       std::memcpy(l_col, lcol.data(), sizeof(int64_t) * (size_t)nl);
       std::memcpy(l_val, lval.data(), sizeof(double) * (size_t)nl);

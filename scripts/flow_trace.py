@@ -10,7 +10,11 @@ sys.path.insert(0, ".")
 import paper_1311_1695_b200 as L
 from paper_1311_1695_b200 import _device as dev, _native as nat
 for name in [x for x in sys.argv[1:] if not x.startswith("--")] or ["C3"]:
-    a = L.build_laplacian(L.config_graph(name))
+    if name.startswith("grid"):   # e.g. grid300: a hub-free 300 x 300 grid
+        k = int(name[4:])
+        a = L.build_laplacian(L.generators.grid_graph(k, k))
+    else:
+        a = L.build_laplacian(L.config_graph(name))
     f = L.ic0_factorize_multicolor(a) if "--mc" in sys.argv else L.ic0_factorize(a)
     d = f.device()
     lib = nat.load()
