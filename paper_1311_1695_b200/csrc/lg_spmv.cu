@@ -400,12 +400,34 @@ __global__ void __launch_bounds__(kWThreads, PACKED ? LG_SPMV_MINB : 3) wspmv_ke
       // open tails with a segmented scan, and a row ends at position j when
       // j is valid and position j + 1 starts a row or ends the block.
       const unsigned F = d.meta & vm & 0xffu;
-      double c[kWPer];
-      double run = 0.0;
+      // row ends: the next position (next lane's first for j = 7) starts a
+      // row, or j is the block's last position
+      const unsigned nf = __shfl_down_sync(0xffffffffu, F & 1u, 1);
+      const int last = (int)(d.nz1 - 1 - (d.nz0 & ~(int64_t)3)) - kWPer * lane;
+      unsigned E = vm & ((F >> 1) | ((lane < 31 ? nf : 0u) << (kWPer - 1)));
+      if (last >= 0 && last < kWPer) E |= 1u << last;
+      // positions before the lane's first row start continue a row from the
+      // lanes before (the head row: its sum needs their carry)
+      const unsigned before = F ? ((F & (0u - F)) - 1u) : 0xffu;
+      const int rfirst = (int)(d.meta >> 8);
+      const int fv = __ffs(vm) - 1;
+      // row of position j: rfirst + (row starts in (fv, j])
+      const unsigned fcount = F & ~(1u << (fv & 31));
+      double run = 0.0, headv = 0.0;
+      bool head_end = false;
 #pragma unroll
       for (int j = 0; j < kWPer; ++j) {
         run = (((F >> j) & 1u) ? 0.0 : run) + p[j];
-        c[j] = run;
+        if ((E >> j) & 1u) {
+          if ((before >> j) & 1u) {
+            headv = run;
+            head_end = true;
+          } else {
+            const int r = rfirst + __popc(fcount & ((2u << j) - 1u));
+            LG_CK(r >= 0 && r < d.nrows, "slot");
+            slot[r] = run;
+          }
+        }
       }
       // segmented inclusive scan of the lanes' open tails
       double v = run;
@@ -421,27 +443,7 @@ __global__ void __launch_bounds__(kWThreads, PACKED ? LG_SPMV_MINB : 3) wspmv_ke
       }
       double cprev = __shfl_up_sync(0xffffffffu, v, 1);
       if (lane == 0) cprev = 0.0;
-      // row ends: the next position (next lane's first for j = 7) starts a
-      // row, or j is the block's last position
-      const unsigned nf = __shfl_down_sync(0xffffffffu, F & 1u, 1);
-      const int last = (int)(d.nz1 - 1 - (d.nz0 & ~(int64_t)3)) - kWPer * lane;
-      unsigned E = vm & ((F >> 1) | ((lane < 31 ? nf : 0u) << (kWPer - 1)));
-      if (last >= 0 && last < kWPer) E |= 1u << last;
-      // positions before the lane's first row start continue a row from the
-      // lanes before: add their carry
-      const unsigned before = F ? ((F & (0u - F)) - 1u) : 0xffu;
-      const int rfirst = (int)(d.meta >> 8);
-      const int fv = __ffs(vm) - 1;
-      // row of position j: rfirst + (row starts in (fv, j])
-      const unsigned fcount = F & ~(1u << fv);
-#pragma unroll
-      for (int j = 0; j < kWPer; ++j) {
-        if ((E >> j) & 1u) {
-          const int r = rfirst + __popc(fcount & ((2u << j) - 1u));
-          LG_CK(r >= 0 && r < d.nrows, "slot");
-          slot[r] = ((before >> j) & 1u) ? cprev + c[j] : c[j];
-        }
-      }
+      if (head_end) slot[rfirst] = cprev + headv;
       __syncwarp();
       for (int i = lane; i < d.nrows; i += 32) finish_row<PACKED>(a, row0 + i, slot[i], theta);
       __syncwarp();

@@ -49,7 +49,7 @@ def rss_gb():
 scale = int(sys.argv[1])
 out = {"scale": scale, "edge_factor": 16}
 t0 = time.perf_counter()
-A = rmat_laplacian_device(scale, 16, seed=0, panels=False)
+A = rmat_laplacian_device(scale, 16, seed=0)
 torch.cuda.synchronize()
 out.update(n=A.n, nnz=A.nnz, build_s=round(time.perf_counter() - t0, 2))
 t0 = time.perf_counter()

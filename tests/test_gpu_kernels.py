@@ -409,7 +409,7 @@ def test_device_rmat_lcc_laplacian_pipeline(L):
              evl.ctypes.data)
     assert np.array_equal(erp, rp) and np.array_equal(ecol, col)
     assert np.array_equal(evl.view(np.int64), val.view(np.int64))
-    f = L.ic0_factorize(L.CsrMatrix(A.n, erp, ecol, evl))
+    f = L.ic0_factorize(L.CsrMatrix(A.n, erp, ecol, evl, symmetric=True))
     lrp, lcol, lval, _, _ = O.ic0_factorize(O.Csr(A.n, rp, col, val))
     assert np.array_equal(f.l.values.view(np.int64), lval.view(np.int64))
 
