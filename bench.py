@@ -575,6 +575,137 @@ def c5_block(peaks, steps=10, dist=None, world=1, rank=0, solve=True):
     return out
 
 
+def c5_main(args):
+    """`--config C5`: BASELINE configs[4] as a first-class bench line -- the
+    largest single-GPU configuration (R-MAT scale 26, 2.14e9 nonzeros,
+    device-built; the reference cannot build it).  A step is one matvec of
+    the panelled product; x (262 MB) exceeds L2, so nothing is flushed.  At
+    N > 1 each rank multiplies its nnz-balanced row block after the in-place
+    slice exchange (time = max over ranks)."""
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    peaks, peak_kind = _peaks()
+    A = rmat_laplacian_device(26, 16, seed=0, panels=(world == 1))
+    n = A.n
+    xh = np.random.default_rng(0).standard_normal(n)
+    x, y = dev.to_device(xh), dev.empty(n)
+    gather = None
+    if world > 1:
+        part = RowPartition(device_row_ptr(A.device()), world)
+        d = local_operator_device(A.device(), part, rank)
+        gather = _OverlappedProduct(dist, part, rank, d)
+    else:
+        d = A.device()
+
+    def step():
+        if gather is not None:
+            gather(x, y)
+        else:
+            d.matvec(x, y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    st = torch.cuda.current_stream()
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            e0[i].record(st)
+            step()
+            e1[i].record(st)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = float(np.mean([p.elapsed_time(q) for p, q in zip(e0, e1)]))
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    algo = 12 * A.nnz + 8 * (n + 1) + 16 * n
+    stream = d.stream_bytes
+    traffic = None
+    try:
+        tr = json.loads((ROOT / "profiles" / "spmv_traffic_c5.json").read_text())
+        traffic = float(tr["dram_bytes_per_product"]) if world == 1 else None
+    except Exception:
+        pass
+    launches_per_step = (1 + 2 * getattr(d, "npanels", 0)) if world == 1 and getattr(
+        d, "npanels", 0) > 1 else 2
+    line = {
+        "metric": METRIC, "value": 1e3 / ms, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (device-built R-MAT, counter-based RNG)",
+        "config": {"workload": "C5: one SpMV of the R-MAT scale 26 ef 16 Laplacian (BASELINE "
+                               "configs[4], LCC, unit weights)", "n": n, "nnz": A.nnz,
+                   "l2": "x (262 MB) and the 8.5 GB stream exceed L2; not flushed",
+                   "parallelism": f"rows{world}" if world > 1 else "single"},
+        "effective_gbs": algo / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": stream / (ms * 1e-3) / 1e9,
+                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": stream / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                     "traffic": traffic, "peak_kind": peak_kind, "bytes_per_launch": stream,
+                     "format": "packed Laplacian, 4 column panels (x slices L2-resident)"
+                               if world == 1 else "packed row block",
+                     "bytes_model": "diag init 24 n + per panel: 4 B / off-diagonal + 96 B / "
+                                    "warp block + 8 B / column of its x slice + 20 B / row "
+                                    "written (y read-modify-write, row map)"},
+        "gpu_launches": args.steps * launches_per_step,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        reps = 3
+        L.spmv(A, xh)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            L.spmv(A, xh)
+        line["e2e"] = {"value": reps / (time.perf_counter() - t0), "unit": UNIT,
+                       "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                       "path": "paper_1311_1695_b200.spmv(A, numpy x) -> numpy y"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the reference's SpMV on a bounded sample: the host CSR (exported
+        # from the device, bit-exact) restricted to the first 1/64 of the
+        # nonzeros, one host core, scaled to a whole matvec
+        from oracle import lapeig_oracle as O
+        from paper_1311_1695_b200 import _native as nat
+        rp = np.empty(n + 1, dtype=np.int64)
+        col = np.empty(A.nnz, dtype=np.int64)
+        val = np.empty(A.nnz)
+        nat.call("lg_csr_export_host", d.handle, rp.ctypes.data, col.ctypes.data, val.ctypes.data)
+        r1 = int(np.searchsorted(rp, A.nnz // 64))
+        sub = O.Csr(r1, rp[:r1 + 1].copy(), col[:rp[r1]], val[:rp[r1]])
+        sub.n = n   # columns index all of x
+        O.spmv(sub, xh)
+        t0 = time.perf_counter()
+        O.spmv(sub, xh)
+        dt = (time.perf_counter() - t0) * A.nnz / max(1, int(rp[r1]))
+        line["cpu_baseline"] = {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"oracle reduceat SpMV over the first {r1} rows "
+                                          f"({int(rp[r1])} nonzeros, 1/64 of the matrix), "
+                                          "one host core, scaled to a whole matvec"}
+        del rp, col, val, sub
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -590,6 +721,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return reference_arm(args)
+    if args.config == "C5":
+        return c5_main(args)
 
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))

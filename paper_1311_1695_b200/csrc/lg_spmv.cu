@@ -127,6 +127,7 @@ struct lg_csr {
   // compacted schedule (an operator whose rows with entries are scattered,
   // e.g. a column panel): schedule row i is matrix row rowmap[i]
   int32_t* rowmap = nullptr;       // device [rows with entries] or NULL
+  int64_t nrows_sched = 0;         // rows the schedule writes (present rows)
   // columns a column panel reads (x[pf_c0:pf_c1] is what it prefetches)
   int64_t pf_c0 = 0, pf_c1 = 0;
 };
@@ -615,6 +616,11 @@ static int attach_schedule(lg_csr* a, const int64_t* rp, const std::vector<char>
       if (!map.empty()) crp.push_back(rp[map.back() + 1]);
     }
   }
+  a->nrows_sched = a->n;
+  if (absent) {
+    a->nrows_sched = 0;
+    for (int64_t r = 0; r < a->n; ++r) a->nrows_sched += !(*absent)[(size_t)r];
+  }
   if (!map.empty()) {
     const int64_t nc = (int64_t)map.size();
     build_schedule(nc, crp.data(), blocks, lnp, lfirst, lrow, nullptr);
@@ -1002,6 +1008,18 @@ int lg_csr_info(const lg_csr* a, int64_t* n, int64_t* nnz, int64_t* nblocks,
     const int64_t sched = (int64_t)sizeof(SpmvBlock) * a->nblocks;
     *stream_bytes = a->packed ? 4 * a->noff + sched + 8 * a->n + 16 * a->n
                               : 12 * a->nnz + sched + 16 * a->n;
+    if (a->npanels > 1) {
+      // panelled product: the (d - theta) x init pass, then per panel its
+      // words and schedule, its slice of x, y read-modify-write and the row
+      // map of the rows it writes
+      int64_t b = 24 * a->n;
+      for (int k = 0; k < a->npanels; ++k) {
+        const lg_csr* m = a->panel[k];
+        b += 4 * m->noff + (int64_t)sizeof(SpmvBlock) * m->nblocks +
+             8 * (m->pf_c1 - m->pf_c0) + m->nrows_sched * (16 + (m->rowmap ? 4 : 0));
+      }
+      *stream_bytes = b;
+    }
   }
   return LG_OK;
 }
