@@ -61,7 +61,7 @@ constexpr int kST = 128;                 // CTA size of the build kernels
 // entries, so a lane's two 128-bit loads never leave the allocation
 constexpr int64_t kStreamPad = 8;
 
-enum : int32_t { kBlkLong = -1, kBlkSeg = 0, kBlkRows = 1, kBlkNone = 7 };
+enum : int32_t { kBlkLong = -1, kBlkSeg = 0, kBlkRows = 1 };
 
 // -DLG_SPMV_CHECK: bounds-check every index the SpMV kernel uses (debug)
 #ifdef LG_SPMV_CHECK
@@ -199,30 +199,6 @@ __device__ __forceinline__ void wload(const SpmvArgs& a, int64_t p, WWords<PACKE
       const double2 v1 = __ldcs(reinterpret_cast<const double2*>(a.val + q + 2));
       L.v[4 * h] = v0.x; L.v[4 * h + 1] = v0.y; L.v[4 * h + 2] = v1.x; L.v[4 * h + 3] = v1.y;
     }
-  }
-}
-
-// x values of the valid positions (vm bit j) of one lane's window
-template <bool PACKED>
-__device__ __forceinline__ void wgather(const SpmvArgs& a, const WWords<PACKED>& L, unsigned vm,
-                                        uint32_t cmask, double (&xv)[kWPer]) {
-#pragma unroll
-  for (int j = 0; j < kWPer; ++j) {
-    const uint32_t c = PACKED ? (L.w[j] & cmask) : L.w[j];
-    xv[j] = ((vm >> j) & 1u) ? __ldg(a.x + c) : 0.0;
-  }
-}
-
-template <bool PACKED>
-__device__ __forceinline__ void wmul(const SpmvArgs& a, const WWords<PACKED>& L, unsigned vm,
-                                     const double* tab, const double (&xv)[kWPer],
-                                     double (&p)[kWPer]) {
-#pragma unroll
-  for (int j = 0; j < kWPer; ++j) {
-    if constexpr (PACKED)
-      p[j] = a.intw ? -(xv[j] * __uint2double_rn((L.w[j] >> a.cbits) + 1u))
-                    : xv[j] * tab[((vm >> j) & 1u) ? (L.w[j] >> a.cbits) : 0u];
-    else p[j] = ((vm >> j) & 1u) ? L.v[j] * xv[j] : 0.0;
   }
 }
 
@@ -488,105 +464,6 @@ __global__ void __launch_bounds__(kWThreads, PACKED ? LG_SPMV_MINB : 3) wspmv_ke
     d = dn;
     vm = vmn;
     W = Wn;
-  }
-}
-
-// Warp-specialised variant (LG_SPMV_WS=1): in each 1024-thread CTA (one per
-// SM) kWsG gather warps only load words, gather x and multiply, writing a
-// block's products into a double-buffered shared-memory slot, while kWsR
-// reduce warps fold / scan / finish the blocks the gather warps filled in
-// the previous phase (the same process_block code); one __syncthreads per
-// phase.  The gather warps never wait on a reduction, so the SM keeps more
-// gathers in flight (the loop is bound by outstanding x gathers).
-#ifndef LG_SPMV_WS_G
-#define LG_SPMV_WS_G 16   // gather warps per CTA
-#endif
-#ifndef LG_SPMV_WS_R
-#define LG_SPMV_WS_R 16   // reduce warps per CTA
-#endif
-constexpr int kWsG = LG_SPMV_WS_G, kWsR = LG_SPMV_WS_R, kWsThreads = 32 * (kWsG + kWsR);
-constexpr int kWsBlkWords = (int)(sizeof(SpmvBlock) / 4);
-constexpr int kWsTab = kMaxTable;   // doubles reserved for the value table
-constexpr size_t kWsSmem = sizeof(double) * ((size_t)kWsTab + 2 * kWsG * kWPer * 32 +
-                                             (size_t)kWsBlkWords * kWsG + kWsR * kWRows);
-
-template <bool PACKED>
-__global__ void __launch_bounds__(kWsThreads, 1) wspmv_ws_kernel(SpmvArgs a) {
-  if (a.skip && *a.skip) return;
-  // dynamic shared memory: value table | products (2 x kWsG blocks) | raw
-  // descriptors | the reduce warps' row slots
-  extern __shared__ double ws_sm[];
-  double* tab_sm = ws_sm;
-  auto prod = reinterpret_cast<double (*)[kWsG][kWPer][32]>(ws_sm + kWsTab);
-  auto dsm = reinterpret_cast<uint32_t (*)[kWsG][kWsBlkWords]>(ws_sm + kWsTab +
-                                                               2 * kWsG * kWPer * 32);
-  auto rsum = reinterpret_cast<double (*)[kWRows]>(ws_sm + kWsTab + 2 * kWsG * kWPer * 32 +
-                                                  kWsBlkWords * kWsG);
-  if constexpr (PACKED) {
-    for (int i = threadIdx.x; i < max(a.nvals, 1); i += kWsThreads)
-      tab_sm[i] = i < a.nvals ? a.table[i] : 0.0;
-  }
-  __syncthreads();
-  double theta = a.theta_h;
-  if (a.theta_d) theta += a.theta_neg ? -*a.theta_d : *a.theta_d;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t cmask = PACKED ? ((a.cbits >= 32) ? 0xffffffffu : ((1u << a.cbits) - 1u)) : 0u;
-  const int64_t per_phase = (int64_t)gridDim.x * kWsG;
-  const int64_t nphase = (a.nblocks + per_phase - 1) / per_phase;
-  if (warp < kWsG) {
-    // ---- gather warp: block b = phase * per_phase + blockIdx.x * kWsG + warp
-    int64_t b = (int64_t)blockIdx.x * kWsG + warp;
-    WDesc d = desc_decode(desc_word(a, b, lane), lane);
-    unsigned vm = b < a.nblocks ? valid_mask(d, lane) : 0u;
-    uint32_t wraw = desc_word(a, b, lane);
-    WWords<PACKED> W;
-    if (vm) wload<PACKED>(a, (d.nz0 & ~(int64_t)3) + kWPer * lane, W);
-    for (int64_t ph = 0; ph <= nphase; ++ph) {
-      if (ph < nphase) {
-        const int buf = (int)(ph & 1);
-        double xv[kWPer], p[kWPer];
-        wgather<PACKED>(a, W, vm, cmask, xv);
-        // next phase's block: descriptor + words in flight during this one
-        const int64_t bn = b + per_phase;
-        const uint32_t wn = desc_word(a, bn, lane);
-        const WDesc dn = desc_decode(wn, lane);
-        const unsigned vmn = bn < a.nblocks ? valid_mask(dn, lane) : 0u;
-        WWords<PACKED> Wn;
-        if (vmn) wload<PACKED>(a, (dn.nz0 & ~(int64_t)3) + kWPer * lane, Wn);
-        wmul<PACKED>(a, W, vm, tab_sm, xv, p);
-#pragma unroll
-        for (int j = 0; j < kWPer; ++j) prod[buf][warp][j][lane] = p[j];
-        if (lane < kWsBlkWords) dsm[buf][warp][lane] = b < a.nblocks ? wraw : 0u;
-        if (lane == 6 && b >= a.nblocks) dsm[buf][warp][6] = (uint32_t)kBlkNone;
-        b = bn;
-        d = dn;
-        vm = vmn;
-        W = Wn;
-        wraw = wn;
-      }
-      __syncthreads();
-    }
-  } else {
-    // ---- reduce warp: the blocks of gather warps r, r + kWsR, ... of the
-    // previous phase
-    const int r = warp - kWsG;
-    double* slot = rsum[r];
-    for (int64_t ph = 0; ph <= nphase; ++ph) {
-      if (ph > 0) {
-        const int buf = (int)((ph - 1) & 1);
-        for (int g = r; g < kWsG; g += kWsR) {
-          const uint32_t w = lane < kWsBlkWords ? dsm[buf][g][lane] : 0u;
-          const WDesc d = desc_decode(w, lane);
-          if (d.kind == kBlkNone) continue;
-          const unsigned vm = valid_mask(d, lane);
-          double p[kWPer];
-#pragma unroll
-          for (int j = 0; j < kWPer; ++j) p[j] = prod[buf][g][j][lane];
-          process_block<PACKED>(a, d, vm, p, lane, theta, slot, tab_sm, cmask);
-        }
-      }
-      __syncthreads();
-    }
   }
 }
 
@@ -873,33 +750,6 @@ static SpmvArgs spmv_args(const lg_csr* m, const double* x, double* y, lg_ws* ws
 
 template <bool PACKED>
 static int launch_t(const SpmvArgs& args, cudaStream_t s) {
-  static const int ws_env = [] {
-    const char* e = getenv("LG_SPMV_WS");
-    return e ? atoi(e) : 0;
-  }();
-  if (ws_env && args.defer_long) {
-    static bool attr = false;
-    if (!attr) {
-      LG_CUDA(cudaFuncSetAttribute(wspmv_ws_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsSmem));
-      LG_CUDA(cudaFuncSetAttribute(wspmv_ws_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsSmem));
-      attr = true;
-    }
-    const size_t dyn = kWsSmem;
-    const int64_t per = (int64_t)kWsG;
-    const int64_t g = std::max<int64_t>(
-        1, std::min<int64_t>((args.nblocks + per - 1) / per, dev_info().sm_count));
-    wspmv_ws_kernel<PACKED><<<(unsigned)g, kWsThreads, dyn, s>>>(args);
-    LG_LAUNCH_CHECK("wspmv_ws_kernel");
-    const int64_t gl = std::max<int64_t>(
-        1, std::min<int64_t>((args.nlong + 7) / 8, (int64_t)dev_info().sm_count * 8));
-    if (args.nlong > 0) {
-      long_finish_kernel<PACKED><<<(unsigned)gl, 256, 0, s>>>(args);
-      LG_LAUNCH_CHECK("long_finish_kernel");
-    }
-    return LG_OK;
-  }
   static thread_local int occ = 0;
   if (!occ) {
     int o = 0;
