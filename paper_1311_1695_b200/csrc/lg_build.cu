@@ -95,26 +95,41 @@ __global__ void degree_kernel(int64_t n, const int64_t* ustart, const int32_t* c
   }
 }
 
-// one warp per long row (integer weights only): lane-strided partial sums,
-// exact because every partial is an integer below 2^53
+// long rows (integer weights only), cut into chunks of kDegChunk entries --
+// one warp per (row, chunk): lane-strided partial sums and a butterfly, then
+// one double atomicAdd per chunk into the row's (zeroed) diagonal slot.  Every
+// partial and every sum is an integer below 2^53, so the result is exact and
+// the same in any order (C4's 107,553-entry hub row no longer serialises on
+// one warp).
+constexpr int64_t kDegChunk = 2048;
+
+__global__ void zero_diag_kernel(int64_t n, const int32_t* cnt_up, const int32_t* cnt_lo,
+                                 const int64_t* rp, double* val) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += stride)
+    if ((int64_t)cnt_up[v] + cnt_lo[v] > kWideDeg) val[rp[v] + cnt_lo[v]] = 0.0;
+}
+
 __global__ void degree_wide_kernel(int64_t n, const int64_t* ustart, const int32_t* cnt_up,
                                    const int64_t* lstart, const int32_t* cnt_lo,
                                    const int64_t* perm, const double* w, const int64_t* rp,
-                                   int32_t* col, double* val) {
+                                   int32_t* col, double* val, const int64_t* crow,
+                                   const int64_t* cfirst, int64_t nchunks) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += nw) {
-    if ((int64_t)cnt_up[v] + cnt_lo[v] <= kWideDeg) continue;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += nw) {
+    const int64_t v = crow[c];
+    const int64_t k0 = (c - cfirst[c]) * kDegChunk;   // chunk's first entry in the row
+    const int64_t nup = cnt_up[v], len = nup + cnt_lo[v];
+    const int64_t k1 = min(len, k0 + kDegChunk);
     double s = 0.0;
-    const int64_t u0 = ustart[v], u1 = u0 + cnt_up[v];
-    for (int64_t e = u0 + lane; e < u1; e += 32) s += w[e];
-    const int64_t l0 = lstart[v], l1 = l0 + cnt_lo[v];
-    for (int64_t p = l0 + lane; p < l1; p += 32) s += w[perm[p]];
+    for (int64_t k = k0 + lane; k < k1; k += 32)
+      s += k < nup ? w[ustart[v] + k] : w[perm[lstart[v] + (k - nup)]];
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
       const int64_t q = rp[v] + cnt_lo[v];
-      col[q] = (int32_t)v;
-      val[q] = s;
+      if (k0 == 0) col[q] = (int32_t)v;
+      atomicAdd(val + q, s);
     }
   }
 }
@@ -220,9 +235,36 @@ extern "C" int lg_build_laplacian(int64_t n, int64_t m, const int64_t* i_h,
   degree_kernel<<<grid_for_n(n), kThreads, 0, s>>>(n, ustart.p, cnt_up.p, lstart.p,
                                                    cnt_lo.p, perm.p, w.p, rp.p, col.p,
                                                    val.p, wide_ok);
-  if (wide_ok)
-    degree_wide_kernel<<<grid_for_n(32 * n), kThreads, 0, s>>>(
-        n, ustart.p, cnt_up.p, lstart.p, cnt_lo.p, perm.p, w.p, rp.p, col.p, val.p);
+  if (wide_ok) {
+    // chunk list of the long rows (host: the counts are small to copy)
+    std::vector<int32_t> cu((size_t)n), cl((size_t)n);
+    LG_CUDA(cudaMemcpy(cu.data(), cnt_up.p, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    LG_CUDA(cudaMemcpy(cl.data(), cnt_lo.p, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> crow, cfirst;
+    std::vector<int64_t> qzero;
+    for (int64_t v = 0; v < n; ++v) {
+      const int64_t len = (int64_t)cu[(size_t)v] + cl[(size_t)v];
+      if (len <= kWideDeg) continue;
+      const int64_t first = (int64_t)crow.size();
+      for (int64_t k = 0; k < len; k += kDegChunk) {
+        crow.push_back(v);
+        cfirst.push_back(first);
+      }
+    }
+    if (!crow.empty()) {
+      DevBuf<int64_t> dcrow, dcfirst;
+      if (!dcrow.alloc(crow.size()) || !dcfirst.alloc(cfirst.size()))
+        return fail(LG_ENOMEM, "lg_build_laplacian: chunk list alloc");
+      LG_CUDA(cudaMemcpy(dcrow.p, crow.data(), 8 * crow.size(), cudaMemcpyHostToDevice));
+      LG_CUDA(cudaMemcpy(dcfirst.p, cfirst.data(), 8 * cfirst.size(), cudaMemcpyHostToDevice));
+      // the long rows' diagonal slots start from +0.0 (the chunks add into them)
+      zero_diag_kernel<<<grid_for_n(n), kThreads, 0, s>>>(n, cnt_up.p, cnt_lo.p, rp.p, val.p);
+      degree_wide_kernel<<<grid_for_n(32 * (int64_t)crow.size()), kThreads, 0, s>>>(
+          n, ustart.p, cnt_up.p, lstart.p, cnt_lo.p, perm.p, w.p, rp.p, col.p, val.p, dcrow.p,
+          dcfirst.p, (int64_t)crow.size());
+      LG_CUDA(cudaDeviceSynchronize());
+    }
+  }
   LG_LAUNCH_CHECK("build scatter");
   LG_CUDA(cudaDeviceSynchronize());
   LG_CUDA(cudaMemcpy(rp_h, rp.p, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost));

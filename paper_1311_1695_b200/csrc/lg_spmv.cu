@@ -1082,6 +1082,8 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
   cudaStream_t s = (cudaStream_t)stream;
   if (a->npanels > 1 && ws == &local)
     return fail(LG_EINVAL, "lg_spmv: panelled matrix; pass a workspace");
+  if (a->npanels > 1 && !a->pdiag)
+    return fail(LG_EINVAL, "lg_spmv: panelled diagonal-free row block; apply it with lg_spmv_acc");
   int rc = a->npanels > 1
                ? lg_spmv_panels_(a, x, y, theta_h, theta_d, theta_neg, skip, ws, stream)
                : launch(args, s, a->packed != 0);
@@ -1949,8 +1951,13 @@ extern "C" int lg_csr_col_panel(const lg_csr* a, int64_t c0, int64_t c1, int wit
 extern "C" int lg_csr_set_panels(lg_csr* a, int p) {
   if (!a || p < 0 || p > 16) return fail(LG_EINVAL, "lg_csr_set_panels: bad argument");
   if (p > 1 && !a->packed) return fail(LG_EINVAL, "lg_csr_set_panels: only for packed matrices");
-  if (p > 1 && a->is_block)
-    return fail(LG_EINVAL, "lg_csr_set_panels: only for full operators (this one has absent rows)");
+  // a row block may be panelled only as an accumulating operator without a
+  // diagonal (the exterior half of a split row block, applied by
+  // lg_spmv_acc): its panels then hold only the block's rows; a full operator
+  // gets the (d - theta) x init pass in lg_spmv
+  if (p > 1 && a->is_block && a->pdiag)
+    return fail(LG_EINVAL, "lg_csr_set_panels: only for full operators or the diagonal-free "
+                           "exterior half of a row block (this one has absent rows)");
   cudaDeviceSynchronize();
   for (int k = 0; k < a->npanels; ++k) lg_csr_destroy(a->panel[k]);
   a->npanels = 0;
@@ -2025,6 +2032,23 @@ extern "C" int lg_spmv_acc(const lg_csr* a, const double* x, double* y, lg_ws* w
   if (a->nlong) {
     int rc = ensure_long_ws(ws, a);
     if (rc) return rc;
+  }
+  if (a->npanels > 1) {   // accumulating panels (exterior half of a row block)
+    for (int k = 0; k < a->npanels; ++k) {
+      const lg_csr* m = a->panel[k];
+      if (m->nblocks == 0) continue;
+      if (m->nlong) {
+        int rc = ensure_long_ws(ws, m);
+        if (rc) return rc;
+      }
+      SpmvArgs args = spmv_args(m, x, y, ws);
+      args.accum = 1;
+      args.pdiag = nullptr;
+      args.skip = skip;
+      int rc = launch(args, (cudaStream_t)stream, true);
+      if (rc) return rc;
+    }
+    return LG_OK;
   }
   SpmvArgs args = spmv_args(a, x, y, ws);
   args.accum = 1;

@@ -372,6 +372,10 @@ def split_cols(dmat, r0, r1):
         info = [ctypes.c_int64() for _ in range(4)] + [ctypes.c_int(), ctypes.c_int64()]
         nat.call("lg_csr_info", h, *[ctypes.byref(v) for v in info])
         out.append(DeviceCsr.from_handle(h, dmat.n, info[1].value))
+    # the exterior half reads all of x but the rank's own slice: when x
+    # exceeds L2 (C5) its product runs as column panels whose x slices stay
+    # L2-resident, like the single-GPU product (accumulating, block rows only)
+    out[1].auto_panels()
     return tuple(out)
 
 

@@ -574,6 +574,50 @@ def test_split_row_block_interior_exterior(world):
             assert err <= 1e-12 * max(1.0, want.abs().max().item())
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_row_block_panelled_exterior(world):
+    """The exterior half of a rank's row block as accumulating column panels
+    (what C5's row-partitioned product uses: its x exceeds L2; forced here
+    with LG_SPMV_PANELS=3 on small graphs): interior product + panelled
+    exterior = the full product on the rank's rows to roundoff, every other
+    row untouched; a panelled exterior refuses the non-accumulating lg_spmv."""
+    import torch
+
+    import paper_1311_1695_b200 as L
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200._plan import SpmvAcc
+    from paper_1311_1695_b200.device_graphs import rmat_laplacian_device
+    from paper_1311_1695_b200.dist import (RowPartition, local_operator_device, matrix_row_ptr,
+                                           split_cols)
+    g, _ = L.largest_component(L.generators.chung_lu_graph(20000, 2.1, 8.0, max_degree=4000,
+                                                           weighted=True, seed=13))
+    for A in (L.build_laplacian(g), rmat_laplacian_device(13, 8, seed=4)):
+        full = A.device()
+        n = A.n
+        x = dev.to_device(np.random.default_rng(6).standard_normal(n))
+        want = dev.empty(n)
+        full.matvec(x, want)
+        part = RowPartition(matrix_row_ptr(A), world)
+        for r in range(world):
+            r0, r1 = part.rows(r)
+            op = local_operator_device(full, part, r)
+            os.environ["LG_SPMV_PANELS"] = "3"
+            try:
+                inner, outer = split_cols(op, r0, r1)
+            finally:
+                del os.environ["LG_SPMV_PANELS"]
+            assert outer.npanels == 3
+            y = torch.full((n,), 555.0, dtype=torch.float64, device="cuda")
+            inner.matvec(x, y)
+            SpmvAcc(outer, x, y)()
+            torch.cuda.synchronize()
+            assert torch.all(y[:r0] == 555.0) and torch.all(y[r1:] == 555.0)
+            err = (y[r0:r1] - want[r0:r1]).abs().max().item()
+            assert err <= 1e-12 * max(1.0, want.abs().max().item())
+            with pytest.raises(ValueError):
+                outer.matvec(x, y)
+
+
 @pytest.mark.parametrize("panels", [2, 5])
 def test_col_panels_sum_to_full_product(panels):
     """lg_csr_col_panel: the column panels of an operator (diagonal in the
