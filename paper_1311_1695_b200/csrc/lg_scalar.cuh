@@ -46,46 +46,52 @@ struct ScalarProg {
   double imm[LG_MAXIMM];
 };
 
-// one thread; ops, slots and flags all in shared memory
+// one thread; ops, slots and flags all in shared memory.  The operands are
+// read before the dispatch and every arithmetic case is a single expression
+// into r, so the switch compiles to a compact table of small cases (the
+// interpreter sits on the iteration's critical path on small graphs).
 __device__ __forceinline__ void run_program(const uint32_t* ops, int nops, const double* imm,
                                             double* s, int* flags) {
   for (int k = 0; k < nops; ++k) {
     const uint32_t w = ops[k];
-    const uint8_t op = w & 0xff, d = (w >> 8) & 0xff, a = (w >> 16) & 0xff,
-                  b = (w >> 24) & 0xff;
+    const uint32_t op = w & 0xff, d = (w >> 8) & 0xff, a = (w >> 16) & 0xff,
+                   b = (w >> 24) & 0xff;
+    const double va = s[a], vb = s[b];
+    double r;
     switch (op) {
-      case OP_NOP: break;
-      case OP_MOV: s[d] = s[a]; break;
-      case OP_IMM: s[d] = imm[a]; break;
-      case OP_ADD: s[d] = s[a] + s[b]; break;
-      case OP_SUB: s[d] = s[a] - s[b]; break;
-      case OP_MUL: s[d] = s[a] * s[b]; break;
-      case OP_DIV: s[d] = s[a] / s[b]; break;
-      case OP_SQRT: s[d] = sqrt(s[a]); break;
-      case OP_NEG: s[d] = -s[a]; break;
-      case OP_HYPOT: s[d] = hypot(s[a], s[b]); break;
-      case OP_ABS: s[d] = fabs(s[a]); break;
-      case OP_MAX: s[d] = fmax(s[a], s[b]); break;
-      case OP_MIN: s[d] = fmin(s[a], s[b]); break;
-      case OP_LE: s[d] = (s[a] <= s[b]) ? 1.0 : 0.0; break;
-      case OP_LT: s[d] = (s[a] < s[b]) ? 1.0 : 0.0; break;
-      case OP_EQ: s[d] = (s[a] == s[b]) ? 1.0 : 0.0; break;
-      case OP_NE: s[d] = (s[a] != s[b]) ? 1.0 : 0.0; break;
-      case OP_GT: s[d] = (s[a] > s[b]) ? 1.0 : 0.0; break;
-      case OP_GE: s[d] = (s[a] >= s[b]) ? 1.0 : 0.0; break;
-      case OP_SEL: if (s[a] != 0.0) s[d] = s[b]; break;
-      case OP_AND: s[d] = (s[a] != 0.0 && s[b] != 0.0) ? 1.0 : 0.0; break;
-      case OP_OR: s[d] = (s[a] != 0.0 || s[b] != 0.0) ? 1.0 : 0.0; break;
-      case OP_NOT: s[d] = (s[a] == 0.0) ? 1.0 : 0.0; break;
-      case OP_FLAG: flags[d & 31] = (s[a] != 0.0) ? 1 : 0; break;
-      case OP_FLAGOR: if (s[a] != 0.0) flags[d & 31] = 1; break;
-      case OP_LDFLAG: s[d] = (double)flags[a & 31]; break;
-      case OP_HALTIF: if (s[a] != 0.0) return; break;
-      case OP_DIVZ: s[d] = (s[b] != 0.0) ? s[a] / s[b] : 0.0; break;
-      case OP_INC: s[d] += 1.0; break;
-      case OP_RECIP: s[d] = 1.0 / s[a]; break;
+      case OP_MOV: r = va; break;
+      case OP_IMM: r = imm[a]; break;
+      case OP_ADD: r = va + vb; break;
+      case OP_SUB: r = va - vb; break;
+      case OP_MUL: r = va * vb; break;
+      case OP_DIV: r = va / vb; break;
+      case OP_SQRT: r = sqrt(va); break;
+      case OP_NEG: r = -va; break;
+      case OP_HYPOT: r = hypot(va, vb); break;
+      case OP_ABS: r = fabs(va); break;
+      case OP_MAX: r = fmax(va, vb); break;
+      case OP_MIN: r = fmin(va, vb); break;
+      case OP_LE: r = (va <= vb) ? 1.0 : 0.0; break;
+      case OP_LT: r = (va < vb) ? 1.0 : 0.0; break;
+      case OP_EQ: r = (va == vb) ? 1.0 : 0.0; break;
+      case OP_NE: r = (va != vb) ? 1.0 : 0.0; break;
+      case OP_GT: r = (va > vb) ? 1.0 : 0.0; break;
+      case OP_GE: r = (va >= vb) ? 1.0 : 0.0; break;
+      case OP_SEL: r = (va != 0.0) ? vb : s[d]; break;
+      case OP_AND: r = (va != 0.0 && vb != 0.0) ? 1.0 : 0.0; break;
+      case OP_OR: r = (va != 0.0 || vb != 0.0) ? 1.0 : 0.0; break;
+      case OP_NOT: r = (va == 0.0) ? 1.0 : 0.0; break;
+      case OP_LDFLAG: r = (double)flags[a & 31]; break;
+      case OP_DIVZ: r = (vb != 0.0) ? va / vb : 0.0; break;
+      case OP_INC: r = s[d] + 1.0; break;
+      case OP_RECIP: r = 1.0 / va; break;
+      case OP_NOP: continue;
+      case OP_FLAG: flags[d & 31] = (va != 0.0) ? 1 : 0; continue;
+      case OP_FLAGOR: if (va != 0.0) flags[d & 31] = 1; continue;
+      case OP_HALTIF: if (va != 0.0) return; continue;
       default: return;
     }
+    s[d] = r;
   }
 }
 
