@@ -246,6 +246,11 @@ int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels);
  * one stream.  z may alias r. */
 int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
                  void* stream);
+/* Sweep implementation of a factor: 0 = dataflow sweeps (one cooperative launch
+ * per triangle; the default), 1 = resident sweep (both triangles in one CTA,
+ * levels separated by CTA barriers; opt-in, also LG_SWEEP_CTA=1).  Same bits
+ * either way.  Returns the previous mode; any other `mode` only queries. */
+int lg_ic0_set_mode(lg_ic0* f, int mode);
 /* Debug instrumentation of the sweeps: enable != 0 allocates a timestamp
  * buffer written after every level segment (CTA 0's view); host_out (cap
  * entries) receives the last apply's timestamps.  Returns the number of

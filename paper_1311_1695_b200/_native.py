@@ -109,6 +109,7 @@ _SIGS = {
     "lg_color_smallest_last": (c_int, [c_i64, c_p, c_p, c_p, c_p]),
     "lg_ic0_info": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_ic0_apply": (c_int, [c_p, c_p, c_p, c_p, c_p]),
+    "lg_ic0_set_mode": (c_int, [c_p, c_int]),
     "lg_ic0_trace": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_ic0_flow_trace": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_ic0_schedule": (c_int, [c_p, c_int, c_p, c_int]),

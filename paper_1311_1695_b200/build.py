@@ -84,11 +84,44 @@ def build(force=False, jobs=None, verbose=False):
     return LIB
 
 
+def build_variant(name, defines):
+    """An alternative build with extra -D flags into build/variants/<name>.so
+    (A/B experiments: run with LG_LIB_OVERRIDE=build/variants/<name>.so)."""
+    vdir = HERE.parent / "build" / "variants"
+    odir = vdir / (name + "_obj")
+    odir.mkdir(parents=True, exist_ok=True)
+    flags = [f"-D{d}" for d in defines]
+
+    def comp(src):
+        obj = odir / (src.stem + ".o")
+        res = subprocess.run([nvcc(), *ARCH, *NVCC_FLAGS, *flags, "-c", str(src), "-o", str(obj)],
+                             capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stderr}")
+        (odir / (src.stem + ".ptxas.txt")).write_text(res.stderr)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        objs = list(ex.map(comp, sources()))
+    out = vdir / (name + ".so")
+    res = subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", *map(str, objs),
+                          "-o", str(out), "-lgomp", "-lpthread", "-ldl", "-lrt"],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    return out
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--jobs", type=int, default=None)
+    ap.add_argument("--variant", nargs="+", metavar=("NAME", "DEFINE"),
+                    help="build build/variants/NAME.so with -DDEFINE ... instead")
     args = ap.parse_args(argv)
+    if args.variant:
+        print(build_variant(args.variant[0], args.variant[1:]))
+        return 0
     build(force=args.force, jobs=args.jobs, verbose=True)
 
 

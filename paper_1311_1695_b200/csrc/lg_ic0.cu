@@ -90,6 +90,9 @@ struct SweepDev {
   unsigned long long* ttrace = nullptr;   // debug: dataflow per-task timestamps
   RowInfo* rinfo = nullptr;       // dataflow row records, permuted order
   int32_t* oidx = nullptr;        // permuted row -> second-output index (or NULL)
+  void* cdesc = nullptr;          // [ntasks] CtaDesc records (resident sweep)
+  int32_t* lhub0 = nullptr;       // [levels + 1] first hub-row id of each level (resident sweep)
+  int32_t* hub_prow = nullptr;    // [hub rows] permuted row of each hub row
   int32_t ntasks = 0;
   int32_t nparts = 0;        // hub partial slots
   int32_t nsegs = 0;
@@ -113,6 +116,9 @@ struct lg_ic0 {
   // vice versa, so an apply is exactly two launches; false after a
   // level-barrier apply (the state then needs one explicit re-arm)
   mutable bool flow_armed = false;
+  // 1: both sweeps run as one resident CTA (opt-in), 0: dataflow sweeps
+  int cta_mode = 0;
+  int cta_threads = 0;
 };
 
 namespace lg {
@@ -264,6 +270,7 @@ struct SweepHost {
   std::vector<SweepSeg> segs;
   std::vector<int32_t> hub_first, hub_nchunk;
   std::vector<int32_t> tlevel, lexpect;
+  std::vector<int32_t> lhub0, hub_prow;   // resident sweep: hub rows per level
   int32_t nparts = 0;
   int32_t nbar = 0;
   int levels = 0;
@@ -328,6 +335,7 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
   };
   for (int l = 0; l < nl; ++l) {
     const int32_t t0 = (int32_t)h.tasks.size();
+    h.lhub0.push_back((int32_t)h.hub_first.size());
     int64_t t = lcount[(size_t)l];
     const int64_t te = lcount[(size_t)l + 1];
     while (t < te) {
@@ -339,6 +347,7 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
         const int32_t hid = (int32_t)h.hub_first.size();
         h.hub_first.push_back(h.nparts);
         h.hub_nchunk.push_back(nch);
+        h.hub_prow.push_back((int32_t)t);
         h.nparts += nch;
         for (int32_t c = 0; c < nch; ++c) {
           const int64_t lo = h.prp[(size_t)t] + (int64_t)c * kHubChunk;
@@ -373,6 +382,7 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
     h.segs.push_back({t0, t1, (t1 - t0) <= narrow_tasks ? 1 : 0, 0, 0, 0});
     for (int32_t t = t0; t < t1; ++t) h.tlevel.push_back(l);
   }
+  h.lhub0.push_back((int32_t)h.hub_first.size());
   // re-lay the entries task by task, every task starting on a multiple of 4
   // entries (16-byte aligned columns, 32-byte aligned values); lane tables
   // are relative to the task base
@@ -830,15 +840,16 @@ struct FStaged {
   RowInfo ri;
 };
 
-__device__ __forceinline__ void fstage1(const FlowArgs& a, int64_t t, int lane, FStage1& s) {
+template <class A>
+__device__ __forceinline__ void fstage1(const A& a, int64_t t, int lane, FStage1& s) {
   s.tk = a.tasks[t];
   s.base = a.tbase[t];
   s.lt = a.lanetab[t * 32 + lane];
   s.lev = a.tlevel[t];
 }
 
-__device__ __forceinline__ void fstage2(const FlowArgs& a, const FStage1& s, int lane,
-                                        FStaged& st) {
+template <class A>
+__device__ __forceinline__ void fstage2(const A& a, const FStage1& s, int lane, FStaged& st) {
   const SweepTask tk = s.tk;
   st.info = tk.b;
   st.lev = s.lev;
@@ -1066,6 +1077,297 @@ __global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a)
   if (lane == 0) atomicSub((int*)&s_active, 1);
 }
 
+
+// ---- resident sweep (narrow DAGs: one CTA runs the whole apply) -------------
+// On a factor whose levels are narrow (C1: ~90 rows a level, C2: ~200, C3:
+// ~300) the dataflow sweep is bound by its dependency hop through L2 (store +
+// poll: 1.0-1.4 us a level).  One CTA alone has no such hop: its warps see each
+// other's stores after a __syncthreads (~50 ns) and both sweeps run in ONE
+// launch.  Measured (scripts/micro/sweepchain.cu): 0.22-0.29 us per level for
+// one CTA against 0.83 us for a level across a cluster with x in L2.  The
+// tasks, lane tables and summation order are the dataflow sweep's, so the
+// result is bitwise the same: warp w takes tasks w, w + W, ... (consecutive
+// tasks of a level land on distinct warps) and passes one barrier per level; a
+// level holding hub rows adds a second barrier -- every chunk publishes its
+// partial, then a warp per hub row sums them in chunk order.
+//
+// With only W warps on the SM nothing may wait on a dependent load chain, so a
+// warp's future tasks are staged into shared memory with cp.async, two levels
+// deep: the 96-byte descriptor (task, entry base and count, level, lane table)
+// of the task 2 D ahead, and -- from the descriptor that has landed by then --
+// the entries (columns, values) and row records of the task D ahead.  One
+// commit group per step; cp.async.wait_group<D - 1> covers both.  At its turn
+// a task reads everything but x and b from shared memory.  One SM's
+// throughput bounds the sweep; measured, it only ties the dataflow sweeps on
+// the smallest factor (C1) and loses elsewhere, so it is opt-in
+// (pick_cta_mode below).
+struct CtaDesc {        // 96 bytes, 16-byte aligned
+  SweepTask tk;
+  int64_t base;         // first entry (multiple of 4)
+  int32_t lev;
+  int32_t nent4;        // entries of the task, rounded up to a multiple of 4
+  uint16_t lanetab[32];
+};
+static_assert(sizeof(CtaDesc) == 96, "CtaDesc layout");
+
+constexpr int kCtaEntMax = 256;   // entries per task (pack: 32 lanes x 8; chunk: kHubChunk)
+
+struct CtaDir {
+  const int32_t* pcol;
+  const double* pval;
+  const RowInfo* rinfo;
+  const int32_t* oidx;
+  const CtaDesc* desc;
+  const int32_t* lhub0;
+  const int32_t* hub_prow;
+  const int32_t* hub_first;
+  const int32_t* hub_nchunk;
+  double* hub_part;
+  const double* b;
+  double* x;
+  double* out2;
+  unsigned long long* ttrace;   // debug: per task {start, inputs ready, done}
+  int32_t ntasks;
+  int32_t levels;
+};
+
+struct CtaArgs {
+  CtaDir dir[2];
+  const int* skip;
+};
+
+template <int B>
+struct CtaSlots {       // one warp's staging area
+  CtaDesc desc[2 * (B - 1) + 1];
+  int32_t col[B][kCtaEntMax];
+  double val[B][kCtaEntMax];
+  RowInfo ri[B][32];
+};
+
+__device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst_smem)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer_after(double dep) {
+  unsigned long long t;
+  asm volatile("{ .reg .f64 d; mov.f64 d, %1; mov.u64 %0, %%globaltimer; }" : "=l"(t) : "d"(dep));
+  return t;
+}
+
+__device__ __forceinline__ void cta_publish(const CtaDir& a, int32_t p, const RowInfo& ri,
+                                            double v) {
+  if (__double_as_longlong(v) == (long long)kSentinel) v = __longlong_as_double(0x7ff8000000000000ll);
+  a.x[ri.xrow] = v;
+  if (a.out2) a.out2[a.oidx[p]] = v;
+}
+
+// One staged task: same entry order per lane, same butterfly, same division as
+// flow_complete.
+__device__ __forceinline__ void cta_complete(const CtaDir& a, const CtaDesc& d, const int32_t* col,
+                                             const double* val, const RowInfo* ris, int lane,
+                                             unsigned long long* tr) {
+  const uint32_t lt = d.lanetab[lane];
+  const int ne = lt & 31, rel = lt >> 5;
+  const int32_t info = d.tk.b;
+  int sh = 5;
+  bool owner = false;
+  RowInfo ri;
+  double bv = 0.0;
+  if (info != 0) {
+    const int L = info >> 8, cnt = info & 0xff;
+    sh = __ffs(L) - 1;
+    owner = (lane >> sh) < cnt && (lane & (L - 1)) == 0;
+    if (owner) {
+      ri = ris[lane >> sh];
+      bv = a.b[ri.bidx];
+    }
+  }
+  double xv[kLaneMax], vv[kLaneMax];
+#pragma unroll
+  for (int e = 0; e < kLaneMax; ++e) {
+    if (e < ne) {
+      const int k = rel + (e << sh);
+      xv[e] = a.x[col[k]];
+      vv[e] = val[k];
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int e = 0; e < kLaneMax; ++e)
+    if (e < ne) s += vv[e] * xv[e];
+  if (tr && lane == 0) tr[1] = gtimer_after(s);
+  if (info != 0) {
+    for (int o = (1 << sh) >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (owner) cta_publish(a, d.tk.p + (lane >> sh), ri, (bv - s) / ri.dg);
+    return;
+  }
+  // chunk of a hub row: every chunk (the first too) publishes its partial;
+  // the row is finished behind the level's barrier (cta_level_end)
+  s = warp_sum(s);
+  if (lane == 0) a.hub_part[a.hub_first[d.tk.d] + d.tk.c] = s;
+}
+
+// Split CTA barrier on an mbarrier (one arrival per warp): a warp arrives as
+// soon as its last task of the level is stored and only waits when it next
+// needs the level -- the staging work in between is off the critical path.
+__device__ __forceinline__ void lvl_arrive(uint64_t* bar, int lane) {
+  __syncwarp();   // the warp's stores are ordered before the elected lane's release
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void lvl_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n LVLW_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LVLW_%=;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kCtaHubLevels = 4096;   // level hub flags kept in shared memory
+
+struct CtaShared {
+  uint64_t bar;
+  unsigned char hub[kCtaHubLevels];
+};
+
+// per-warp barrier bookkeeping: the phase the warp will wait on next, and
+// whether it has already arrived there
+struct CtaSync {
+  unsigned phase;
+  bool arrived;
+};
+
+// Pass level l: (arrive,) wait; hub rows of the level are then summed in chunk
+// order (lane-strided, butterfly: the dataflow sweep's order) behind a second
+// phase.  Every warp of the CTA passes every level once.
+__device__ __forceinline__ void cta_level_end(const CtaDir& a, CtaShared& sh, CtaSync& sy, int l,
+                                              int warp, int lane, int W) {
+  // (the flag is read before the wait: once the sweep's last level is passed
+  // the next sweep's flags may overwrite it)
+  const bool hub = l < kCtaHubLevels ? sh.hub[l] != 0 : a.lhub0[l + 1] > a.lhub0[l];
+  if (!sy.arrived) lvl_arrive(&sh.bar, lane);
+  lvl_wait(&sh.bar, sy.phase & 1u);
+  ++sy.phase;
+  sy.arrived = false;
+  if (hub) {
+    const int32_t h0 = a.lhub0[l], h1 = a.lhub0[l + 1];
+    for (int32_t hid = h0 + warp; hid < h1; hid += W) {
+      const int32_t p = a.hub_prow[hid];
+      const RowInfo ri = a.rinfo[p];
+      const int32_t first = a.hub_first[hid], nch = a.hub_nchunk[hid];
+      double t = 0.0;
+      for (int32_t c = lane; c < nch; c += 32) t += a.hub_part[first + c];
+      t = warp_sum(t);
+      if (lane == 0) cta_publish(a, p, ri, (a.b[ri.bidx] - t) / ri.dg);
+    }
+    lvl_arrive(&sh.bar, lane);
+    lvl_wait(&sh.bar, sy.phase & 1u);
+    ++sy.phase;
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void cta_run_dir(const CtaDir& a, CtaSlots<B>& sm, CtaShared& sh,
+                                            CtaSync& sy, int warp, int lane, int W) {
+  constexpr int D = B - 1;          // entries are staged D tasks ahead
+  constexpr int ND = 2 * D + 1;     // descriptors 2 D ahead
+  const int nt = a.ntasks;
+  // hub flags of this direction's levels (the previous direction is done with them)
+  for (int l = threadIdx.x; l < a.levels && l < kCtaHubLevels; l += blockDim.x)
+    sh.hub[l] = a.lhub0[l + 1] > a.lhub0[l];
+  lvl_arrive(&sh.bar, lane);
+  lvl_wait(&sh.bar, sy.phase & 1u);
+  ++sy.phase;
+  int cur = 0;
+  // ring positions of step i (descriptor), i + D (descriptor, entries), i + 2 D
+  // (each ring slot of step j is j mod its ring size)
+  int dq0 = 1, dq1 = (D + 1) % ND, dq2 = 0, eq0 = 0, eq1 = 0;
+  // step i handles task warp + i W; the first 2 D steps only stage
+  int t = warp - 2 * D * W;
+  for (int i = -2 * D;; ++i, t += W) {
+    if (i >= 0 && t >= nt) break;
+    {   // descriptor of the task 2 D steps ahead
+      const int td = t + 2 * D * W;
+      if (td < nt && lane < 6)
+        cp_async16(reinterpret_cast<char*>(&sm.desc[dq2]) + 16 * lane,
+                   reinterpret_cast<const char*>(a.desc + td) + 16 * lane);
+    }
+    cp_async_wait<D - 1 < 0 ? 0 : D - 1>();
+    __syncwarp();
+    {   // entries and row records of the task D steps ahead
+      const int te = t + D * W;
+      if (te >= 0 && te < nt) {
+        const CtaDesc& d = sm.desc[dq1];
+        const int n4 = d.nent4 >> 2;
+        const int32_t* gc = a.pcol + d.base;
+        const double* gv = a.pval + d.base;
+        for (int q = lane; q < n4; q += 32) cp_async16(&sm.col[eq1][4 * q], gc + 4 * q);
+        for (int q = lane; q < 2 * n4; q += 32) cp_async16(&sm.val[eq1][2 * q], gv + 2 * q);
+        if (d.tk.b != 0 && lane < (d.tk.b & 0xff))
+          cp_async16(&sm.ri[eq1][lane], a.rinfo + d.tk.p + lane);
+      }
+    }
+    cp_async_commit();
+    if (i >= 0) {
+      const CtaDesc& d = sm.desc[dq0];
+      const int lev = d.lev;
+      while (cur < lev) cta_level_end(a, sh, sy, cur++, warp, lane, W);
+      unsigned long long* tr = a.ttrace ? a.ttrace + 3 * (int64_t)t : nullptr;
+      if (tr && lane == 0) tr[0] = gtimer();
+      cta_complete(a, d, sm.col[eq0], sm.val[eq0], sm.ri[eq0], lane, tr);
+      if (tr && lane == 0) tr[2] = gtimer();
+      // the warp's last task of this level: arrive now, stage under the wait
+      const int tn = t + W;
+      const int nlev = tn < nt ? sm.desc[dq0 + 1 == ND ? 0 : dq0 + 1].lev : 0x7fffffff;
+      if (nlev > lev) {
+        lvl_arrive(&sh.bar, lane);
+        sy.arrived = true;
+      } else {
+        __syncwarp();   // the slot and the descriptor are reused D / 2 D steps on
+      }
+    }
+    dq0 = dq0 + 1 == ND ? 0 : dq0 + 1;
+    dq1 = dq1 + 1 == ND ? 0 : dq1 + 1;
+    dq2 = dq2 + 1 == ND ? 0 : dq2 + 1;
+    if (i >= 0) eq0 = eq0 + 1 == B ? 0 : eq0 + 1;
+    if (i + D >= 0) eq1 = eq1 + 1 == B ? 0 : eq1 + 1;
+  }
+  cp_async_wait<0>();
+  // remaining levels (every warp passes every level)
+  while (cur < a.levels) cta_level_end(a, sh, sy, cur++, warp, lane, W);
+}
+
+template <int W, int B>
+__global__ void __launch_bounds__(32 * W, 1) sweep_cta_kernel(CtaArgs args) {
+  if (args.skip && *args.skip) return;
+  extern __shared__ __align__(16) unsigned char cta_smem[];
+  __shared__ CtaShared sh;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&sh.bar)),
+                 "r"(W)
+                 : "memory");
+  __syncthreads();
+  CtaSlots<B>& sm = reinterpret_cast<CtaSlots<B>*>(cta_smem)[warp];
+  CtaSync sy{0u, false};
+  cta_run_dir<B>(args.dir[0], sm, sh, sy, warp, lane, W);
+  cta_run_dir<B>(args.dir[1], sm, sh, sy, warp, lane, W);
+}
+
 template <typename T>
 static bool upload(T** dst, const std::vector<T>& v) {
   if (v.empty()) return true;
@@ -1145,8 +1447,24 @@ static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
             upload(&d.tbase, h.tbase) && upload(&d.lanetab, h.lanetab) &&
             upload(&d.segs, h.segs) && upload(&d.hub_first, h.hub_first) &&
             upload(&d.hub_nchunk, h.hub_nchunk) && upload(&d.tlevel, h.tlevel) &&
-            upload(&d.lexpect, h.lexpect);
+            upload(&d.lexpect, h.lexpect) && upload(&d.lhub0, h.lhub0) &&
+            upload(&d.hub_prow, h.hub_prow);
   d.ntasks = (int32_t)h.tasks.size();
+  {
+    std::vector<CtaDesc> cd(h.tasks.size());
+    for (size_t t = 0; t < h.tasks.size(); ++t) {
+      CtaDesc& c = cd[t];
+      c.tk = h.tasks[t];
+      c.base = h.tbase[t];
+      c.lev = h.tlevel[t];
+      const int64_t end = t + 1 < h.tasks.size() ? h.tbase[t + 1] : (int64_t)h.pcol.size();
+      c.nent4 = (int32_t)(end - h.tbase[t]);
+      for (int ln = 0; ln < 32; ++ln) c.lanetab[ln] = h.lanetab[t * 32 + (size_t)ln];
+    }
+    CtaDesc* dp = nullptr;
+    ok = ok && upload(&dp, cd);
+    d.cdesc = dp;
+  }
   d.nparts = h.nparts;
   {
     std::vector<RowInfo> ri((size_t)n);
@@ -1198,6 +1516,9 @@ static void free_sweep(SweepDev& d) {
   cudaFree(d.ttrace);
   cudaFree(d.rinfo);
   cudaFree(d.oidx);
+  cudaFree(d.lhub0);
+  cudaFree(d.hub_prow);
+  cudaFree(d.cdesc);
   d = SweepDev();
 }
 
@@ -1305,6 +1626,62 @@ static int launch_flow(const SweepDev& dv, const SweepDev& other, const double* 
   cfg.numAttrs = 1;
   LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_flow_kernel, a));
   return LG_OK;
+}
+
+static CtaDir cta_dir(const SweepDev& dv, const double* b, double* x, double* out2) {
+  CtaDir a;
+  a.pcol = dv.pcol;
+  a.pval = dv.pval;
+  a.rinfo = dv.rinfo;
+  a.oidx = dv.oidx;
+  a.desc = static_cast<const CtaDesc*>(dv.cdesc);
+  a.lhub0 = dv.lhub0;
+  a.hub_prow = dv.hub_prow;
+  a.hub_first = dv.hub_first;
+  a.hub_nchunk = dv.hub_nchunk;
+  a.hub_part = dv.hub_part;
+  a.b = b;
+  a.x = x;
+  a.out2 = out2;
+  a.ttrace = dv.ttrace;
+  a.ntasks = dv.ntasks;
+  a.levels = dv.levels;
+  return a;
+}
+
+template <int W, int B>
+static int launch_cta_t(const CtaArgs& ca, cudaStream_t s) {
+  constexpr size_t smem = sizeof(CtaSlots<B>) * W;
+  static bool once = false;
+  if (!once) {
+    LG_CUDA(cudaFuncSetAttribute(sweep_cta_kernel<W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    once = true;
+  }
+  sweep_cta_kernel<W, B><<<1, 32 * W, smem, s>>>(ca);
+  LG_CUDA(cudaGetLastError());
+  return LG_OK;
+}
+
+static int launch_cta(const CtaArgs& ca, int threads, cudaStream_t s) {
+  switch (threads) {
+    case 896: return launch_cta_t<28, 2>(ca, s);
+    case 768: return launch_cta_t<24, 2>(ca, s);
+    case 256: return launch_cta_t<8, 3>(ca, s);
+    case 128: return launch_cta_t<4, 3>(ca, s);
+    default: return launch_cta_t<16, 3>(ca, s);
+  }
+}
+
+// Resident-sweep choice.  Measured on B200 (scripts/ic0_modes.py, r02aj):
+// C1 53.6 us against 54.8 us for the dataflow sweeps, C2 287 against 175, C3
+// 5,191 against 1,351 -- one SM completes a level step in ~0.9 us (0.19 us L2
+// gather of x + 0.2 us reduce / divide / store + barrier and staging), no
+// faster than the dataflow hop, and has 1/148 of the task throughput.  So it
+// is opt-in only: LG_SWEEP_CTA=1, or lg_ic0_set_mode(f, 1).
+static int pick_cta_mode(const lg_ic0*) {
+  const char* e = getenv("LG_SWEEP_CTA");
+  return e ? atoi(e) != 0 : 0;
 }
 
 static int launch_sweep(SweepArgs& args, cudaStream_t s) {
@@ -1497,8 +1874,23 @@ int lg_ic0_create_perm(int64_t n, const int64_t* l_rp, const int64_t* l_col,
     return fail(LG_ECUDA, std::string("lg_ic0_create: ") + cudaGetErrorString(err));
   }
   f->grid = sweep_launch().grid;
+  f->cta_mode = pick_cta_mode(f);
+  {
+    const char* e = getenv("LG_SWEEP_CTA_THREADS");
+    f->cta_threads = e ? atoi(e) : 512;
+  }
   *out = f;
   return LG_OK;
+}
+
+// Sweep implementation of a factor: 0 dataflow sweeps, 1 resident CTA sweep
+// (the default is chosen at creation from the level widths).  Both give the
+// same bits; returns the previous mode.
+int lg_ic0_set_mode(lg_ic0* f, int mode) {
+  if (!f) return fail(LG_EINVAL, "lg_ic0_set_mode: NULL handle");
+  const int prev = f->cta_mode;
+  if (mode == 0 || mode == 1) f->cta_mode = mode;
+  return prev;
 }
 
 // Debug: record a device timestamp after every level segment of both sweeps
@@ -1687,6 +2079,15 @@ int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
     // layout: fwd segs, fwd inline-stage counter, bwd segs, bwd counter
     fa.trace = f->trace;
     ba.trace = f->trace + f->fwd.nsegs + 1;
+  }
+  if (f->cta_mode && sweep_mode() != 0 && !f->trace) {
+    double* zx = f->omap ? f->zp : z;
+    CtaArgs ca;
+    ca.dir[0] = cta_dir(f->fwd, r, f->tmp, nullptr);
+    ca.dir[1] = cta_dir(f->bwd, f->tmp, zx, f->omap ? z : nullptr);
+    ca.skip = skip;
+    f->flow_armed = false;   // tmp now holds values, not the dataflow sentinels
+    return launch_cta(ca, f->cta_threads, s);
   }
   if (sweep_mode() != 0 && !f->trace) {
     double* zx = f->omap ? f->zp : z;

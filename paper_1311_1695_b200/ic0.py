@@ -66,6 +66,12 @@ class DeviceIc0:
         if h and h.value and nat._lib is not None:
             nat._lib.lg_ic0_destroy(h)
 
+    def set_mode(self, mode):
+        """Sweep implementation: 0 dataflow sweeps (default), 1 resident
+        one-CTA sweep (opt-in; same bits either way); -1 only queries.
+        Returns the previous mode."""
+        return nat.load().lg_ic0_set_mode(self.handle, int(mode))
+
     def apply_raw(self, r, z, skip, stream):
         nat.check(nat.load().lg_ic0_apply(self.handle, r, z, skip, stream), "lg_ic0_apply")
 

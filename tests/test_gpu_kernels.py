@@ -287,6 +287,7 @@ def test_ic0_dataflow_state_handoff(L, mc):
     a = L.build_laplacian(L.config_graph("C2"))
     f = L.ic0_factorize_multicolor(a) if mc else L.ic0_factorize(a)
     d = f.device()
+    d.set_mode(0)                                   # whatever LG_SWEEP_CTA says
     rng = np.random.default_rng(3)
     xs = [torch.from_numpy(rng.standard_normal(a.n)).cuda() for _ in range(3)]
     want = [f.apply(x.cpu().numpy()) for x in xs]
@@ -307,6 +308,60 @@ def test_ic0_dataflow_state_handoff(L, mc):
     d.apply(y, y)                                   # z aliases r
     assert torch.equal(y, ref[1])
     assert torch.equal(d.apply(xs[2], dev.empty(a.n)), ref[2])
+
+
+@pytest.mark.parametrize("cfg,mc", [("C1", False), ("C2", False), ("C2", True), ("C3", False)])
+def test_ic0_resident_sweep_same_bits(L, cfg, mc):
+    """The resident one-CTA sweep (both triangles in one launch, levels
+    separated by CTA barriers) walks the dataflow sweep's tasks in the same
+    summation order: bitwise the same z, whichever ran before, with skipped
+    and in-place applies, and against the oracle's apply (ic0.py:40-45)."""
+    import torch
+    from paper_1311_1695_b200 import _device as dev
+    a = L.build_laplacian(L.config_graph(cfg))
+    f = L.ic0_factorize_multicolor(a) if mc else L.ic0_factorize(a)
+    d = f.device()
+    rng = np.random.default_rng(5)
+    xs = [torch.from_numpy(rng.standard_normal(a.n)).cuda() for _ in range(3)]
+    d.set_mode(0)
+    flow = [d.apply(x, dev.empty(a.n)).clone() for x in xs]
+    assert d.set_mode(1) == 0
+    for x, w in zip(xs, flow):
+        assert torch.equal(d.apply(x, dev.empty(a.n)), w)
+    d.set_mode(0)                                   # back: the dataflow state is re-armed
+    assert torch.equal(d.apply(xs[1], dev.empty(a.n)), flow[1])
+    d.set_mode(1)
+    skip = torch.ones(1, dtype=torch.int32, device="cuda")
+    z = torch.full((a.n,), 7.0, dtype=torch.float64, device="cuda")
+    d.apply_raw(xs[0].data_ptr(), z.data_ptr(), skip.data_ptr(), dev.stream_ptr())
+    assert torch.all(z == 7.0)
+    y = xs[2].clone()
+    d.apply(y, y)                                   # z aliases r
+    assert torch.equal(y, flow[2])
+    for nthreads in (1, 2):                          # repeated applies
+        assert torch.equal(d.apply(xs[0], dev.empty(a.n)), flow[0])
+    if not mc:
+        zr = O.Ic0(a.n, f.l.row_ptr, f.l.col_idx, f.l.values).apply(xs[0].cpu().numpy())
+        assert np.max(np.abs(flow[0].cpu().numpy() - zr)) <= 1e-12 * np.max(np.abs(zr))
+
+
+@pytest.mark.parametrize("name", KAT)
+def test_ic0_resident_sweep_fixtures(L, kat, name):
+    """Same on the reference's fixture graphs (stars and hubs included):
+    resident and dataflow sweeps agree bit for bit and match the golden apply."""
+    graphs, arrays, _ = kat
+    a = L.build_laplacian(edge_list(L, graphs, name))
+    f = L.ic0_factorize(a)
+    d = f.device()
+    import torch
+    x = torch.from_numpy(np.ascontiguousarray(arrays[name + "_x"])).cuda()
+    d.set_mode(0)
+    z0 = d.apply(x).clone()
+    d.set_mode(1)
+    z1 = d.apply(x).clone()
+    assert torch.equal(z0, z1)
+    want = arrays[name + "_ic0"]
+    assert np.max(np.abs(z1.cpu().numpy() - want)) <= 1e-12 * np.max(np.abs(want))
 
 
 def test_jacobi_variant(L):
