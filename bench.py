@@ -637,6 +637,8 @@ def c5_main(args):
         ms = float(t.item())
     algo = 12 * A.nnz + 8 * (n + 1) + 16 * n
     stream = d.stream_bytes
+    # x gathers of the whole stored column stream alone (one pass, no panels)
+    gather_us = _event_timer(lambda: d.gather_probe(x), reps=5) if world == 1 else None
     traffic = None
     try:
         tr = json.loads((ROOT / "profiles" / "spmv_traffic_c5.json").read_text())
@@ -663,7 +665,11 @@ def c5_main(args):
                                if world == 1 else "packed row block",
                      "bytes_model": "diag init 24 n + per panel: 4 B / off-diagonal + 96 B / "
                                     "warp block + 8 B / column of its x slice + 20 B / row "
-                                    "written (y read-modify-write, row map)"},
+                                    "written (y read-modify-write, row map)",
+                     "gather_floor_us": gather_us,
+                     "frac_of_gather_floor": gather_us / (ms * 1e3) if gather_us else None,
+                     "gather_gsectors_s": (A.nnz - n) / (gather_us * 1e-6) / 1e9
+                     if gather_us else None},
         "gpu_launches": args.steps * launches_per_step,
         "clocks": clk.summary(),
     }
@@ -844,6 +850,10 @@ def main():
             nat.call("lg_spmv_host", *args_c)
         e2e["cabi_value"] = reps / (time.perf_counter() - t0)
         e2e["cabi_path"] = "lg_spmv_host(csr, x_h, y_h, ...) (C ABI, pinned staging)"
+    # the product's real bound: its x gathers alone (lg_spmv_gather_probe: the
+    # stored column stream, eight gathers in flight per thread, nothing
+    # else), timed live on this operator under the same L2 flush
+    gather_us = _event_timer(lambda: d.gather_probe(x), flush=flush, reps=10)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -862,15 +872,16 @@ def main():
                                      "(diagonal) + 16 n (x, y) (packed)" if d.packed
                                      else "12 nnz + 96 B per warp block + 16 n"),
                      "effective_bytes_model": "12 nnz + 8 (n+1) + 16 n (SURVEY 8(d))",
-                     # the kernel is bound by the L1TEX sector rate of the
-                     # random x gathers, not by HBM: one gather per
-                     # off-diagonal nonzero, measured floor 39.1 us for C4's
-                     # 9.9 M gathers (scripts/micro/gather.cu: 0.87 sectors /
-                     # SM / cycle, independent of grid, cache operator or
-                     # block-local sorting)
-                     "gather_floor_us": 39.1 * (local_nnz - local_rows) / 9917680.0,
-                     "frac_of_gather_floor": (39.1 * (local_nnz - local_rows) / 9917680.0)
-                     / (ms * 1e3)},
+                     # the kernel is bound by the rate at which the SMs get
+                     # random 32-byte sectors of x out of L2 (one gather per
+                     # stored off-diagonal: ~230 G sectors/s on this part,
+                     # whatever the grid, cache operator, lane mapping or a
+                     # shared-memory table of the hub columns),
+                     # not by HBM: gather_floor_us is that gather stream
+                     # alone, timed live on this operator
+                     "gather_floor_us": gather_us,
+                     "frac_of_gather_floor": gather_us / (ms * 1e3),
+                     "gather_gsectors_s": (local_nnz - local_rows) / (gather_us * 1e-6) / 1e9},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
     }

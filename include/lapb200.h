@@ -105,6 +105,11 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
             const double* theta_d, int theta_neg, int ndots,
             const double* const* dvec, const double* q, int64_t ldq, int nq,
             double* out, lg_ws* ws, const int* skip, void* stream);
+/* Measurement aid: runs only the x gathers of the operator's stored column
+ * stream (one per stored off-diagonal; no values, rows or y) -- the floor the
+ * product pays for x[col] alone.  out: one device double (scratch).  For a
+ * panelled operator the probe runs on the full stream (one pass). */
+int lg_spmv_gather_probe(const lg_csr* a, const double* x, double* out, void* stream);
 /* End-to-end call through host buffers: H2D of x, SpMV, D2H of y. */
 int lg_spmv_host(const lg_csr* a, const double* x_h, double* y_h,
                  double* x_dev_scratch, double* y_dev_scratch, void* stream);
@@ -239,7 +244,15 @@ int lg_ic0_destroy(lg_ic0* f);
 /* Greedy colouring in smallest-last order (host).  color[v] in [0, ncolors). */
 int lg_color_smallest_last(int64_t n, const int64_t* row_ptr_h, const int64_t* col_h,
                            int32_t* color, int32_t* ncolors);
+/* n, stored nonzeros of L (diagonal included) and the depth of the factor's
+ * dependency DAG (levels of a plain triangular sweep). */
 int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels);
+/* Depth of the two sweeps as scheduled and the entries they stream: the
+ * device applies a level-merged form of the factor (rows of even levels have
+ * the level below substituted in, reading the right-hand side there), about
+ * half the factor's depth for ~1.5x the entries; LG_IC0_MERGE=0 keeps the
+ * plain sweeps. */
+int lg_ic0_sweep_depth(const lg_ic0* f, int* fwd, int* bwd, int64_t* entries);
 /* z = (L L^T)^{-1} r: sync-free forward sweep on L then backward sweep on
  * L^T, one cooperative persistent kernel each.  The forward result lives in
  * scratch owned by the handle, so applies of one handle must be ordered on

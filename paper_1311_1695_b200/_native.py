@@ -91,6 +91,7 @@ _SIGS = {
     "lg_csr_download": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_spmv": (c_int, [c_p, c_p, c_p, c_dbl, c_p, c_int, c_int, c_p, c_p,
                         c_i64, c_int, c_p, c_p, c_p, c_p]),
+    "lg_spmv_gather_probe": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_spmv_host": (c_int, [c_p, c_p, c_p, c_p, c_p, c_p]),
     "lg_spmm": (c_int, [c_p, c_p, c_p, c_int, c_p]),
     "lg_spmm_rowmajor": (c_int, [c_p, c_p, c_p, c_int, c_p, c_p]),
@@ -110,6 +111,7 @@ _SIGS = {
     "lg_ic0_info": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_ic0_apply": (c_int, [c_p, c_p, c_p, c_p, c_p]),
     "lg_ic0_set_mode": (c_int, [c_p, c_int]),
+    "lg_ic0_sweep_depth": (c_int, [c_p, c_p, c_p, c_p]),
     "lg_ic0_trace": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_ic0_flow_trace": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_ic0_schedule": (c_int, [c_p, c_int, c_p, c_int]),

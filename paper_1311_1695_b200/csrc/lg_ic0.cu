@@ -93,11 +93,17 @@ struct SweepDev {
   void* cdesc = nullptr;          // [ntasks] CtaDesc records (resident sweep)
   int32_t* lhub0 = nullptr;       // [levels + 1] first hub-row id of each level (resident sweep)
   int32_t* hub_prow = nullptr;    // [hub rows] permuted row of each hub row
+  int32_t* ubidx = nullptr;       // unknown -> b index (-1: auxiliary unknown)
+  int32_t* uoidx = nullptr;       // unknown -> output index (-1: none)
+  int32_t n = 0;             // rows of the factor
+  int32_t N = 0;             // unknowns of the sweep (entries with col >= N read the right-hand side)
+  int64_t nent = 0;          // entries the sweep streams (after level merging)
   int32_t ntasks = 0;
   int32_t nparts = 0;        // hub partial slots
   int32_t nsegs = 0;
   int32_t nbar = 0;          // grid barriers per sweep
-  int levels = 0;
+  int levels = 0;            // depth of the sweep's DAG as scheduled (after level merging)
+  int flevels = 0;           // depth of the factor's own DAG
 };
 
 }  // namespace lg
@@ -107,9 +113,8 @@ struct lg_ic0 {
   unsigned long long* trace = nullptr;  // debug timestamps (fwd segs, bwd segs)
   lg::SweepDev fwd, bwd;
   double* diag = nullptr;
-  double* tmp = nullptr;     // forward result
-  int32_t* omap = nullptr;   // permuted factor: factor row -> original row
-  double* zp = nullptr;      // permuted factor: backward result (factor numbering)
+  double* tmp = nullptr;     // forward sweep's unknowns [fwd.N]: its first n are L^{-1} r
+  double* xb = nullptr;      // backward sweep's unknowns [bwd.N]; z is written through oidx
   int grid = 0;
   // dataflow sweeps hand their scratch state to each other: the forward
   // sweep re-arms the backward one (x sentinels, counters, hub slots) and
@@ -218,27 +223,171 @@ static bool ic0_attempt(int64_t n, const std::vector<double>& diag,
 }
 #pragma GCC pop_options
 
-static int dag_levels(int64_t n, const std::vector<int64_t>& rp,
-                      const std::vector<int32_t>& col, bool forward,
-                      std::vector<int32_t>& level) {
-  level.assign((size_t)n, 0);
+// A triangular sweep as the device runs it: N unknowns -- the factor's n rows
+// first, auxiliary partial sums after them -- each computed as
+//     y_u = (b[bidx_u] - sum_k val_k * src_k) / dg_u
+// where an entry's source is an unknown (col < N) or the right-hand side (a
+// "b entry", col = N + index into b; during the transformation -1 - index).
+// `order` is a topological order of the unknowns.  For an auxiliary unknown
+// bidx = -1 (no right-hand side), dg = -1 (y = the plain sum) and oidx = -1.
+struct SweepSys {
+  int64_t n = 0, N = 0;
+  std::vector<int64_t> rp;
+  std::vector<int32_t> col;
+  std::vector<double> val;
+  std::vector<double> dg;
+  std::vector<int32_t> bidx, oidx, order;
+};
+
+static int dag_levels(const SweepSys& s, std::vector<int32_t>& level) {
+  level.assign((size_t)s.N, 0);
   int maxl = 0;
-  if (forward) {
-    for (int64_t i = 0; i < n; ++i) {
-      int l = 0;
-      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) l = std::max(l, level[col[k]] + 1);
-      level[i] = l;
-      maxl = std::max(maxl, l);
+  for (int64_t q = 0; q < s.N; ++q) {
+    const int32_t i = s.order[(size_t)q];
+    int l = 0;
+    for (int64_t k = s.rp[(size_t)i]; k < s.rp[(size_t)i + 1]; ++k) {
+      const int32_t c = s.col[(size_t)k];   // b entries: negative, or >= N once encoded
+      if (c >= 0 && c < s.N) l = std::max(l, level[(size_t)c] + 1);
     }
-  } else {
-    for (int64_t i = n - 1; i >= 0; --i) {
-      int l = 0;
-      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) l = std::max(l, level[col[k]] + 1);
-      level[i] = l;
-      maxl = std::max(maxl, l);
+    level[(size_t)i] = l;
+    maxl = std::max(maxl, l);
+  }
+  return s.N ? maxl + 1 : 0;
+}
+
+// Level merging (one pass takes ~30 % off the depth of a sweep's dependency
+// DAG for ~20 % more entries).  A sweep's time is its DAG depth times the
+// dependency hop (~1.6 us), not its bytes, and on power-law graphs the long
+// chains run through hub rows.  Two rewrites, both exact in real arithmetic:
+//  * split: an odd-level unknown j with at least kSplitMin inputs below the
+//    level just under it gets an auxiliary unknown p_j = sum of those early
+//    terms (ready a level sooner); row j keeps p_j and its late inputs.
+//  * substitute: in a row i of an even level every input j on the level just
+//    below is replaced by j's own equation, a_ij y_j = c b_j - c p_j -
+//    sum_late c a_jk y_k with c = a_ij / d_j (short rows j without a p_j are
+//    substituted whole; long ones stay and keep their hop).  Row i then reads
+//    the right-hand side at j -- a b entry, which never waits -- and inputs two
+//    levels down: even rows chain to even rows.
+// The rewritten system has the same form, so passes compose (LG_IC0_MERGE
+// passes, default 2; 0 keeps the factor's own sweep).  Results equal the plain
+// sweep's to roundoff (coefficient products are rounded once on the host), not
+// bitwise.
+constexpr int64_t kMergeLen = 16;   // rows up to this long are substituted whole
+constexpr int64_t kSplitMin = 4;    // early inputs that earn an auxiliary unknown
+
+static void merge_levels(SweepSys& s) {
+  std::vector<int32_t> level;
+  dag_levels(s, level);
+  const int64_t N = s.N;
+  auto early = [&](int64_t j, int64_t k) {   // entry k of row j is not on the level just below
+    const int32_t c = s.col[(size_t)k];
+    return c < 0 || level[(size_t)c] < level[(size_t)j] - 1;
+  };
+  std::vector<int32_t> aux((size_t)N, -1);
+  int64_t na = 0;
+  for (int64_t q = 0; q < N; ++q) {
+    const int32_t j = s.order[(size_t)q];
+    if (!(level[(size_t)j] & 1)) continue;
+    int64_t ne = 0;
+    for (int64_t k = s.rp[(size_t)j]; k < s.rp[(size_t)j + 1]; ++k) ne += early(j, k);
+    if (ne >= kSplitMin) aux[(size_t)j] = (int32_t)(N + na++);
+  }
+  const int64_t NN = N + na;
+  // how an entry (i, k) of an even-level row is rewritten
+  auto subst = [&](int64_t i, int64_t k) {
+    const int32_t j = s.col[(size_t)k];
+    if (j < 0 || (level[(size_t)i] & 1) || level[(size_t)j] != level[(size_t)i] - 1) return 0;
+    if (aux[(size_t)j] >= 0) return 2;                                   // through p_j
+    return s.rp[(size_t)j + 1] - s.rp[(size_t)j] <= kMergeLen ? 1 : 0;   // whole row
+  };
+  std::vector<int64_t> nrp((size_t)NN + 1, 0);
+  for (int64_t i = 0; i < N; ++i) {
+    int64_t len = 0;
+    if (aux[(size_t)i] >= 0) {
+      int64_t ne = 0;
+      for (int64_t k = s.rp[(size_t)i]; k < s.rp[(size_t)i + 1]; ++k) ne += early(i, k);
+      len = 1 + (s.rp[(size_t)i + 1] - s.rp[(size_t)i] - ne);
+      nrp[(size_t)aux[(size_t)i] + 1] = ne;
+    } else {
+      for (int64_t k = s.rp[(size_t)i]; k < s.rp[(size_t)i + 1]; ++k) {
+        const int how = subst(i, k);
+        if (!how) {
+          ++len;
+          continue;
+        }
+        const int32_t j = s.col[(size_t)k];
+        len += s.bidx[(size_t)j] >= 0;
+        if (how == 1) {
+          len += s.rp[(size_t)j + 1] - s.rp[(size_t)j];
+        } else {
+          ++len;
+          for (int64_t q = s.rp[(size_t)j]; q < s.rp[(size_t)j + 1]; ++q) len += !early(j, q);
+        }
+      }
+    }
+    nrp[(size_t)i + 1] = len;
+  }
+  for (int64_t i = 0; i < NN; ++i) nrp[(size_t)i + 1] += nrp[(size_t)i];
+  std::vector<int32_t> ncol((size_t)nrp[(size_t)NN]);
+  std::vector<double> nval((size_t)nrp[(size_t)NN]);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t i = 0; i < N; ++i) {
+    int64_t w = nrp[(size_t)i];
+    auto put = [&](int32_t c, double v) {
+      ncol[(size_t)w] = c;
+      nval[(size_t)w++] = v;
+    };
+    if (aux[(size_t)i] >= 0) {
+      int64_t wa = nrp[(size_t)aux[(size_t)i]];
+      put(aux[(size_t)i], 1.0);
+      for (int64_t k = s.rp[(size_t)i]; k < s.rp[(size_t)i + 1]; ++k) {
+        if (early(i, k)) {
+          ncol[(size_t)wa] = s.col[(size_t)k];
+          nval[(size_t)wa++] = s.val[(size_t)k];
+        } else {
+          put(s.col[(size_t)k], s.val[(size_t)k]);
+        }
+      }
+      continue;
+    }
+    for (int64_t k = s.rp[(size_t)i]; k < s.rp[(size_t)i + 1]; ++k) {
+      const int how = subst(i, k);
+      const int32_t j = s.col[(size_t)k];
+      if (!how) {
+        put(j, s.val[(size_t)k]);
+        continue;
+      }
+      const double c = s.val[(size_t)k] / s.dg[(size_t)j];
+      if (s.bidx[(size_t)j] >= 0) put(-1 - s.bidx[(size_t)j], c);
+      if (how == 2) put(aux[(size_t)j], -c);
+      for (int64_t q = s.rp[(size_t)j]; q < s.rp[(size_t)j + 1]; ++q)
+        if (how == 1 || !early(j, q)) put(s.col[(size_t)q], -(c * s.val[(size_t)q]));
     }
   }
-  return n ? maxl + 1 : 0;
+  std::vector<int32_t> norder;
+  norder.reserve((size_t)NN);
+  for (int64_t q = 0; q < N; ++q) {
+    const int32_t u = s.order[(size_t)q];
+    if (aux[(size_t)u] >= 0) norder.push_back(aux[(size_t)u]);
+    norder.push_back(u);
+  }
+  s.dg.resize((size_t)NN, -1.0);
+  s.bidx.resize((size_t)NN, -1);
+  s.oidx.resize((size_t)NN, -1);
+  s.N = NN;
+  s.rp.swap(nrp);
+  s.col.swap(ncol);
+  s.val.swap(nval);
+  s.order.swap(norder);
+}
+
+static int merge_passes() {
+  static int p = -1;
+  if (p < 0) {
+    const char* e = getenv("LG_IC0_MERGE");
+    p = e ? std::max(0, std::min(4, atoi(e))) : 2;
+  }
+  return p;
 }
 
 // Lanes per row.  On wide levels (many more rows than warps) tasks are
@@ -281,12 +430,14 @@ struct SweepHost {
 // 32-lane table of (start, count) so staging a task is one level of
 // independent loads.  Levels with at most `narrow_tasks` tasks run on the
 // first cluster only.
-static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
-                        const std::vector<int32_t>& col, const std::vector<double>& val,
-                        const std::vector<double>& diag, bool forward, int narrow_tasks,
-                        SweepHost& h) {
+static void build_sweep(const SweepSys& sys, int narrow_tasks, SweepHost& h) {
+  const int64_t n = sys.N;   // unknowns of the scheduled system
+  const std::vector<int64_t>& rp = sys.rp;
+  const std::vector<int32_t>& col = sys.col;
+  const std::vector<double>& val = sys.val;
+  const std::vector<double>& diag = sys.dg;
   std::vector<int32_t> level;
-  h.levels = dag_levels(n, rp, col, forward, level);
+  h.levels = dag_levels(sys, level);
   const int nl = h.levels;
   std::vector<int64_t> lcount((size_t)nl + 1, 0);
   for (int64_t i = 0; i < n; ++i) lcount[(size_t)level[(size_t)i] + 1]++;
@@ -305,7 +456,7 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
   {
     std::vector<int64_t> fill(lcount.begin(), lcount.end() - 1);
     for (int64_t k = 0; k < n; ++k) {
-      const int64_t i = forward ? k : n - 1 - k;
+      const int64_t i = sys.order[(size_t)k];
       h.perm[(size_t)fill[(size_t)level[(size_t)i]]++] = (int32_t)i;
     }
   }
@@ -430,6 +581,13 @@ static void build_sweep(int64_t n, const std::vector<int64_t>& rp,
 }
 
 // ----------------------------------------------------------- device side --
+// Source of entry `col` of a sweep: the solution vector, or -- a b entry of a
+// level-merged row (col >= n) -- the right-hand side.
+__device__ __forceinline__ const double* entry_src(const double* x, const double* b, int32_t n,
+                                                   int32_t col) {
+  return (col >= n ? b - n : x) + col;
+}
+
 struct SweepArgs {
   const int64_t* prp;
   const int32_t* pcol;
@@ -450,12 +608,13 @@ struct SweepArgs {
   unsigned long long* bar;
   const double* b;
   double* x;
-  const int32_t* bmap;   // b index of a row (permuted factor: original row) or NULL
-  double* out2;          // second output in original numbering (or NULL)
-  const int32_t* omap;   // original index of a row for out2
+  const int32_t* bmap;   // unknown -> b index (-1: none)
+  double* out2;          // the sweep's output vector (or NULL)
+  const int32_t* omap;   // unknown -> index in out2 (-1: none)
   const int* skip;
   unsigned long long* trace;  // optional: globaltimer after every segment (CTA 0)
   int dbg;                    // timing experiments only (LG_SWEEP_DBG)
+  int32_t n;
 };
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
@@ -509,7 +668,8 @@ __device__ __forceinline__ void stage2(const SweepArgs& a, const Stage1& s1, int
       const int64_t p = tk.p + g;
       st.row = a.perm[p];
       st.dg = a.pdiag[p];
-      st.bv = a.b[a.bmap ? a.bmap[st.row] : st.row];
+      const int32_t bi = a.bmap[st.row];
+      st.bv = bi >= 0 ? a.b[bi] : 0.0;   // auxiliary unknowns have no right-hand side
     }
   } else {
     st.row = tk.p;
@@ -542,7 +702,7 @@ __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int
   } else {
 #pragma unroll
     for (int e = 0; e < kLaneMax; ++e)
-      if (e < st.ne) s += st.val[e] * __ldcg(a.x + st.col[e]);
+      if (e < st.ne) s += st.val[e] * __ldcg(entry_src(a.x, a.b, a.n, st.col[e]));
   }
   if (st.info != 0) {
     const int L = st.info >> 8, cnt = st.info & 0xff;
@@ -550,7 +710,10 @@ __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int
     if ((lane / L) < cnt && (lane % L) == 0 && !(a.dbg & 8)) {
       const double v = (st.bv - s) / st.dg;
       a.x[st.row] = v;
-      if (a.out2) a.out2[a.omap[st.row]] = v;
+      if (a.out2) {
+        const int32_t oi = a.omap[st.row];
+        if (oi >= 0) a.out2[oi] = v;
+      }
     }
     return;
   }
@@ -573,9 +736,13 @@ __device__ __forceinline__ void finish(const SweepArgs& a, const Staged& st, int
     if (lane == 0) {
       a.hub_ticket[st.d] = 0u;
       const int32_t row = a.perm[st.row];
-      const double v = (a.b[a.bmap ? a.bmap[row] : row] - t) / a.pdiag[st.row];
+      const int32_t bi = a.bmap[row];
+      const double v = ((bi >= 0 ? a.b[bi] : 0.0) - t) / a.pdiag[st.row];
       a.x[row] = v;
-      if (a.out2) a.out2[a.omap[row]] = v;
+      if (a.out2) {
+        const int32_t oi = a.omap[row];
+        if (oi >= 0) a.out2[oi] = v;
+      }
     }
   }
 }
@@ -756,7 +923,10 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
 // only on tasks of lower levels, which precede it in their own warps' lists,
 // and the cooperative launch keeps all warps resident.
 constexpr unsigned long long kSentinel = ~0ull;
-constexpr int kFlowThreads = 384;   // 1 poller + 11 worker warps, one CTA per SM
+#ifndef LG_FLOW_THREADS
+#define LG_FLOW_THREADS 384
+#endif
+constexpr int kFlowThreads = LG_FLOW_THREADS;   // 1 poller + 11 worker warps, one CTA per SM
 
 struct FlowArgs {
   const int32_t* pcol;
@@ -785,6 +955,13 @@ struct FlowArgs {
   int32_t levels;
   int32_t gate;
   uint32_t backoff;   // max poll back-off (ns)
+  int32_t n;          // unknowns of this sweep (entries with col >= n read b)
+  int32_t nreal;      // rows of the factor (unknowns beyond are auxiliary)
+  int32_t next_n;     // unknowns of the other sweep (length of next_x)
+  // next_x is this sweep's own right-hand side (the backward sweep re-arming
+  // the forward scratch): level-merged rows read b at other rows too, so the
+  // rows are re-armed once the whole sweep is complete, not one by one
+  int32_t defer_rearm;
 };
 
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
@@ -882,10 +1059,15 @@ __device__ __forceinline__ void fstage2(const A& a, const FStage1& s, int lane, 
 
 __device__ __forceinline__ void publish(const FlowArgs& a, int32_t p, const RowInfo& ri, double v) {
   st_relaxed_f64(a.x + ri.xrow, v);
-  if (a.out2) a.out2[a.oidx[p]] = v;
-  // this row's b has been consumed (by this thread, once): re-arm the row in
-  // the other sweep's x.  Safe when that buffer aliases b (z == r).
-  a.next_x[ri.xrow] = __longlong_as_double((long long)kSentinel);
+  if (a.out2) {
+    const int32_t oi = a.oidx[p];
+    if (oi >= 0) a.out2[oi] = v;
+  }
+  // this row's b has been consumed: re-arm the row in the other sweep's x
+  // (unless that buffer is this sweep's b, which merged rows still read)
+  // (the other sweep's auxiliary unknowns are re-armed in this kernel's prologue)
+  if (!a.defer_rearm && ri.xrow < a.nreal)
+    a.next_x[ri.xrow] = __longlong_as_double((long long)kSentinel);
 }
 
 __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& st, int lane,
@@ -893,14 +1075,14 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
   const bool owner = st.info != 0 ? (st.p >= 0 && (lane & ((1 << st.sh) - 1)) == 0)
                                   : (st.c == 0 && lane == 0);
   double bv = 0.0;
-  if (owner) bv = a.b[st.ri.bidx];
+  if (owner && st.ri.bidx >= 0) bv = a.b[st.ri.bidx];
   double xv[kLaneMax];
   unsigned miss = 0;
 #pragma unroll
   for (int e = 0; e < kLaneMax; ++e) {
     if (e < st.ne) {
-      xv[e] = ld_relaxed_f64(a.x + st.col[e]);
-      if (is_sentinel(xv[e])) miss |= 1u << e;
+      xv[e] = ld_relaxed_f64(entry_src(a.x, a.b, a.n, st.col[e]));
+      if (st.col[e] < a.n && is_sentinel(xv[e])) miss |= 1u << e;   // b entries never wait
     }
   }
   unsigned spins = 0, nap = 16;
@@ -1024,13 +1206,15 @@ __global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a)
   __syncthreads();
   const int gate = a.gate;
   if (warp == 0) {   // level watcher
-    for (int L = 0; L < a.levels - gate; ++L) {
+    // (a deferred re-arm waits for the whole sweep: watch through the last level)
+    const int lend = a.defer_rearm ? a.levels : a.levels - gate;
+    for (int L = 0; L < lend; ++L) {
       const int idx = L * 32 + lane;
       const unsigned want = (unsigned)a.lexpect[idx];
       while (true) {
         const unsigned v = ld_relaxed_u32(a.lcount + idx);
         if (__all_sync(0xffffffffu, v >= want)) break;
-        if (s_active == 0) return;
+        if (s_active == 0 && !a.defer_rearm) return;
         __nanosleep(32);
       }
       s_done = L;
@@ -1045,6 +1229,9 @@ __global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a)
     for (int64_t i = i0; i < a.next_ncnt; i += stride) a.next_cnt[i] = 0u;
     for (int64_t i = i0; i < a.next_npart; i += stride)
       a.next_part[i] = __longlong_as_double((long long)kSentinel);
+    if (!a.defer_rearm)
+      for (int64_t i = a.nreal + i0; i < a.next_n; i += stride)
+        a.next_x[i] = __longlong_as_double((long long)kSentinel);
   }
   int64_t t = (int64_t)blockIdx.x * kWorkers + warp - 1;
   if (t < nt) {
@@ -1074,9 +1261,20 @@ __global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a)
     }
   }
   __syncwarp();
+  if (a.defer_rearm) {
+    // every task of the sweep is complete (its b is no longer read): re-arm
+    // this CTA's share of the other sweep's x
+    for (unsigned spins = 0; s_done < a.levels - 1; ++spins) {
+      __nanosleep(64);
+      if (spins > (1u << 26)) __trap();
+    }
+    const int64_t i0 = (int64_t)blockIdx.x * (kFlowThreads - 32) + threadIdx.x - 32;
+    const int64_t stride = (int64_t)gridDim.x * (kFlowThreads - 32);
+    for (int64_t i = i0; i < a.next_n; i += stride)
+      a.next_x[i] = __longlong_as_double((long long)kSentinel);
+  }
   if (lane == 0) atomicSub((int*)&s_active, 1);
 }
-
 
 // ---- resident sweep (narrow DAGs: one CTA runs the whole apply) -------------
 // On a factor whose levels are narrow (C1: ~90 rows a level, C2: ~200, C3:
@@ -1129,6 +1327,7 @@ struct CtaDir {
   unsigned long long* ttrace;   // debug: per task {start, inputs ready, done}
   int32_t ntasks;
   int32_t levels;
+  int32_t n;
 };
 
 struct CtaArgs {
@@ -1168,7 +1367,10 @@ __device__ __forceinline__ void cta_publish(const CtaDir& a, int32_t p, const Ro
                                             double v) {
   if (__double_as_longlong(v) == (long long)kSentinel) v = __longlong_as_double(0x7ff8000000000000ll);
   a.x[ri.xrow] = v;
-  if (a.out2) a.out2[a.oidx[p]] = v;
+  if (a.out2) {
+    const int32_t oi = a.oidx[p];
+    if (oi >= 0) a.out2[oi] = v;
+  }
 }
 
 // One staged task: same entry order per lane, same butterfly, same division as
@@ -1189,7 +1391,7 @@ __device__ __forceinline__ void cta_complete(const CtaDir& a, const CtaDesc& d, 
     owner = (lane >> sh) < cnt && (lane & (L - 1)) == 0;
     if (owner) {
       ri = ris[lane >> sh];
-      bv = a.b[ri.bidx];
+      if (ri.bidx >= 0) bv = a.b[ri.bidx];
     }
   }
   double xv[kLaneMax], vv[kLaneMax];
@@ -1197,7 +1399,7 @@ __device__ __forceinline__ void cta_complete(const CtaDir& a, const CtaDesc& d, 
   for (int e = 0; e < kLaneMax; ++e) {
     if (e < ne) {
       const int k = rel + (e << sh);
-      xv[e] = a.x[col[k]];
+      xv[e] = *entry_src(a.x, a.b, a.n, col[k]);
       vv[e] = val[k];
     }
   }
@@ -1271,7 +1473,7 @@ __device__ __forceinline__ void cta_level_end(const CtaDir& a, CtaShared& sh, Ct
       double t = 0.0;
       for (int32_t c = lane; c < nch; c += 32) t += a.hub_part[first + c];
       t = warp_sum(t);
-      if (lane == 0) cta_publish(a, p, ri, (a.b[ri.bidx] - t) / ri.dg);
+      if (lane == 0) cta_publish(a, p, ri, ((ri.bidx >= 0 ? a.b[ri.bidx] : 0.0) - t) / ri.dg);
     }
     lvl_arrive(&sh.bar, lane);
     lvl_wait(&sh.bar, sy.phase & 1u);
@@ -1430,15 +1632,42 @@ static SweepLaunch& sweep_launch() {
 
 // omap (permuted factor, else NULL): factor row -> original row; the forward
 // sweep reads b there and the backward sweep writes its second output there.
-static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
-                       const std::vector<int32_t>& col, const std::vector<double>& val,
-                       const std::vector<double>& diag, bool forward, const int32_t* omap,
-                       SweepDev& d) {
+// omap (permuted factor, else NULL): factor row -> original row; the forward
+// sweep reads b there and the backward sweep writes z there.  The backward
+// sweep's right-hand side is the forward sweep's solution (factor numbering).
+static bool make_sweep(int64_t n, std::vector<int64_t>& rp, std::vector<int32_t>& col,
+                       std::vector<double>& val, const std::vector<double>& diag, bool forward,
+                       const int32_t* omap, SweepDev& d) {
+  SweepSys sys;
+  sys.n = sys.N = n;
+  sys.rp.swap(rp);
+  sys.col.swap(col);
+  sys.val.swap(val);
+  sys.dg = diag;
+  sys.bidx.resize((size_t)n);
+  sys.oidx.resize((size_t)n);
+  sys.order.resize((size_t)n);
+  for (int64_t r = 0; r < n; ++r) {
+    sys.bidx[(size_t)r] = (int32_t)((forward && omap) ? omap[r] : r);
+    sys.oidx[(size_t)r] = forward ? -1 : (int32_t)(omap ? omap[r] : r);
+    sys.order[(size_t)r] = (int32_t)(forward ? r : n - 1 - r);
+  }
+  {
+    std::vector<int32_t> lv;
+    d.flevels = dag_levels(sys, lv);
+  }
+  for (int p = 0; p < merge_passes() && 3 * sys.N < ((int64_t)1 << 31); ++p) merge_levels(sys);
+  // b entries: -1 - index  ->  N + index (entry_src on the device)
+  for (int32_t& c : sys.col)
+    if (c < 0) c = (int32_t)(sys.N + (-1 - (int64_t)c));
   SweepHost h;
+  d.n = (int32_t)n;
+  d.N = (int32_t)sys.N;
+  d.nent = (int64_t)sys.col.size();
   const SweepLaunch& L = sweep_launch();
   const char* nm = getenv("LG_NARROW_MULT");
   const int mult = nm ? atoi(nm) : 1;
-  build_sweep(n, rp, col, val, diag, forward, L.csize * kSweepWarps * mult, h);
+  build_sweep(sys, L.csize * kSweepWarps * mult, h);
   d.nsegs = (int32_t)h.segs.size();
   d.nbar = h.nbar;
   d.levels = h.levels;
@@ -1467,17 +1696,16 @@ static bool make_sweep(int64_t n, const std::vector<int64_t>& rp,
   }
   d.nparts = h.nparts;
   {
-    std::vector<RowInfo> ri((size_t)n);
-    std::vector<int32_t> oi;
-    for (int64_t p = 0; p < n; ++p) {
+    std::vector<RowInfo> ri((size_t)sys.N);
+    std::vector<int32_t> oi((size_t)sys.N);
+    for (int64_t p = 0; p < sys.N; ++p) {
       const int32_t r = h.perm[(size_t)p];
-      ri[(size_t)p] = {h.pdiag[(size_t)p], r, (forward && omap) ? omap[r] : r};
+      ri[(size_t)p] = {h.pdiag[(size_t)p], r, sys.bidx[(size_t)r]};
+      oi[(size_t)p] = sys.oidx[(size_t)r];
     }
-    if (!forward && omap) {
-      oi.resize((size_t)n);
-      for (int64_t p = 0; p < n; ++p) oi[(size_t)p] = omap[h.perm[(size_t)p]];
-    }
-    ok = ok && upload(&d.rinfo, ri) && upload(&d.oidx, oi);
+    // (the level-barrier kernel indexes b and the output by unknown)
+    ok = ok && upload(&d.rinfo, ri) && upload(&d.oidx, oi) && upload(&d.ubidx, sys.bidx) &&
+         upload(&d.uoidx, sys.oidx);
   }
   if (ok && !h.lexpect.empty())
     ok = cudaMalloc(&d.lcount, 4 * h.lexpect.size()) == cudaSuccess &&
@@ -1519,6 +1747,8 @@ static void free_sweep(SweepDev& d) {
   cudaFree(d.lhub0);
   cudaFree(d.hub_prow);
   cudaFree(d.cdesc);
+  cudaFree(d.ubidx);
+  cudaFree(d.uoidx);
   d = SweepDev();
 }
 
@@ -1543,13 +1773,14 @@ static SweepArgs sweep_args(const SweepDev& d, const double* b, double* x, const
   a.bar = d.bar;
   a.b = b;
   a.x = x;
-  a.bmap = nullptr;
+  a.bmap = d.ubidx;
   a.out2 = nullptr;
-  a.omap = nullptr;
+  a.omap = d.uoidx;
   a.skip = skip;
   a.trace = nullptr;
   const char* dbg = getenv("LG_SWEEP_DBG");
   a.dbg = dbg ? atoi(dbg) : 0;
+  a.n = d.N;
   return a;
 }
 
@@ -1610,6 +1841,10 @@ static int launch_flow(const SweepDev& dv, const SweepDev& other, const double* 
   a.next_npart = other.nparts;
   a.ntasks = dv.ntasks;
   a.levels = dv.levels;
+  a.n = dv.N;
+  a.nreal = dv.n;
+  a.next_n = other.N;
+  a.defer_rearm = next_x == b;
   a.gate = sweep_gate();
   {
     const char* e = getenv("LG_SWEEP_BACKOFF");
@@ -1646,6 +1881,7 @@ static CtaDir cta_dir(const SweepDev& dv, const double* b, double* x, double* ou
   a.ttrace = dv.ttrace;
   a.ntasks = dv.ntasks;
   a.levels = dv.levels;
+  a.n = dv.N;
   return a;
 }
 
@@ -1854,11 +2090,11 @@ int lg_ic0_create_perm(int64_t n, const int64_t* l_rp, const int64_t* l_col,
   f->nnz_l = nnz;
   bool ok = make_sweep(n, frp, fcol, fval, dg, true, omp, f->fwd) &&
             make_sweep(n, brp, bcol, bval, dg, false, omp, f->bwd) && upload(&f->diag, dg) &&
-            (n == 0 || cudaMalloc(&f->tmp, 8 * (size_t)n) == cudaSuccess);
-  if (ok && perm_h)
-    ok = upload(&f->omap, om) && cudaMalloc(&f->zp, 8 * (size_t)n) == cudaSuccess;
+            (n == 0 || (cudaMalloc(&f->tmp, 8 * (size_t)f->fwd.N) == cudaSuccess &&
+                        cudaMalloc(&f->xb, 8 * (size_t)f->bwd.N) == cudaSuccess));
   if (ok && n) {   // arm the dataflow forward sweep (all-ones = the x sentinel)
-    ok = cudaMemset(f->tmp, 0xff, 8 * (size_t)n) == cudaSuccess;
+    ok = cudaMemset(f->tmp, 0xff, 8 * (size_t)f->fwd.N) == cudaSuccess &&
+         cudaMemset(f->xb, 0xff, 8 * (size_t)f->bwd.N) == cudaSuccess;
     for (SweepDev* d : {&f->fwd, &f->bwd})
       if (ok && d->nparts)
         ok = cudaMemset(d->hub_part, 0xff, 8 * (size_t)d->nparts) == cudaSuccess;
@@ -2048,8 +2284,7 @@ int lg_ic0_destroy(lg_ic0* f) {
   free_sweep(f->bwd);
   cudaFree(f->diag);
   cudaFree(f->tmp);
-  cudaFree(f->omap);
-  cudaFree(f->zp);
+  cudaFree(f->xb);
   delete f;
   return LG_OK;
 }
@@ -2058,7 +2293,15 @@ int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels) {
   if (!f) return fail(LG_EINVAL, "lg_ic0_info: NULL handle");
   if (n) *n = f->n;
   if (nnz_l) *nnz_l = f->nnz_l;
-  if (levels) *levels = std::max(f->fwd.levels, f->bwd.levels);
+  if (levels) *levels = std::max(f->fwd.flevels, f->bwd.flevels);
+  return LG_OK;
+}
+
+int lg_ic0_sweep_depth(const lg_ic0* f, int* fwd, int* bwd, int64_t* entries) {
+  if (!f) return fail(LG_EINVAL, "lg_ic0_sweep_depth: NULL handle");
+  if (fwd) *fwd = f->fwd.levels;
+  if (bwd) *bwd = f->bwd.levels;
+  if (entries) *entries = f->fwd.nent + f->bwd.nent;
   return LG_OK;
 }
 
@@ -2067,39 +2310,36 @@ int lg_ic0_apply(const lg_ic0* f, const double* r, double* z, const int* skip,
   if (!f || !r || !z) return fail(LG_EINVAL, "lg_ic0_apply: NULL argument");
   if (f->n == 0) return LG_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  SweepArgs fa = sweep_args(f->fwd, r, f->tmp, skip);
-  SweepArgs ba = sweep_args(f->bwd, f->tmp, f->omap ? f->zp : z, skip);
-  if (f->omap) {
-    // permuted factor: read r at original rows, write z at original rows
-    fa.bmap = f->omap;
-    ba.out2 = z;
-    ba.omap = f->omap;
-  }
-  if (f->trace) {
-    // layout: fwd segs, fwd inline-stage counter, bwd segs, bwd counter
-    fa.trace = f->trace;
-    ba.trace = f->trace + f->fwd.nsegs + 1;
-  }
+  // forward: b = r, unknowns in tmp; backward: b = tmp, unknowns in xb, z
+  // written through the sweep's output map.  r is only read by the forward
+  // launch, so z may alias r.
   if (f->cta_mode && sweep_mode() != 0 && !f->trace) {
-    double* zx = f->omap ? f->zp : z;
     CtaArgs ca;
     ca.dir[0] = cta_dir(f->fwd, r, f->tmp, nullptr);
-    ca.dir[1] = cta_dir(f->bwd, f->tmp, zx, f->omap ? z : nullptr);
+    ca.dir[1] = cta_dir(f->bwd, f->tmp, f->xb, z);
     ca.skip = skip;
     f->flow_armed = false;   // tmp now holds values, not the dataflow sentinels
     return launch_cta(ca, f->cta_threads, s);
   }
   if (sweep_mode() != 0 && !f->trace) {
-    double* zx = f->omap ? f->zp : z;
-    if (!f->flow_armed) {   // arm the forward sweep (creation, or after a barrier apply)
-      flow_init_kernel<<<vec_grid(f->n), kThreads, 0, s>>>(
-          f->tmp, f->n, f->fwd.lcount, f->fwd.levels * 32, f->fwd.hub_part, f->fwd.nparts, nullptr);
+    if (!f->flow_armed) {   // arm the forward sweep (after a barrier / resident apply)
+      flow_init_kernel<<<vec_grid(f->fwd.N), kThreads, 0, s>>>(
+          f->tmp, f->fwd.N, f->fwd.lcount, f->fwd.levels * 32, f->fwd.hub_part, f->fwd.nparts,
+          nullptr);
       LG_CUDA(cudaGetLastError());
       f->flow_armed = true;
     }
-    int rc = launch_flow(f->fwd, f->bwd, r, f->tmp, nullptr, zx, skip, s);
+    int rc = launch_flow(f->fwd, f->bwd, r, f->tmp, nullptr, f->xb, skip, s);
     if (rc) return rc;
-    return launch_flow(f->bwd, f->fwd, f->tmp, zx, f->omap ? z : nullptr, f->tmp, skip, s);
+    return launch_flow(f->bwd, f->fwd, f->tmp, f->xb, z, f->tmp, skip, s);
+  }
+  SweepArgs fa = sweep_args(f->fwd, r, f->tmp, skip);
+  SweepArgs ba = sweep_args(f->bwd, f->tmp, f->xb, skip);
+  ba.out2 = z;
+  if (f->trace) {
+    // layout: fwd segs, fwd inline-stage counter, bwd segs, bwd counter
+    fa.trace = f->trace;
+    ba.trace = f->trace + f->fwd.nsegs + 1;
   }
   f->flow_armed = false;
   int rc = launch_sweep(fa, s);

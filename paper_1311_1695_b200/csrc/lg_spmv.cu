@@ -490,6 +490,24 @@ __global__ void __launch_bounds__(256) long_finish_kernel(SpmvArgs a) {
   }
 }
 
+// Measurement aid (lg_spmv_gather_probe): the x gathers of an operator's
+// off-diagonal stream and nothing else -- no values, no row structure, no y --
+// eight independent gathers in flight per thread.  Its time is the floor any
+// SpMV on this stream pays for x[col] alone (bench.py reports the product
+// against it next to the HBM roofline).
+__global__ void __launch_bounds__(256) gather_probe_kernel(const uint32_t* __restrict__ words,
+                                                            uint32_t cmask, int64_t m,
+                                                            const double* __restrict__ x,
+                                                            double* out) {
+  double s = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+#pragma unroll 8
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride)
+    s += __ldg(x + (__ldcs(words + e) & cmask));
+  // keep the loads alive without a store per thread
+  if (s == 12345.678) *out = s;
+}
+
 // Build the warp-block schedule on the host.
 // absent (optional): rows left out of the schedule altogether (y is not
 // written there) -- the row block of one rank in the row-partitioned
@@ -1108,6 +1126,20 @@ int lg_spmv(const lg_csr* a, const double* x, double* y, double theta_h,
   f.result = out;
   f.skip = skip;
   return lg_fused(&f, ws, stream);
+}
+
+int lg_spmv_gather_probe(const lg_csr* a, const double* x, double* out, void* stream) {
+  if (!a || !x || !out) return fail(LG_EINVAL, "lg_spmv_gather_probe: NULL argument");
+  if (a->n == 0) return LG_OK;
+  const uint32_t* words = a->packed ? a->pcol : reinterpret_cast<const uint32_t*>(a->col);
+  const int64_t m = a->packed ? a->noff : a->nnz;
+  const uint32_t cmask =
+      a->packed ? (a->cbits >= 32 ? 0xffffffffu : ((1u << a->cbits) - 1u)) : 0xffffffffu;
+  if (!words || m <= 0) return LG_OK;
+  gather_probe_kernel<<<dev_info().sm_count * 8, 256, 0, (cudaStream_t)stream>>>(words, cmask, m,
+                                                                                  x, out);
+  LG_LAUNCH_CHECK("gather_probe_kernel");
+  return LG_OK;
 }
 
 }  // extern "C"

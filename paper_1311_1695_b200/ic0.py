@@ -57,6 +57,11 @@ class DeviceIc0:
         nat.call("lg_ic0_info", h, ctypes.byref(n_), ctypes.byref(nnz), ctypes.byref(lev))
         self.nnz_l = nnz.value
         self.levels = lev.value
+        fw, bw, ent = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        nat.call("lg_ic0_sweep_depth", h, ctypes.byref(fw), ctypes.byref(bw), ctypes.byref(ent))
+        # depth and entries of the sweeps as scheduled (level-merged form)
+        self.sweep_levels = (fw.value, bw.value)
+        self.sweep_entries = ent.value
         # algorithmic bytes of one apply: two sweeps over L
         # (f64 val + int32 col + int64 row_ptr) plus r, y, z traffic
         self.algo_bytes = 2 * (12 * self.nnz_l + 8 * (self.n + 1)) + 32 * self.n

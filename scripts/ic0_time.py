@@ -15,5 +15,9 @@ for name in sys.argv[1:] or ["C1", "C2", "C3", "C4"]:
     e0.record()
     for _ in range(10): d.apply(x, z)
     e1.record(); torch.cuda.synchronize()
-    want = f.apply(x.cpu().numpy())
-    print(name, "levels", d.levels, "apply %.1f us" % (e0.elapsed_time(e1) * 100), flush=True)
+    from oracle import lapeig_oracle as O
+    want = O.Ic0(a.n, f.l.row_ptr, f.l.col_idx, f.l.values).apply(x.cpu().numpy())
+    err = np.max(np.abs(z.cpu().numpy() - want)) / np.max(np.abs(want))
+    print(name, "levels", d.levels, "sweep depth", d.sweep_levels, "entries", d.sweep_entries,
+          "(factor %d)" % (2 * (d.nnz_l - a.n)), "apply %.1f us" % (e0.elapsed_time(e1) * 100),
+          "err vs oracle apply %.1e" % err, flush=True)

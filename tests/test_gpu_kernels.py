@@ -364,6 +364,22 @@ def test_ic0_resident_sweep_fixtures(L, kat, name):
     assert np.max(np.abs(z1.cpu().numpy() - want)) <= 1e-12 * np.max(np.abs(want))
 
 
+@pytest.mark.parametrize("flags", [0, 1])
+def test_gather_probe_runs(L, flags):
+    """lg_spmv_gather_probe (the bench's gather floor) walks the stored column
+    stream of either format without touching y; it must launch cleanly and
+    leave x alone."""
+    import torch
+    from paper_1311_1695_b200.sparse import DeviceCsr
+    a = L.build_laplacian(L.config_graph("C2"))
+    d = DeviceCsr(a.n, a.row_ptr, a.col_idx, a.values, flags=flags)
+    x = torch.randn(a.n, dtype=torch.float64, device="cuda")
+    x0 = x.clone()
+    d.gather_probe(x)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x0)
+
+
 def test_jacobi_variant(L):
     a = L.build_laplacian(L.config_graph("C1"))
     jf = L.JacobiFactor(a)
