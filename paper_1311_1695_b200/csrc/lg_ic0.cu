@@ -275,10 +275,16 @@ static int dag_levels(const SweepSys& s, std::vector<int32_t>& level) {
 constexpr int64_t kMergeLen = 16;   // rows up to this long are substituted whole
 constexpr int64_t kSplitMin = 4;    // early inputs that earn an auxiliary unknown
 
-static void merge_levels(SweepSys& s) {
+constexpr int64_t kMergeWide = 16384;   // mean rows per level beyond which a sweep is not latency-bound
+
+static bool merge_levels(SweepSys& s) {
   std::vector<int32_t> level;
-  dag_levels(s, level);
+  const int depth = dag_levels(s, level);
   const int64_t N = s.N;
+  // a shallow, wide DAG (the multicolour factor: 26 levels of ~38 k rows on C4)
+  // is bound by its entries, not its depth: merging only adds work there
+  // (measured: C4 multicolour DACG iteration 424 -> 620 us)
+  if (N > kMergeWide * (int64_t)depth) return false;
   auto early = [&](int64_t j, int64_t k) {   // entry k of row j is not on the level just below
     const int32_t c = s.col[(size_t)k];
     return c < 0 || level[(size_t)c] < level[(size_t)j] - 1;
@@ -379,6 +385,7 @@ static void merge_levels(SweepSys& s) {
   s.col.swap(ncol);
   s.val.swap(nval);
   s.order.swap(norder);
+  return true;
 }
 
 static int merge_passes() {
@@ -1656,7 +1663,8 @@ static bool make_sweep(int64_t n, std::vector<int64_t>& rp, std::vector<int32_t>
     std::vector<int32_t> lv;
     d.flevels = dag_levels(sys, lv);
   }
-  for (int p = 0; p < merge_passes() && 3 * sys.N < ((int64_t)1 << 31); ++p) merge_levels(sys);
+  for (int p = 0; p < merge_passes() && 3 * sys.N < ((int64_t)1 << 31); ++p)
+    if (!merge_levels(sys)) break;
   // b entries: -1 - index  ->  N + index (entry_src on the device)
   for (int32_t& c : sys.col)
     if (c < 0) c = (int32_t)(sys.N + (-1 - (int64_t)c));
