@@ -388,13 +388,9 @@ static bool merge_levels(SweepSys& s) {
   return true;
 }
 
-static int merge_passes() {
-  static int p = -1;
-  if (p < 0) {
-    const char* e = getenv("LG_IC0_MERGE");
-    p = e ? std::max(0, std::min(4, atoi(e))) : 2;
-  }
-  return p;
+static int merge_passes() {   // read at every factor creation
+  const char* e = getenv("LG_IC0_MERGE");
+  return e ? std::max(0, std::min(4, atoi(e))) : 2;
 }
 
 // Lanes per row.  On wide levels (many more rows than warps) tasks are
@@ -930,10 +926,13 @@ __global__ void __launch_bounds__(kSweepThreads, 1) sweep_kernel(SweepArgs a) {
 // only on tasks of lower levels, which precede it in their own warps' lists,
 // and the cooperative launch keeps all warps resident.
 constexpr unsigned long long kSentinel = ~0ull;
-#ifndef LG_FLOW_THREADS
-#define LG_FLOW_THREADS 384
-#endif
-constexpr int kFlowThreads = LG_FLOW_THREADS;   // 1 poller + 11 worker warps, one CTA per SM
+// CTA size of the dataflow sweep, one CTA per SM: 1 poller + 11 worker warps
+// (139 registers), or + 15 (128 registers) for schedules with many tasks per
+// level, where resident warps rather than the hop bound the sweep (level-
+// merged C4: 577 -> 551 us; C1-C3 lose 2-4 % with it)
+constexpr int kFlowThreads = 384;
+constexpr int kFlowThreadsWide = 512;
+constexpr int kFlowWideTasks = 512;   // mean tasks per level from which the wide CTA is used
 
 struct FlowArgs {
   const int32_t* pcol;
@@ -1019,6 +1018,7 @@ struct FStaged {
   int32_t p;      // pack: permuted row of the lane's group (-1: idle) | chunk: permuted hub row
   int32_t c, hid; // chunk: chunk index, hub id
   int32_t ne, sh, lev;
+  int32_t oi;     // output index of the owner lane's row (-1: none), staged with the row record
   int32_t col[kLaneMax];
   double val[kLaneMax];
   RowInfo ri;
@@ -1043,16 +1043,22 @@ __device__ __forceinline__ void fstage2(const A& a, const FStage1& s, int lane, 
     const int L = tk.b >> 8, cnt = tk.b & 0xff;
     st.sh = __ffs(L) - 1;
     st.p = -1;
+    st.oi = -1;
     if ((lane >> st.sh) < cnt) {
       st.p = tk.p + (lane >> st.sh);
       st.ri = a.rinfo[st.p];
+      if (a.out2) st.oi = a.oidx[st.p];
     }
   } else {
     st.p = tk.p;
     st.c = tk.c;
     st.hid = tk.d;
     st.sh = 5;
-    if (tk.c == 0) st.ri = a.rinfo[tk.p];
+    st.oi = -1;
+    if (tk.c == 0) {
+      st.ri = a.rinfo[tk.p];
+      if (a.out2) st.oi = a.oidx[tk.p];
+    }
   }
 #pragma unroll
   for (int e = 0; e < kLaneMax; ++e) {
@@ -1064,12 +1070,9 @@ __device__ __forceinline__ void fstage2(const A& a, const FStage1& s, int lane, 
   }
 }
 
-__device__ __forceinline__ void publish(const FlowArgs& a, int32_t p, const RowInfo& ri, double v) {
+__device__ __forceinline__ void publish(const FlowArgs& a, int32_t oi, const RowInfo& ri, double v) {
   st_relaxed_f64(a.x + ri.xrow, v);
-  if (a.out2) {
-    const int32_t oi = a.oidx[p];
-    if (oi >= 0) a.out2[oi] = v;
-  }
+  if (oi >= 0) a.out2[oi] = v;
   // this row's b has been consumed: re-arm the row in the other sweep's x
   // (unless that buffer is this sweep's b, which merged rows still read)
   // (the other sweep's auxiliary unknowns are re-armed in this kernel's prologue)
@@ -1168,9 +1171,9 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
   if (st.info != 0) {
     for (int o = (1 << st.sh) >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
 #ifdef LG_FLOW_RCP
-    if (owner) publish(a, st.p, st.ri, (bv - s) * (1.0 / st.ri.dg));
+    if (owner) publish(a, st.oi, st.ri, (bv - s) * (1.0 / st.ri.dg));
 #else
-    if (owner) publish(a, st.p, st.ri, (bv - s) / st.ri.dg);
+    if (owner) publish(a, st.oi, st.ri, (bv - s) / st.ri.dg);
 #endif
     return;
   }
@@ -1197,9 +1200,10 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
     t += v;
   }
   t = warp_sum(t);
-  if (lane == 0) publish(a, st.p, st.ri, (bv - t) / st.ri.dg);
+  if (lane == 0) publish(a, st.oi, st.ri, (bv - t) / st.ri.dg);
 }
 
+template <int kFlowThreads>
 __global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a) {
   if (a.skip && *a.skip) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1665,6 +1669,38 @@ static bool make_sweep(int64_t n, std::vector<int64_t>& rp, std::vector<int32_t>
   }
   for (int p = 0; p < merge_passes() && 3 * sys.N < ((int64_t)1 << 31); ++p)
     if (!merge_levels(sys)) break;
+  if (!getenv("LG_IC0_NOHUBSORT")) {
+    // A hub row (> kHubChunk entries) is cut into chunk tasks whose partials
+    // chunk 0 sums -- a second hop after the last chunk.  Put the entries whose
+    // sources sit deepest first: the late inputs then belong to chunk 0 itself,
+    // the other chunks (early inputs only) are done long before, and the row
+    // finishes one hop after its last input.  (Summation order changes within
+    // the row: roundoff only, still fixed.)
+    std::vector<int32_t> lv;
+    dag_levels(sys, lv);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t u = 0; u < sys.N; ++u) {
+      const int64_t lo = sys.rp[(size_t)u], hi = sys.rp[(size_t)u + 1];
+      if (hi - lo <= kHubChunk) continue;
+      std::vector<std::pair<int32_t, int64_t>> key((size_t)(hi - lo));
+      for (int64_t k = lo; k < hi; ++k) {
+        const int32_t c = sys.col[(size_t)k];
+        key[(size_t)(k - lo)] = {c < 0 ? -1 : lv[(size_t)c], k};
+      }
+      std::stable_sort(key.begin(), key.end(),
+                       [](const std::pair<int32_t, int64_t>& a, const std::pair<int32_t, int64_t>& b) {
+                         return a.first > b.first;
+                       });
+      std::vector<int32_t> c2((size_t)(hi - lo));
+      std::vector<double> v2((size_t)(hi - lo));
+      for (size_t q = 0; q < key.size(); ++q) {
+        c2[q] = sys.col[(size_t)key[q].second];
+        v2[q] = sys.val[(size_t)key[q].second];
+      }
+      std::copy(c2.begin(), c2.end(), sys.col.begin() + lo);
+      std::copy(v2.begin(), v2.end(), sys.val.begin() + lo);
+    }
+  }
   // b entries: -1 - index  ->  N + index (entry_src on the device)
   for (int32_t& c : sys.col)
     if (c < 0) c = (int32_t)(sys.N + (-1 - (int64_t)c));
@@ -1812,17 +1848,24 @@ static int sweep_gate() {
   return g;
 }
 
-static int launch_flow(const SweepDev& dv, const SweepDev& other, const double* b, double* x,
-                       double* out2, double* next_x, const int* skip, cudaStream_t s) {
+template <int THREADS>
+static int flow_grid() {
   static int grid = 0;
   if (!grid) {
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_flow_kernel, kFlowThreads, 0) !=
-            cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_flow_kernel<THREADS>, THREADS,
+                                                      0) != cudaSuccess ||
         occ < 1)
       occ = 1;
-    grid = occ * dev_info().sm_count;
+    grid = std::min(occ, 1) * dev_info().sm_count;
   }
+  return grid;
+}
+
+static int launch_flow(const SweepDev& dv, const SweepDev& other, const double* b, double* x,
+                       double* out2, double* next_x, const int* skip, cudaStream_t s) {
+  const bool wide = (int64_t)dv.ntasks > (int64_t)kFlowWideTasks * std::max(1, dv.levels);
+  const int grid = wide ? flow_grid<kFlowThreadsWide>() : flow_grid<kFlowThreads>();
   FlowArgs a;
   a.pcol = dv.pcol;
   a.pval = dv.pval;
@@ -1860,14 +1903,15 @@ static int launch_flow(const SweepDev& dv, const SweepDev& other, const double* 
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kFlowThreads);
+  cfg.blockDim = dim3(wide ? kFlowThreadsWide : kFlowThreads);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeCooperative;   // all warps co-resident
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_flow_kernel, a));
+  if (wide) LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_flow_kernel<kFlowThreadsWide>, a));
+  else LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_flow_kernel<kFlowThreads>, a));
   return LG_OK;
 }
 

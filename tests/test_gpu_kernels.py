@@ -364,6 +364,53 @@ def test_ic0_resident_sweep_fixtures(L, kat, name):
     assert np.max(np.abs(z1.cpu().numpy() - want)) <= 1e-12 * np.max(np.abs(want))
 
 
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3"])
+def test_ic0_level_merging(L, cfg, monkeypatch):
+    """The device applies a level-merged form of the factor (odd-level rows
+    split off a partial sum of their early inputs, even-level rows substitute
+    the level below): shallower sweeps, the same z to roundoff -- against the
+    factor's own sweeps (LG_IC0_MERGE=0), against the oracle (ic0.py:40-45),
+    for every pass count, in place, and for a permuted (multicolour) factor."""
+    import torch
+    from paper_1311_1695_b200 import _device as dev
+    from paper_1311_1695_b200.ic0 import DeviceIc0
+    a = L.build_laplacian(L.config_graph(cfg))
+    f = L.ic0_factorize(a)
+    x = np.random.default_rng(11).standard_normal(a.n)
+    xd = torch.from_numpy(x).cuda()
+    zr = O.Ic0(a.n, f.l.row_ptr, f.l.col_idx, f.l.values).apply(x)
+    scale = np.max(np.abs(zr))
+    monkeypatch.setenv("LG_IC0_MERGE", "0")
+    d0 = DeviceIc0(f.l)
+    assert d0.sweep_levels == (d0.levels, d0.levels) and d0.sweep_entries == 2 * (d0.nnz_l - a.n)
+    z0 = d0.apply(xd).cpu().numpy()
+    assert np.max(np.abs(z0 - zr)) <= 1e-12 * scale
+    prev = d0.sweep_levels
+    for passes in (1, 2, 3):
+        monkeypatch.setenv("LG_IC0_MERGE", str(passes))
+        d = DeviceIc0(f.l)
+        assert d.levels == d0.levels                      # the factor's own depth is reported unchanged
+        assert max(d.sweep_levels) < max(prev) and d.sweep_entries > d0.sweep_entries
+        prev = d.sweep_levels
+        z = d.apply(xd)
+        assert np.max(np.abs(z.cpu().numpy() - zr)) <= 1e-12 * scale
+        assert np.max(np.abs(z.cpu().numpy() - z0)) <= 1e-13 * scale
+        assert torch.equal(d.apply(xd), z)                # deterministic
+        y = xd.clone()
+        d.apply(y, y)                                     # z aliases r
+        assert torch.equal(y, z)
+        d.set_mode(1)                                     # resident sweep: same merged schedule, same bits
+        assert torch.equal(d.apply(xd), z)
+    monkeypatch.delenv("LG_IC0_MERGE")
+    fm = L.ic0_factorize_multicolor(a)
+    zm = fm.apply(x)
+    Pm = fm.perm
+    lm = fm.l
+    zmr = np.empty(a.n)
+    zmr[Pm] = O.Ic0(a.n, lm.row_ptr, lm.col_idx, lm.values).apply(x[Pm])
+    assert np.max(np.abs(zm - zmr)) <= 1e-12 * np.max(np.abs(zmr))
+
+
 @pytest.mark.parametrize("flags", [0, 1])
 def test_gather_probe_runs(L, flags):
     """lg_spmv_gather_probe (the bench's gather floor) walks the stored column
