@@ -253,6 +253,13 @@ int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels);
  * half the factor's depth for ~1.5x the entries; LG_IC0_MERGE=0 keeps the
  * plain sweeps. */
 int lg_ic0_sweep_depth(const lg_ic0* f, int* fwd, int* bwd, int64_t* entries);
+/* Host only (no device needed): one triangular solve -- L y = b, or L^T y = b
+ * when `backward` -- through the level-merged system the device would run
+ * after `passes` merging passes, in the system's topological order.  Test hook
+ * for the host transformation; depth / entries / unknowns describe the system. */
+int lg_ic0_merged_solve_host(int64_t n, const int64_t* l_row_ptr_h, const int64_t* l_col_h,
+                             const double* l_val_h, int passes, int backward, const double* b_h,
+                             double* y_h, int* depth, int64_t* entries, int64_t* unknowns);
 /* z = (L L^T)^{-1} r: sync-free forward sweep on L then backward sweep on
  * L^T, one cooperative persistent kernel each.  The forward result lives in
  * scratch owned by the handle, so applies of one handle must be ordered on

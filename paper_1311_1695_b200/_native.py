@@ -112,6 +112,8 @@ _SIGS = {
     "lg_ic0_apply": (c_int, [c_p, c_p, c_p, c_p, c_p]),
     "lg_ic0_set_mode": (c_int, [c_p, c_int]),
     "lg_ic0_sweep_depth": (c_int, [c_p, c_p, c_p, c_p]),
+    "lg_ic0_merged_solve_host": (c_int, [c_i64, c_p, c_p, c_p, c_int, c_int, c_p, c_p, c_p, c_p,
+                                         c_p]),
     "lg_ic0_trace": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_ic0_flow_trace": (c_int, [c_p, c_int, c_p, c_int]),
     "lg_ic0_schedule": (c_int, [c_p, c_int, c_p, c_int]),

@@ -1646,10 +1646,11 @@ static SweepLaunch& sweep_launch() {
 // omap (permuted factor, else NULL): factor row -> original row; the forward
 // sweep reads b there and the backward sweep writes z there.  The backward
 // sweep's right-hand side is the forward sweep's solution (factor numbering).
-static bool make_sweep(int64_t n, std::vector<int64_t>& rp, std::vector<int32_t>& col,
-                       std::vector<double>& val, const std::vector<double>& diag, bool forward,
-                       const int32_t* omap, SweepDev& d) {
-  SweepSys sys;
+// Host half of make_sweep: the sweep's system in its level-merged form, b
+// entries encoded as N + index.  flevels: depth of the factor's own DAG.
+static bool build_system(int64_t n, std::vector<int64_t>& rp, std::vector<int32_t>& col,
+                         std::vector<double>& val, const std::vector<double>& diag, bool forward,
+                         const int32_t* omap, int passes, SweepSys& sys, int* flevels) {
   sys.n = sys.N = n;
   sys.rp.swap(rp);
   sys.col.swap(col);
@@ -1665,9 +1666,10 @@ static bool make_sweep(int64_t n, std::vector<int64_t>& rp, std::vector<int32_t>
   }
   {
     std::vector<int32_t> lv;
-    d.flevels = dag_levels(sys, lv);
+    const int fl = dag_levels(sys, lv);
+    if (flevels) *flevels = fl;
   }
-  for (int p = 0; p < merge_passes() && 3 * sys.N < ((int64_t)1 << 31); ++p)
+  for (int p = 0; p < passes && 3 * sys.N < ((int64_t)1 << 31); ++p)
     if (!merge_levels(sys)) break;
   if (!getenv("LG_IC0_NOHUBSORT")) {
     // A hub row (> kHubChunk entries) is cut into chunk tasks whose partials
@@ -1704,6 +1706,25 @@ static bool make_sweep(int64_t n, std::vector<int64_t>& rp, std::vector<int32_t>
   // b entries: -1 - index  ->  N + index (entry_src on the device)
   for (int32_t& c : sys.col)
     if (c < 0) c = (int32_t)(sys.N + (-1 - (int64_t)c));
+  // every entry reads an unknown of this sweep or one of the n right-hand-side
+  // values, and every unknown has a nonzero pivot (the device trusts this)
+  bool valid = true;
+  for (const int32_t c : sys.col) valid = valid && c >= 0 && (int64_t)c < sys.N + n;
+  for (int64_t u = 0; u < sys.N; ++u)
+    valid = valid && sys.dg[(size_t)u] != 0.0 && sys.bidx[(size_t)u] < n && sys.oidx[(size_t)u] < n;
+  if (!valid) {
+    fprintf(stderr, "[lapb200] internal error: level-merged sweep system failed validation\n");
+    return false;
+  }
+  return true;
+}
+
+static bool make_sweep(int64_t n, std::vector<int64_t>& rp, std::vector<int32_t>& col,
+                       std::vector<double>& val, const std::vector<double>& diag, bool forward,
+                       const int32_t* omap, SweepDev& d) {
+  SweepSys sys;
+  if (!build_system(n, rp, col, val, diag, forward, omap, merge_passes(), sys, &d.flevels))
+    return false;
   SweepHost h;
   d.n = (int32_t)n;
   d.N = (int32_t)sys.N;
@@ -1953,7 +1974,6 @@ static int launch_cta_t(const CtaArgs& ca, cudaStream_t s) {
 
 static int launch_cta(const CtaArgs& ca, int threads, cudaStream_t s) {
   switch (threads) {
-    case 896: return launch_cta_t<28, 2>(ca, s);
     case 768: return launch_cta_t<24, 2>(ca, s);
     case 256: return launch_cta_t<8, 3>(ca, s);
     case 128: return launch_cta_t<4, 3>(ca, s);
@@ -1999,6 +2019,57 @@ static int launch_sweep(SweepArgs& args, cudaStream_t s) {
 }  // namespace lg
 
 using namespace lg;
+
+// Strictly lower part of L by rows, its transpose by rows, and the diagonal
+// (validated: lower triangular, sorted, the diagonal last in every row).
+static int split_factor(int64_t n, const int64_t* l_rp, const int64_t* l_col, const double* l_val,
+                        std::vector<int64_t>& frp, std::vector<int32_t>& fcol,
+                        std::vector<double>& fval, std::vector<int64_t>& brp,
+                        std::vector<int32_t>& bcol, std::vector<double>& bval,
+                        std::vector<double>& dg) {
+  // validate: lower triangular with the diagonal last in every row
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t lo = l_rp[i], hi = l_rp[i + 1];
+    if (hi <= lo || l_col[hi - 1] != i)
+      return fail(LG_EINVAL, "lg_ic0_create: every row needs its diagonal last");
+    for (int64_t k = lo; k < hi - 1; ++k)
+      if (l_col[k] < 0 || l_col[k] >= i || (k > lo && l_col[k] <= l_col[k - 1]))
+        return fail(LG_EINVAL, "lg_ic0_create: factor must be strictly lower, sorted");
+    if (!(l_val[hi - 1] != 0.0)) return fail(LG_EINVAL, "lg_ic0_create: zero pivot");
+  }
+  const int64_t nnz = n ? l_rp[n] : 0;
+  const int64_t noff = nnz - n;
+  frp.assign((size_t)n + 1, 0);
+  brp.assign((size_t)n + 1, 0);
+  fcol.assign((size_t)noff, 0);
+  bcol.assign((size_t)noff, 0);
+  fval.assign((size_t)noff, 0.0);
+  bval.assign((size_t)noff, 0.0);
+  dg.assign((size_t)n, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t lo = l_rp[i], hi = l_rp[i + 1] - 1;
+    frp[(size_t)i + 1] = frp[(size_t)i] + (hi - lo);
+    for (int64_t k = lo; k < hi; ++k) {
+      fcol[(size_t)(frp[(size_t)i] + k - lo)] = (int32_t)l_col[k];
+      fval[(size_t)(frp[(size_t)i] + k - lo)] = l_val[k];
+      brp[(size_t)l_col[k] + 1]++;
+    }
+    dg[(size_t)i] = l_val[hi];
+  }
+  for (int64_t i = 0; i < n; ++i) brp[(size_t)i + 1] += brp[(size_t)i];
+  {
+    // transpose: row j of L^T lists i > j in ascending i
+    std::vector<int64_t> fill(brp.begin(), brp.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t k = frp[(size_t)i]; k < frp[(size_t)i + 1]; ++k) {
+        int64_t j = fcol[(size_t)k];
+        bcol[(size_t)fill[(size_t)j]] = (int32_t)i;
+        bval[(size_t)fill[(size_t)j]] = fval[(size_t)k];
+        fill[(size_t)j]++;
+      }
+  }
+  return LG_OK;
+}
 
 extern "C" {
 
@@ -2088,43 +2159,14 @@ int lg_ic0_create_perm(int64_t n, const int64_t* l_rp, const int64_t* l_col,
   if (!out || n < 0 || !l_rp || (n > 0 && (!l_col || !l_val)))
     return fail(LG_EINVAL, "lg_ic0_create: bad argument");
   if (n >= ((int64_t)1 << 31)) return fail(LG_EINVAL, "lg_ic0_create: n too large");
-  // validate: lower triangular with the diagonal last in every row
-  for (int64_t i = 0; i < n; ++i) {
-    int64_t lo = l_rp[i], hi = l_rp[i + 1];
-    if (hi <= lo || l_col[hi - 1] != i)
-      return fail(LG_EINVAL, "lg_ic0_create: every row needs its diagonal last");
-    for (int64_t k = lo; k < hi - 1; ++k)
-      if (l_col[k] < 0 || l_col[k] >= i || (k > lo && l_col[k] <= l_col[k - 1]))
-        return fail(LG_EINVAL, "lg_ic0_create: factor must be strictly lower, sorted");
-    if (!(l_val[hi - 1] != 0.0)) return fail(LG_EINVAL, "lg_ic0_create: zero pivot");
+  std::vector<int64_t> frp, brp;
+  std::vector<int32_t> fcol, bcol;
+  std::vector<double> fval, bval, dg;
+  {
+    const int rc = split_factor(n, l_rp, l_col, l_val, frp, fcol, fval, brp, bcol, bval, dg);
+    if (rc) return rc;
   }
   const int64_t nnz = n ? l_rp[n] : 0;
-  const int64_t noff = nnz - n;
-  std::vector<int64_t> frp((size_t)n + 1, 0), brp((size_t)n + 1, 0);
-  std::vector<int32_t> fcol((size_t)noff), bcol((size_t)noff);
-  std::vector<double> fval((size_t)noff), bval((size_t)noff), dg((size_t)n);
-  for (int64_t i = 0; i < n; ++i) {
-    int64_t lo = l_rp[i], hi = l_rp[i + 1] - 1;
-    frp[(size_t)i + 1] = frp[(size_t)i] + (hi - lo);
-    for (int64_t k = lo; k < hi; ++k) {
-      fcol[(size_t)(frp[(size_t)i] + k - lo)] = (int32_t)l_col[k];
-      fval[(size_t)(frp[(size_t)i] + k - lo)] = l_val[k];
-      brp[(size_t)l_col[k] + 1]++;
-    }
-    dg[(size_t)i] = l_val[hi];
-  }
-  for (int64_t i = 0; i < n; ++i) brp[(size_t)i + 1] += brp[(size_t)i];
-  {
-    // transpose: row j of L^T lists i > j in ascending i
-    std::vector<int64_t> fill(brp.begin(), brp.end() - 1);
-    for (int64_t i = 0; i < n; ++i)
-      for (int64_t k = frp[(size_t)i]; k < frp[(size_t)i + 1]; ++k) {
-        int64_t j = fcol[(size_t)k];
-        bcol[(size_t)fill[(size_t)j]] = (int32_t)i;
-        bval[(size_t)fill[(size_t)j]] = fval[(size_t)k];
-        fill[(size_t)j]++;
-      }
-  }
   std::vector<int32_t> om;
   if (perm_h) {
     om.resize((size_t)n);
@@ -2346,6 +2388,44 @@ int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels) {
   if (n) *n = f->n;
   if (nnz_l) *nnz_l = f->nnz_l;
   if (levels) *levels = std::max(f->fwd.flevels, f->bwd.flevels);
+  return LG_OK;
+}
+
+// Host-only (no device): one triangular solve through the level-merged system
+// the device would run -- forward (L y = b) or backward (L^T y = b) -- in the
+// system's topological order.  Test hook for the host transformation: y must
+// equal the plain substitution to roundoff for any number of passes.
+int lg_ic0_merged_solve_host(int64_t n, const int64_t* l_rp, const int64_t* l_col,
+                             const double* l_val, int passes, int backward, const double* b,
+                             double* y, int* depth, int64_t* entries, int64_t* unknowns) {
+  if (n < 0 || !l_rp || (n > 0 && (!l_col || !l_val || !b || !y)))
+    return fail(LG_EINVAL, "lg_ic0_merged_solve_host: bad argument");
+  std::vector<int64_t> frp, brp;
+  std::vector<int32_t> fcol, bcol;
+  std::vector<double> fval, bval, dg;
+  const int rc = split_factor(n, l_rp, l_col, l_val, frp, fcol, fval, brp, bcol, bval, dg);
+  if (rc) return rc;
+  SweepSys sys;
+  const bool ok = backward ? build_system(n, brp, bcol, bval, dg, false, nullptr, passes, sys, nullptr)
+                           : build_system(n, frp, fcol, fval, dg, true, nullptr, passes, sys, nullptr);
+  if (!ok) return fail(LG_EINVAL, "lg_ic0_merged_solve_host: system failed validation");
+  std::vector<int32_t> lv;
+  const int dep = dag_levels(sys, lv);
+  std::vector<double> x((size_t)sys.N, 0.0);
+  for (int64_t q = 0; q < sys.N; ++q) {
+    const int32_t u = sys.order[(size_t)q];
+    double sum = 0.0;
+    for (int64_t k = sys.rp[(size_t)u]; k < sys.rp[(size_t)u + 1]; ++k) {
+      const int32_t c = sys.col[(size_t)k];
+      sum += sys.val[(size_t)k] * (c >= sys.N ? b[c - sys.N] : x[(size_t)c]);
+    }
+    const double bv = sys.bidx[(size_t)u] >= 0 ? b[sys.bidx[(size_t)u]] : 0.0;
+    x[(size_t)u] = (bv - sum) / sys.dg[(size_t)u];
+  }
+  for (int64_t i = 0; i < n; ++i) y[i] = x[(size_t)i];
+  if (depth) *depth = dep;
+  if (entries) *entries = (int64_t)sys.col.size();
+  if (unknowns) *unknowns = sys.N;
   return LG_OK;
 }
 

@@ -72,6 +72,56 @@ def test_host_ic0_factor_configs(cfg):
     assert h.hexdigest() == ref["ic0_sha256"]
 
 
+@pytest.mark.parametrize("name", ["P4", "grid4x5", "rand50", "rand200", "geo1000", "C1", "C2"])
+def test_level_merged_system_solves_like_the_factor(kat, name):
+    """Host half of the device IC(0) apply: the level-merged system (auxiliary
+    partial sums, the level below substituted, right-hand-side entries; any
+    number of passes) solved in its own topological order gives the plain
+    triangular solves of ic0.py:40-45 to roundoff, with a shallower DAG."""
+    import ctypes
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    from oracle import lapeig_oracle as O
+    from paper_1311_1695_b200 import _native as nat
+    from paper_1311_1695_b200.generators import config_graph
+    from paper_1311_1695_b200.ic0 import ic0_factorize
+    from paper_1311_1695_b200.sparse import CsrMatrix
+    if name.startswith("C"):
+        g = config_graph(name)
+        rp, col, val = O.build_laplacian(g.n_nodes, g.i, g.j, g.w)
+        a = CsrMatrix(g.n_nodes, rp, col, val, symmetric=True)
+    else:
+        graphs, arrays, _ = kat
+        a = CsrMatrix(int(graphs[name + "_n"][0]), arrays[name + "_rp"], arrays[name + "_col"],
+                      arrays[name + "_val"], symmetric=True)
+    l = ic0_factorize(a).l
+    n = l.n
+    lrp = np.ascontiguousarray(l.row_ptr, dtype=np.int64)
+    lcol = np.ascontiguousarray(l.col_idx, dtype=np.int64)
+    lval = np.ascontiguousarray(l.values, dtype=np.float64)
+    Lm = sp.csr_matrix((lval, lcol, lrp), shape=(n, n))
+    b = np.random.default_rng(7).standard_normal(n)
+    want = {0: spla.spsolve_triangular(Lm, b, lower=True),
+            1: spla.spsolve_triangular(Lm.T.tocsr(), b, lower=False)}
+    for backward in (0, 1):
+        depth0 = None
+        for passes in (0, 1, 2, 4):
+            y = np.empty(n)
+            dep, ent, unk = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+            nat.call("lg_ic0_merged_solve_host", n, lrp.ctypes.data, lcol.ctypes.data,
+                     lval.ctypes.data, passes, backward, b.ctypes.data, y.ctypes.data,
+                     ctypes.byref(dep), ctypes.byref(ent), ctypes.byref(unk))
+            ref = want[backward]
+            assert np.max(np.abs(y - ref)) <= 1e-12 * np.max(np.abs(ref)), (backward, passes)
+            if passes == 0:
+                depth0 = dep.value
+                assert ent.value == lrp[-1] - n and unk.value == n
+            else:
+                assert dep.value <= depth0 and unk.value >= n and ent.value >= lrp[-1] - n
+                if depth0 >= 8:
+                    assert dep.value < depth0                # a real chain gets shorter
+
+
 def test_ic0_shift_ladder_and_breakdown():
     from paper_1311_1695_b200.ic0 import Ic0Error, ic0_factorize
     from paper_1311_1695_b200.sparse import CsrMatrix
