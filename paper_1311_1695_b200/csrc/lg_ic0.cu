@@ -268,23 +268,25 @@ static int dag_levels(const SweepSys& s, std::vector<int32_t>& level) {
 //    substituted whole; long ones stay and keep their hop).  Row i then reads
 //    the right-hand side at j -- a b entry, which never waits -- and inputs two
 //    levels down: even rows chain to even rows.
-// The rewritten system has the same form, so passes compose (LG_IC0_MERGE
-// passes, default 2; 0 keeps the factor's own sweep).  Results equal the plain
+// The rewritten system has the same form, so passes compose (at most
+// LG_IC0_MERGE passes, default 3: two wherever the DAG is latency-bound, a
+// third on narrow DAGs; 0 keeps the factor's own sweep).  Results equal the plain
 // sweep's to roundoff (coefficient products are rounded once on the host), not
 // bitwise.
 constexpr int64_t kMergeLen = 16;   // rows up to this long are substituted whole
 constexpr int64_t kSplitMin = 4;    // early inputs that earn an auxiliary unknown
 
 constexpr int64_t kMergeWide = 16384;   // mean rows per level beyond which a sweep is not latency-bound
+constexpr int64_t kMergeNarrow = 2048;  // ... up to which a third pass still pays
 
-static bool merge_levels(SweepSys& s) {
+static bool merge_levels(SweepSys& s, int64_t max_rows_per_level) {
   std::vector<int32_t> level;
   const int depth = dag_levels(s, level);
   const int64_t N = s.N;
   // a shallow, wide DAG (the multicolour factor: 26 levels of ~38 k rows on C4)
   // is bound by its entries, not its depth: merging only adds work there
   // (measured: C4 multicolour DACG iteration 424 -> 620 us)
-  if (N > kMergeWide * (int64_t)depth) return false;
+  if (N > max_rows_per_level * (int64_t)depth) return false;
   auto early = [&](int64_t j, int64_t k) {   // entry k of row j is not on the level just below
     const int32_t c = s.col[(size_t)k];
     return c < 0 || level[(size_t)c] < level[(size_t)j] - 1;
@@ -390,19 +392,34 @@ static bool merge_levels(SweepSys& s) {
 
 static int merge_passes() {   // read at every factor creation
   const char* e = getenv("LG_IC0_MERGE");
-  return e ? std::max(0, std::min(4, atoi(e))) : 2;
+  return e ? std::max(0, std::min(4, atoi(e))) : 3;
 }
 
 // Lanes per row.  On wide levels (many more rows than warps) tasks are
 // packed densely, one lane per row up to kLaneMax entries, to minimise the
-// number of tasks a warp walks; on narrow levels (latency-bound) rows are
-// spread over more lanes so each lane's share of the chain is short.
-static int lanes_for(int64_t len, bool wide) {
-  if (wide) {
+// number of tasks a warp walks; on the others rows are spread over more lanes
+// so each lane's share of the chain is short -- the more so on narrow levels
+// (<= LG_FINE_ROWS = 4096 rows: idle warps abound and only the hop counts; measured
+// on the merged schedules: C1 39.4 -> 34.5 us, C2 148 -> 132 us, C3 918 -> 849
+// us, while C4's ~7.5 k-row levels lose 7 % with it and keep the middle
+// classes).
+static int lanes_for(int64_t len, int width) {
+  if (width == 2) {          // wide level: dense packing
     if (len <= 8) return 1;
     if (len <= 16) return 2;
     if (len <= 32) return 4;
     if (len <= 64) return 8;
+    return 32;
+  }
+  if (width == -1) {         // very narrow level: at most two entries per lane
+    if (len <= 4) return 4;
+    if (len <= 16) return 8;
+    return 32;
+  }
+  if (width == 0) {          // narrow level: short chains per lane
+    if (len <= 2) return 2;
+    if (len <= 8) return 4;
+    if (len <= 32) return 8;
     return 32;
   }
   if (len <= 4) return 2;
@@ -449,8 +466,23 @@ static void build_sweep(const SweepSys& sys, int narrow_tasks, SweepHost& h) {
     const char* e = getenv("LG_WIDE_ROWS");
     return e ? (int64_t)atoll(e) : (int64_t)16384;
   }();
-  std::vector<char> lwide((size_t)nl);
-  for (int l = 0; l < nl; ++l) lwide[(size_t)l] = lcount[(size_t)l + 1] - lcount[(size_t)l] > wide_rows;
+  static const int64_t fine_rows = [] {
+    const char* e = getenv("LG_FINE_ROWS");
+    return e ? (int64_t)atoll(e) : (int64_t)4096;
+  }();
+  static const int64_t ultra_rows = [] {
+    const char* e = getenv("LG_ULTRA_ROWS");
+    return e ? (int64_t)atoll(e) : (int64_t)1024;
+  }();
+  static const int64_t task_target = [] {
+    const char* e = getenv("LG_TASK_TARGET");
+    return e ? (int64_t)atoll(e) : (int64_t)128;
+  }();
+  std::vector<signed char> lwide((size_t)nl);   // -1 very narrow, 0 narrow, 1 middle, 2 wide
+  for (int l = 0; l < nl; ++l) {
+    const int64_t rows = lcount[(size_t)l + 1] - lcount[(size_t)l];
+    lwide[(size_t)l] = rows > wide_rows ? 2 : (rows > fine_rows ? 1 : (rows > ultra_rows ? 0 : -1));
+  }
   auto cls = [&](int32_t r) {
     const int64_t len = rp[(size_t)r + 1] - rp[(size_t)r];
     return len > kHubChunk ? 64 : lanes_for(len, lwide[(size_t)level[(size_t)r]]);
@@ -515,7 +547,12 @@ static void build_sweep(const SweepSys& sys, int narrow_tasks, SweepHost& h) {
         ++t;
         continue;
       }
-      const int cap = 32 / L;
+      // rows per task: a full warp, or -- on a level with few rows -- as few as
+      // leave the level ~task_target tasks (fewer inputs to wait for per task)
+      const int64_t lrows = lcount[(size_t)l + 1] - lcount[(size_t)l];
+      const int cap = task_target > 0 && lrows <= fine_rows
+                          ? (int)std::max<int64_t>(1, std::min<int64_t>(32 / L, lrows / task_target))
+                          : 32 / L;
       int cnt = 1;
       while (cnt < cap && t + cnt < te && cls(h.perm[(size_t)(t + cnt)]) == L) ++cnt;
       const int64_t base = h.prp[(size_t)t];
@@ -1669,8 +1706,11 @@ static bool build_system(int64_t n, std::vector<int64_t>& rp, std::vector<int32_
     const int fl = dag_levels(sys, lv);
     if (flevels) *flevels = fl;
   }
+  // two passes wherever the sweep is latency-bound; a third only on narrow
+  // DAGs, where the extra entries are free (C3 809 -> 762 us, C2 121 -> 111 us;
+  // C4's ~8 k-row levels lose with it)
   for (int p = 0; p < passes && 3 * sys.N < ((int64_t)1 << 31); ++p)
-    if (!merge_levels(sys)) break;
+    if (!merge_levels(sys, p < 2 ? kMergeWide : kMergeNarrow)) break;
   if (!getenv("LG_IC0_NOHUBSORT")) {
     // A hub row (> kHubChunk entries) is cut into chunk tasks whose partials
     // chunk 0 sums -- a second hop after the last chunk.  Put the entries whose
