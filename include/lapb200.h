@@ -250,8 +250,8 @@ int lg_ic0_info(const lg_ic0* f, int64_t* n, int64_t* nnz_l, int* levels);
 /* Depth of the two sweeps as scheduled and the entries they stream: the
  * device applies a level-merged form of the factor (rows of even levels have
  * the level below substituted in, reading the right-hand side there), about
- * half the factor's depth for ~1.5x the entries; LG_IC0_MERGE=0 keeps the
- * plain sweeps. */
+ * 0.6x the factor's depth for ~1.5x the entries; LG_IC0_MERGE caps the number
+ * of merging passes (default 3), 0 keeps the plain sweeps. */
 int lg_ic0_sweep_depth(const lg_ic0* f, int* fwd, int* bwd, int64_t* entries);
 /* Host only (no device needed): one triangular solve -- L y = b, or L^T y = b
  * when `backward` -- through the level-merged system the device would run
