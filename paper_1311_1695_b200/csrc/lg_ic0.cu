@@ -969,6 +969,7 @@ constexpr unsigned long long kSentinel = ~0ull;
 // merged C4: 577 -> 551 us; C1-C3 lose 2-4 % with it)
 constexpr int kFlowThreads = 384;
 constexpr int kFlowThreadsWide = 512;
+constexpr int kFlowThreadsSm = 768;   // entries staged through shared memory: 23 worker warps
 constexpr int kFlowWideTasks = 512;   // mean tasks per level from which the wide CTA is used
 
 struct FlowArgs {
@@ -1069,8 +1070,35 @@ __device__ __forceinline__ void fstage1(const A& a, int64_t t, int lane, FStage1
   s.lev = a.tlevel[t];
 }
 
-template <class A>
-__device__ __forceinline__ void fstage2(const A& a, const FStage1& s, int lane, FStaged& st) {
+// Entries staged through shared memory (SM = true, opt-in LG_FLOW_WIDE=2):
+// the lane's columns and values go from global into its own slots with
+// cp.async -- no registers and no scoreboard wait -- so the kernel fits 23
+// worker warps per SM instead of 15 (80 registers); slot of entry e of stage
+// g: [(g * kLaneMax + e) * 32 + lane].  Same bits; not faster (launch_flow).
+__device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst_smem)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst_smem)),
+               "l"(src)
+               : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <bool SM = false, class A>
+__device__ __forceinline__ void fstage2(const A& a, const FStage1& s, int lane, FStaged& st,
+                                        int32_t* sc = nullptr, double* sv = nullptr) {
   const SweepTask tk = s.tk;
   st.info = tk.b;
   st.lev = s.lev;
@@ -1101,8 +1129,13 @@ __device__ __forceinline__ void fstage2(const A& a, const FStage1& s, int lane, 
   for (int e = 0; e < kLaneMax; ++e) {
     if (e < st.ne) {
       const int64_t k = lo + ((int64_t)e << st.sh);
-      st.col[e] = a.pcol[k];
-      st.val[e] = a.pval[k];
+      if constexpr (SM) {
+        cp_async4(sc + e * 32, a.pcol + k);
+        cp_async8(sv + e * 32, a.pval + k);
+      } else {
+        st.col[e] = a.pcol[k];
+        st.val[e] = a.pval[k];
+      }
     }
   }
 }
@@ -1117,8 +1150,19 @@ __device__ __forceinline__ void publish(const FlowArgs& a, int32_t oi, const Row
     a.next_x[ri.xrow] = __longlong_as_double((long long)kSentinel);
 }
 
+template <bool SM = false>
 __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& st, int lane,
-                                              unsigned long long* tr) {
+                                              unsigned long long* tr, const int32_t* sc = nullptr,
+                                              const double* sv = nullptr) {
+  // entry e's column / value: the staged registers, or the lane's shared-memory slots
+  auto COL = [&](int e) -> int32_t {
+    if constexpr (SM) return sc[e * 32];
+    else return st.col[e];
+  };
+  auto VAL = [&](int e) -> double {
+    if constexpr (SM) return sv[e * 32];
+    else return st.val[e];
+  };
   const bool owner = st.info != 0 ? (st.p >= 0 && (lane & ((1 << st.sh) - 1)) == 0)
                                   : (st.c == 0 && lane == 0);
   double bv = 0.0;
@@ -1128,8 +1172,8 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
 #pragma unroll
   for (int e = 0; e < kLaneMax; ++e) {
     if (e < st.ne) {
-      xv[e] = ld_relaxed_f64(entry_src(a.x, a.b, a.n, st.col[e]));
-      if (st.col[e] < a.n && is_sentinel(xv[e])) miss |= 1u << e;   // b entries never wait
+      xv[e] = ld_relaxed_f64(entry_src(a.x, a.b, a.n, COL(e)));
+      if (COL(e) < a.n && is_sentinel(xv[e])) miss |= 1u << e;   // b entries never wait
     }
   }
   unsigned spins = 0, nap = 16;
@@ -1146,7 +1190,7 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
 #pragma unroll
     for (int e = 0; e < kLaneMax; ++e) {
       if (probe & (1u << e)) {
-        xv[e] = ld_relaxed_f64(a.x + st.col[e]);
+        xv[e] = ld_relaxed_f64(a.x + COL(e));
         if (!is_sentinel(xv[e])) {
           miss &= ~(1u << e);
           if (e == fe) got = true;
@@ -1163,13 +1207,13 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
     __nanosleep(LG_FLOW_POLL2);
 #pragma unroll
     for (int e = 0; e < kLaneMax; ++e)
-      if (miss & (1u << e)) xb[e] = ld_relaxed_f64(a.x + st.col[e]);
+      if (miss & (1u << e)) xb[e] = ld_relaxed_f64(a.x + COL(e));
     while (true) {
 #pragma unroll
       for (int e = 0; e < kLaneMax; ++e)
         if (miss & (1u << e)) {
           if (!is_sentinel(xv[e])) miss &= ~(1u << e);
-          else xv[e] = ld_relaxed_f64(a.x + st.col[e]);
+          else xv[e] = ld_relaxed_f64(a.x + COL(e));
         }
       if (!__any_sync(0xffffffffu, miss != 0)) break;
 #pragma unroll
@@ -1179,7 +1223,7 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
             xv[e] = xb[e];
             miss &= ~(1u << e);
           } else {
-            xb[e] = ld_relaxed_f64(a.x + st.col[e]);
+            xb[e] = ld_relaxed_f64(a.x + COL(e));
           }
         }
       if (!__any_sync(0xffffffffu, miss != 0)) break;
@@ -1194,7 +1238,7 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
 #pragma unroll
     for (int e = 0; e < kLaneMax; ++e) {
       if (miss & (1u << e)) {
-        xv[e] = ld_relaxed_f64(a.x + st.col[e]);
+        xv[e] = ld_relaxed_f64(a.x + COL(e));
         if (!is_sentinel(xv[e])) miss &= ~(1u << e);
       }
     }
@@ -1204,7 +1248,7 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
   double s = 0.0;
 #pragma unroll
   for (int e = 0; e < kLaneMax; ++e)
-    if (e < st.ne) s += st.val[e] * xv[e];
+    if (e < st.ne) s += VAL(e) * xv[e];
   if (st.info != 0) {
     for (int o = (1 << st.sh) >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
 #ifdef LG_FLOW_RCP
@@ -1240,11 +1284,20 @@ __device__ __forceinline__ void flow_complete(const FlowArgs& a, const FStaged& 
   if (lane == 0) publish(a, st.oi, st.ri, (bv - t) / st.ri.dg);
 }
 
-template <int kFlowThreads>
+template <int kFlowThreads, bool SM = false>
 __global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a) {
   if (a.skip && *a.skip) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWorkers = kFlowThreads / 32 - 1;
+  // SM: per worker warp two stages of lane-private entry slots (columns, values)
+  extern __shared__ __align__(16) unsigned char flow_smem[];
+  int32_t* sc_base = nullptr;
+  double* sv_base = nullptr;
+  if constexpr (SM) {
+    sv_base = reinterpret_cast<double*>(flow_smem) + (size_t)(warp - 1) * 2 * kLaneMax * 32 + lane;
+    sc_base = reinterpret_cast<int32_t*>(flow_smem + (size_t)kWorkers * 2 * kLaneMax * 32 * 8) +
+              (size_t)(warp - 1) * 2 * kLaneMax * 32 + lane;
+  }
   __shared__ volatile int s_done;
   __shared__ volatile int s_active;
   if (threadIdx.x == 0) {
@@ -1285,27 +1338,34 @@ __global__ void __launch_bounds__(kFlowThreads, 1) sweep_flow_kernel(FlowArgs a)
   if (t < nt) {
     FStaged st, stn;
     FStage1 s1n;
+    int g = 0;   // SM: stage holding the current task's entries
     {
       FStage1 s1;
       fstage1(a, t, lane, s1);
-      fstage2(a, s1, lane, st);
+      fstage2<SM>(a, s1, lane, st, sc_base, sv_base);
+      if constexpr (SM) cp_async_commit();
     }
     if (t + W < nt) fstage1(a, t + W, lane, s1n);
     for (; t < nt; t += W) {
       FStage1 s1nn;
       if (t + 2 * W < nt) fstage1(a, t + 2 * W, lane, s1nn);
-      if (t + W < nt) fstage2(a, s1n, lane, stn);
+      if (t + W < nt)
+        fstage2<SM>(a, s1n, lane, stn, sc_base + (g ^ 1) * kLaneMax * 32,
+                    sv_base + (g ^ 1) * kLaneMax * 32);
+      if constexpr (SM) cp_async_commit();   // one group per step, empty or not
       for (unsigned spins = 0; s_done < st.lev - gate; ++spins) {
         __nanosleep(32);
         if (spins > (1u << 24)) __trap();
       }
       unsigned long long* tr = a.ttrace ? a.ttrace + 3 * t : nullptr;
       if (tr && lane == 0) tr[0] = gtimer();
-      flow_complete(a, st, lane, tr);
+      if constexpr (SM) cp_async_wait<1>();   // the current task's entries have landed
+      flow_complete<SM>(a, st, lane, tr, sc_base + g * kLaneMax * 32, sv_base + g * kLaneMax * 32);
       if (tr && lane == 0) tr[2] = gtimer();
       if (lane == 0) red_relaxed_add(a.lcount + st.lev * 32 + (t & 31), 1u);
       st = stn;
       s1n = s1nn;
+      g ^= 1;
     }
   }
   __syncwarp();
@@ -1396,13 +1456,6 @@ __device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
                    (uint32_t)__cvta_generic_to_shared(dst_smem)),
                "l"(src)
                : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long gtimer_after(double dep) {
@@ -1909,13 +1962,23 @@ static int sweep_gate() {
   return g;
 }
 
-template <int THREADS>
+template <int THREADS, bool SM>
+static size_t flow_smem() {
+  return SM ? (size_t)(THREADS / 32 - 1) * 2 * kLaneMax * 32 * 12 : 0;
+}
+
+template <int THREADS, bool SM>
 static int flow_grid() {
   static int grid = 0;
   if (!grid) {
+    if (SM)
+      cudaFuncSetAttribute(sweep_flow_kernel<THREADS, SM>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)flow_smem<THREADS, SM>());
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_flow_kernel<THREADS>, THREADS,
-                                                      0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sweep_flow_kernel<THREADS, SM>,
+                                                      THREADS, flow_smem<THREADS, SM>()) !=
+            cudaSuccess ||
         occ < 1)
       occ = 1;
     grid = std::min(occ, 1) * dev_info().sm_count;
@@ -1923,10 +1986,25 @@ static int flow_grid() {
   return grid;
 }
 
+template <int THREADS, bool SM>
+static int launch_flow_t(const FlowArgs& a, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(flow_grid<THREADS, SM>());
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = flow_smem<THREADS, SM>();
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;   // all warps co-resident
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_flow_kernel<THREADS, SM>, a));
+  return LG_OK;
+}
+
 static int launch_flow(const SweepDev& dv, const SweepDev& other, const double* b, double* x,
                        double* out2, double* next_x, const int* skip, cudaStream_t s) {
   const bool wide = (int64_t)dv.ntasks > (int64_t)kFlowWideTasks * std::max(1, dv.levels);
-  const int grid = wide ? flow_grid<kFlowThreadsWide>() : flow_grid<kFlowThreads>();
   FlowArgs a;
   a.pcol = dv.pcol;
   a.pval = dv.pval;
@@ -1962,18 +2040,17 @@ static int launch_flow(const SweepDev& dv, const SweepDev& other, const double* 
     const char* e = getenv("LG_SWEEP_BACKOFF");
     a.backoff = e ? (uint32_t)std::max(16, atoi(e)) : 16u;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(wide ? kFlowThreadsWide : kFlowThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;   // all warps co-resident
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  if (wide) LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_flow_kernel<kFlowThreadsWide>, a));
-  else LG_CUDA(cudaLaunchKernelEx(&cfg, sweep_flow_kernel<kFlowThreads>, a));
-  return LG_OK;
+  // LG_FLOW_WIDE: 0 narrow CTA everywhere, 1 (default) the register-staged wide
+  // CTA, 2 the shared-memory-staged one (23 worker warps) -- measured on the
+  // merged C4 schedule: 560 / 534 / 552 us: beyond 15 warps the extra resident
+  // tasks only add pollers
+  static const int wide_kind = [] {
+    const char* e = getenv("LG_FLOW_WIDE");
+    return e ? atoi(e) : 1;
+  }();
+  if (wide && wide_kind == 2) return launch_flow_t<kFlowThreadsSm, true>(a, s);
+  if (wide && wide_kind == 1) return launch_flow_t<kFlowThreadsWide, false>(a, s);
+  return launch_flow_t<kFlowThreads, false>(a, s);
 }
 
 static CtaDir cta_dir(const SweepDev& dv, const double* b, double* x, double* out2) {
