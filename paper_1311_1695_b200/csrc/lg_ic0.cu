@@ -10,23 +10,25 @@
 //
 // Apply: ic0.py:40-45 solves L y = r then L^T z = y (SuperLU, natural
 // ordering).  On the GPU each triangular sweep is a dependency DAG: 227
-// levels on C4, 476 on C3, 72 on C2.  A launch per level costs ~2 us x
-// levels and per-row ready flags with spinning lanes saturate L2 with polls
-// (measured: 8 ms per C4 apply), so each sweep is ONE cooperative persistent
-// kernel that walks the levels in order:
-//   * a level's rows are packed into warp tasks -- 32/L rows of one length
-//     class (L = 2, 4, 8 or 32 lanes per row), or a 512-nonzero chunk of a
-//     hub row (C4's largest lower row has 84,860 entries); a hub row's
-//     chunks publish partials and the last chunk to arrive (ticket) sums
-//     them in chunk order, so the result stays deterministic;
-//   * a "wide" level is spread over every warp of the grid and closed by a
-//     grid barrier (one atomic per CTA on a monotonic 64-bit counter);
-//   * a run of "narrow" levels (no more tasks than one CTA has warps) is
-//     executed by CTA 0 alone with __syncthreads between levels -- ~50 ns
-//     instead of a ~1 us grid barrier -- while the other CTAs wait at the
-//     next grid barrier.
-// Per-row summation order is fixed (lane-strided, butterfly), so z is
-// bitwise reproducible.
+// levels on C4, 476 on C3, 72 on C2; its time is depth x dependency hop, not
+// bytes.  What this file does about it, in order of appearance:
+//   * host: the sweep's system is rewritten into a level-merged form
+//     (merge_levels: auxiliary partial sums + the level below substituted in;
+//     ~0.6x the depth for ~1.5x the entries, exact in real arithmetic), hub
+//     rows get their deepest inputs first, and the rows are permuted into
+//     processing order and packed into warp tasks -- 32/L rows of one length
+//     class (L = 1 ... 32 lanes per row, chosen per level width), or a
+//     256-entry chunk of a hub row whose partials chunk 0 sums in chunk order;
+//   * device, default: the dataflow sweep (sweep_flow_kernel) -- no barriers,
+//     the solution vector is its own dependency flag, one cooperative
+//     persistent launch per triangle;
+//   * device, kept for comparison / tracing (LG_SWEEP_MODE=0, lg_ic0_trace):
+//     the level-barrier sweep (sweep_kernel: grid barriers after wide levels,
+//     runs of narrow levels on one cluster);
+//   * device, opt-in (LG_SWEEP_CTA=1): the resident sweep (sweep_cta_kernel:
+//     both triangles in one CTA).
+// All three run the same schedule with the same per-row summation order
+// (lane-strided, butterfly), so they agree bit for bit and z is reproducible.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
