@@ -261,8 +261,9 @@ static int dag_levels(const SweepSys& s, std::vector<int32_t>& level) {
 // DAG for ~20 % more entries).  A sweep's time is its DAG depth times the
 // dependency hop (~1.6 us), not its bytes, and on power-law graphs the long
 // chains run through hub rows.  Two rewrites, both exact in real arithmetic:
-//  * split: an odd-level unknown j with at least kSplitMin inputs below the
-//    level just under it gets an auxiliary unknown p_j = sum of those early
+//  * split: an odd-level unknown j with at least kSplitMin (12: measured best
+//    of 2 ... 32; fewer auxiliary rows than at 4, C4 539 -> 515 us) inputs below
+//    the level just under it gets an auxiliary unknown p_j = sum of those early
 //    terms (ready a level sooner); row j keeps p_j and its late inputs.
 //  * substitute: in a row i of an even level every input j on the level just
 //    below is replaced by j's own equation, a_ij y_j = c b_j - c p_j -
@@ -275,8 +276,14 @@ static int dag_levels(const SweepSys& s, std::vector<int32_t>& level) {
 // third on narrow DAGs; 0 keeps the factor's own sweep).  Results equal the plain
 // sweep's to roundoff (coefficient products are rounded once on the host), not
 // bitwise.
-constexpr int64_t kMergeLen = 16;   // rows up to this long are substituted whole
-constexpr int64_t kSplitMin = 4;    // early inputs that earn an auxiliary unknown
+static int64_t env_i64(const char* name, int64_t dflt) {
+  const char* e = getenv(name);
+  return e ? (int64_t)atoll(e) : dflt;
+}
+// rows up to kMergeLen entries are substituted whole; kSplitMin early inputs
+// earn an auxiliary unknown (LG_IC0_MERGELEN / LG_IC0_SPLITMIN override)
+static int64_t merge_len() { return env_i64("LG_IC0_MERGELEN", 16); }
+static int64_t split_min() { return env_i64("LG_IC0_SPLITMIN", 12); }
 
 constexpr int64_t kMergeWide = 16384;   // mean rows per level beyond which a sweep is not latency-bound
 constexpr int64_t kMergeNarrow = 2048;  // ... up to which a third pass still pays
@@ -285,6 +292,7 @@ static bool merge_levels(SweepSys& s, int64_t max_rows_per_level) {
   std::vector<int32_t> level;
   const int depth = dag_levels(s, level);
   const int64_t N = s.N;
+  const int64_t kMergeLen = merge_len(), kSplitMin = split_min();
   // a shallow, wide DAG (the multicolour factor: 26 levels of ~38 k rows on C4)
   // is bound by its entries, not its depth: merging only adds work there
   // (measured: C4 multicolour DACG iteration 424 -> 620 us)
