@@ -65,9 +65,43 @@ class ClockSampler:
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        self.source = "nvidia-smi"
+        # in-process NVML when available: a query takes tens of microseconds, so
+        # a timed region of a few milliseconds still gets several samples taken
+        # while it runs (an nvidia-smi process takes ~50 ms to come back)
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._nvml = pynvml
+            self.source = "nvml"
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        n = self._nvml
+        sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)
+        get = getattr(n, "nvmlDeviceGetCurrentClocksEventReasons", None) or getattr(
+            n, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        bits = int(get(self._h))
+        # NVML reason bits: HwSlowdown 0x8, HwThermalSlowdown 0x40,
+        # SwThermalSlowdown 0x20, SwPowerCap 0x4
+        flags = ["Active" if bits & b else "Not Active" for b in (0x8, 0x40, 0x20, 0x4)]
+        return [str(sm), str(mx)] + flags
 
     def _run(self):
         while not self._stop.is_set():
+            if self._nvml is not None:
+                try:
+                    self.rows.append(self._sample_nvml())
+                except Exception:
+                    self._nvml = None
+                    self.source = "nvidia-smi"
+                    continue
+                self._stop.wait(0.0005)
+                continue
             try:
                 out = subprocess.run(
                     ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -98,7 +132,7 @@ class ClockSampler:
                           if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "source": self.source}
 
 
 def build_graph(config):
