@@ -113,6 +113,11 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        # the timed loop is a busy Python thread: shorten the interpreter's
+        # thread switch interval so the sampler gets to run while it does
+        # (kernels are timed by CUDA events; the host loop only enqueues)
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(2e-4)
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
@@ -121,6 +126,7 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        sys.setswitchinterval(self._switch)
 
     def summary(self):
         if not self.rows:
